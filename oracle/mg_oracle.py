@@ -1,0 +1,551 @@
+"""ORACLE — plain, slow, CPU reference of the adaptive FAS V-cycle (test infrastructure).
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+``--impl reference``) may import or execute this module.  The CUDA product path
+(paper_2512_08555_b200) never imports it and shares no code with it: the only
+common module is `workloads` (seeded inputs, no method arithmetic).
+
+Representation (independent of the GPU's block layout): every multigrid level k
+is a dense lattice N_k^3 (index J = (Jx, Jy, Jz), node at origin + J h_k) with a
+boolean mask of the nodes that lie in level-k blocks.  Values are looked up
+through ``lookup``: stored value inside level-k blocks (periodic
+images by wrap), coarse-to-fine interpolation (c2f) from W_{k-1} at resolution
+jumps / exterior nodes, or the last coarse-solve band at the coarsest level.
+Extended arrays carry a pad of width E on every axis.  NaN marks "undefined";
+a NaN reaching a result means a value outside the method's footprint was used.
+
+Paper passages (PAPER.md line numbers, P:n):
+* Alg. 1 adaptive FAS V(η1,η2)-cycle ............................ P:137-168
+* residual r = f - ∇²u ........................................... P:152
+* full-weighting restriction ¼[1 2 1] (E6) ....................... P:230-235
+* injection of u (E7) ............................................ P:236-241
+* block-wise trilinear prolongation ............................... P:228
+* smoother: "an iteration of the Gauss-Seidel method" ............ P:227
+* 2nd-order cross stencil (E8, E9) ............................... P:252-262
+* Mehrstellen Δ_h^M u = R_h^M f, f* = R_h^M f stored once (E10-E12) P:343-354
+* ghost interpolation order M+2 (polynomial) ..................... P:63
+* coarse FFT direct solve, LGF kernels, Spietz 2-unbounded (E14) .. P:67-100
+* zero-average of the coarse solution for periodic problems ...... P:455
+* ∞-norm residual convergence / Cauchy criterion (E20) ........... P:170
+Readings of silent/garbled passages are listed in DESIGN.md §Readings (Z-codes
+from SURVEY.md §8(c)); the ones used here are cited inline.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import lgf as LGF
+
+PERIODIC, UNBOUNDED = 0, 1
+JACOBI, RBGS = 0, 1
+E = 6          # pad width of extended arrays
+GE = 5         # exterior band width computed by the coarse solve (reading Z21/U1)
+
+
+# ----------------------------------------------------------------------------------
+# 1D rules
+# ----------------------------------------------------------------------------------
+def lagrange_midpoint_weights(I: int) -> np.ndarray:
+    """Weights of the I-point centred Lagrange interpolant at the midpoint between
+    nodes 0 and 1; nodes t = -I/2+1 … I/2 (reading Z7: fixed-weight, always centred)."""
+    t = np.arange(-I // 2 + 1, I // 2 + 1, dtype=np.float64)
+    w = np.empty(I)
+    for a in range(I):
+        p = 1.0
+        for b in range(I):
+            if b != a:
+                p *= (0.5 - t[b]) / (t[a] - t[b])
+        w[a] = p
+    return w
+
+
+def _shift(A, ax, s):
+    """A shifted along axis ax by s (out[i] = A[i+s]); NaN where out of range."""
+    out = np.full_like(A, np.nan)
+    n = A.shape[ax]
+    src = [slice(None)] * A.ndim
+    dst = [slice(None)] * A.ndim
+    if s >= 0:
+        src[ax] = slice(s, n)
+        dst[ax] = slice(0, n - s)
+    else:
+        src[ax] = slice(0, n + s)
+        dst[ax] = slice(-s, n)
+    out[tuple(dst)] = A[tuple(src)]
+    return out
+
+
+def d2(A, ax):
+    """Dimensionless second difference δ² = [1 -2 1] along ax (E9);
+    NaN on the two end planes where the stencil leaves the array."""
+    out = np.full_like(A, np.nan)
+    c = [slice(None)] * A.ndim
+    m = [slice(None)] * A.ndim
+    p = [slice(None)] * A.ndim
+    c[ax], m[ax], p[ax] = slice(1, -1), slice(0, -2), slice(2, None)
+    c, m, p = tuple(c), tuple(m), tuple(p)
+    out[c] = A[m] - 2.0 * A[c] + A[p]
+    return out
+
+
+def apply_L(X, h, order):
+    """Δ_h^M on an extended array (E8 for M=2, E12 for M=4, E13 for M=6)."""
+    D = [d2(X, a) for a in range(3)]
+    s = D[0] + D[1] + D[2]
+    if order >= 4:
+        s = s + (d2(D[0], 1) + d2(D[1], 2) + d2(D[2], 0)) / 6.0
+    if order == 6:
+        s = s + d2(d2(D[0], 1), 2) / 30.0
+    return s / (h * h)
+
+
+def apply_R(X, order):
+    """R_h^M f: identity (M=2); f + (1/12)Σδ²f (M=4, right side of E12).
+    M=6 (E13 with the δ²_yδ²_z reading Z24): + (1/90)Σδ²δ² - (1/240)Σδ⁴."""
+    if order == 2:
+        return X.copy()
+    D = [d2(X, a) for a in range(3)]
+    s = X + (D[0] + D[1] + D[2]) / 12.0
+    if order == 6:
+        s = s + (d2(D[0], 1) + d2(D[1], 2) + d2(D[2], 0)) / 90.0
+        s = s - (d2(D[0], 0) + d2(D[1], 1) + d2(D[2], 2)) / 240.0
+    return s
+
+
+def diag_L(h, order):
+    """Centre coefficient of Δ_h^M (fig:stencils P:272-328): -6/h², -24/(6h²), -128/(30h²)."""
+    return {2: -6.0, 4: -24.0 / 6.0, 6: -128.0 / 30.0}[order] / (h * h)
+
+
+def symbol(order, thetas, h):
+    """σ_M(θ): eigenvalue of Δ_h^M on e^{iθ·J}; δ² → ŝ = 2cosθ - 2 (P:398 'Fourier symbol')."""
+    lams = [2.0 * np.cos(t) - 2.0 for t in thetas]
+    return LGF.lattice_symbol_poly(lams, order) / (h * h)
+
+
+# ----------------------------------------------------------------------------------
+# Hierarchy
+# ----------------------------------------------------------------------------------
+class Level:
+    pass
+
+
+class Oracle:
+    """Dense-lattice oracle of the whole solver state.
+
+    desc keys: origin, h0, base_blocks, B, bc (per axis), order, smoother, omega,
+    eta1, eta2, coarse_n (0 = AMR level 0 is coarsest), leaves[n,4].
+    """
+
+    def __init__(self, desc, leaves):
+        self.order = int(desc["order"])
+        self.I = self.order + 2                       # interpolation order M+2
+        self.w_c2f = lagrange_midpoint_weights(self.I)
+        self.smoother = int(desc["smoother"])
+        self.omega = float(desc["omega"])
+        self.eta1, self.eta2 = int(desc["eta1"]), int(desc["eta2"])
+        self.B = int(desc["B"])
+        self.bc = tuple(int(b) for b in desc["bc"])
+        self.per = tuple(b == PERIODIC for b in self.bc)
+        self.origin = np.asarray(desc["origin"], dtype=np.float64)
+        self.leaves = np.asarray(leaves, dtype=np.int64)
+        base = np.asarray(desc["base_blocks"], dtype=np.int64)
+        N0 = base * self.B
+        amr_max = int(self.leaves[:, 0].max())
+        coarse_n = int(desc.get("coarse_n", 0) or 0)
+        nsub = 0
+        if coarse_n:
+            nsub = int(round(math.log2(N0[0] / coarse_n)))
+            if not np.all(N0 >> nsub << nsub == N0) or N0[0] >> nsub != coarse_n:
+                raise ValueError("coarse_n must be N0 / 2^j on every axis")
+        self.nsub = nsub
+        self.levels = []
+        # MG level m: m < nsub -> sub-base uniform level; m = nsub + a -> AMR level a
+        for m in range(nsub + amr_max + 1):
+            L = Level()
+            a = m - nsub
+            L.amr = a
+            L.N = (N0 >> (-a)) if a < 0 else (N0 << a)
+            L.h = float(desc["h0"]) * (2.0 ** (-a))
+            L.mask = np.zeros(tuple(L.N), dtype=bool)
+            self.levels.append(L)
+        # masks: AMR level a holds leaves at a and ancestors of deeper leaves
+        for lev, bi, bj, bk in self.leaves.tolist():
+            c = np.array([bi, bj, bk])
+            for a in range(lev, -1, -1):
+                Lv = self.levels[nsub + a]
+                s = c * self.B
+                Lv.mask[s[0]:s[0] + self.B, s[1]:s[1] + self.B, s[2]:s[2] + self.B] = True
+                c = c // 2
+        for m in range(nsub):
+            self.levels[m].mask[...] = True
+        for m, L in enumerate(self.levels):
+            if m + 1 < len(self.levels):
+                fm = self.levels[m + 1].mask
+                L.cov = fm[::2, ::2, ::2].copy()      # coarse i covered iff fine 2i in a level-(m+1) block
+            else:
+                L.cov = np.zeros(tuple(L.N), dtype=bool)
+            L.cov &= L.mask
+            L.leaf = L.mask & ~L.cov
+            n = tuple(L.N)
+            L.u = np.zeros(n)
+            L.f = np.zeros(n)
+            L.r = np.zeros(n)
+            L.uhat = np.zeros(n)
+            L.mask_ext = self._pad(L.mask.astype(np.float64), fill=0.0) > 0.5
+            L.parity_ext = self._parity_ext(L)
+        c = self.levels[0]
+        if not c.mask.all():
+            raise ValueError("coarsest level must cover the domain")
+        c.band = np.zeros(tuple(c.N + 2 * E))        # exterior values of the last coarse solve
+        self.fstar_norm = None
+        self._coarse_setup()
+
+    # --------------------------------------------------------------- extended arrays
+    def _pad(self, A, fill=np.nan):
+        """Extend an interior array by E on every axis: periodic axes by wrap,
+        unbounded axes with `fill` (exterior)."""
+        X = A
+        for ax in range(3):
+            if self.per[ax]:
+                n = X.shape[ax]
+                X = np.take(X, np.arange(-E, n + E) % n, axis=ax)
+            else:
+                shp = list(X.shape)
+                shp[ax] = E
+                Z = np.full(shp, fill)
+                X = np.concatenate([Z, X, Z], axis=ax)
+        return X
+
+    def _parity_ext(self, L):
+        idx = [np.arange(-E, n + E) for n in L.N]
+        J = np.meshgrid(*idx, indexing="ij")
+        return ((J[0] + J[1] + J[2]) % 2 == 0)
+
+    def _interior(self, X, L):
+        return X[E:E + L.N[0], E:E + L.N[1], E:E + L.N[2]]
+
+    def _exterior_ext(self, L):
+        """True at extended positions outside an unbounded face."""
+        ext = np.zeros(tuple(L.N + 2 * E), dtype=bool)
+        for ax in range(3):
+            if not self.per[ax]:
+                sl = [slice(None)] * 3
+                sl[ax] = slice(0, E)
+                ext[tuple(sl)] = True
+                sl[ax] = slice(E + L.N[ax], None)
+                ext[tuple(sl)] = True
+        return ext
+
+    # --------------------------------------------------------------- c2f (a1-iii)
+    def _c2f_axis(self, W, ax, nf):
+        """Refine W (extended coarse, along ax) to the extended fine lattice of
+        nf interior nodes: fine J even -> coarse J/2; J odd -> centred I-point
+        Lagrange midpoint rule on coarse (J-1)/2 - I/2 + 1 … (J-1)/2 + I/2."""
+        Wm = np.moveaxis(W, ax, 0)
+        nce = Wm.shape[0]
+        out = np.full((nf + 2 * E,) + Wm.shape[1:], np.nan)
+        I = self.I
+        # E is even, so extended position p = J + E has the parity of J.
+        # even J = 2q -> coarse extended index q + E/2 ... written per position set:
+        pe = np.arange(0, nf + 2 * E, 2)                 # J even
+        qe = (pe - E) // 2 + E
+        ok = (qe >= 0) & (qe < nce)
+        out[pe[ok]] = Wm[qe[ok]]
+        po = np.arange(1, nf + 2 * E, 2)                 # J odd
+        base = (po - E - 1) // 2 - I // 2 + 1 + E
+        ok = (base >= 0) & (base + I - 1 < nce)
+        po, base = po[ok], base[ok]
+        acc = np.zeros((len(po),) + Wm.shape[1:])
+        for t in range(I):
+            acc += self.w_c2f[t] * Wm[base + t]
+        out[po] = acc
+        return np.moveaxis(out, 0, ax)
+
+    def c2f(self, W, Lf):
+        """Tensor product of the 1D rule (reading Z7: tensor product at edges/corners)."""
+        X = W
+        for ax in range(3):
+            X = self._c2f_axis(X, ax, int(Lf.N[ax]))
+        return X
+
+    # --------------------------------------------------------------- value lookup (O2)
+    def lookup(self, m, vals, exterior="band"):
+        """Extended level-m array of V_m(J): stored values in level-m blocks,
+        ghosts from c2f of W_{m-1} (jump and exterior nodes, m >= 1), the last
+        coarse-solve band (m = 0, exterior='band') or 0 (exterior='zero', for f)."""
+        L = self.levels[m]
+        A = self._pad(vals[m])
+        if L.mask_ext.all():
+            return A                                  # no ghost nodes on this level
+        if m == 0:
+            G = np.full(tuple(L.N + 2 * E), np.nan)
+            ext = self._exterior_ext(L)
+            if exterior == "band":
+                G[ext] = L.band[ext]
+            else:
+                G[ext] = 0.0
+        else:
+            G = self.c2f(self.source_W(m - 1, vals, exterior), L)
+            if exterior == "zero":
+                G[self._exterior_ext(L)] = 0.0       # f := 0 beyond unbounded faces (Z16)
+        return np.where(L.mask_ext, A, G)
+
+    def source_W(self, m, vals, exterior):
+        """W_m: level-m values with every node coinciding with a level-(m+1) block
+        node replaced by the fine value (f2c injection, reading Z8), plus exterior
+        values; NaN at level-m jump-ghost positions (c2f never reads them, Z7)."""
+        L = self.levels[m]
+        fine = vals[m + 1]
+        Am = vals[m].copy()
+        Am[L.cov] = fine[::2, ::2, ::2][L.cov]
+        X = np.where(L.mask_ext, self._pad(Am), np.nan)
+        ext = self._exterior_ext(L)
+        if ext.any():
+            v2 = list(vals)
+            v2[m] = Am
+            Y = self.lookup(m, v2, exterior)          # exterior values (band / c2f / 0)
+            X[ext] = Y[ext]
+        return X
+
+    def uvals(self):
+        return [L.u for L in self.levels]
+
+    # --------------------------------------------------------------- operators
+    def Lu(self, m, vals=None):
+        """Δ_h^M u at level m using current ghosts (interior lattice)."""
+        vals = self.uvals() if vals is None else vals
+        X = self.lookup(m, vals)
+        return self._interior(apply_L(X, self.levels[m].h, self.order), self.levels[m])
+
+    def residual(self, m):
+        """r_m = f_m - Δ u_m on level-m block nodes (Alg. 1 line P:152)."""
+        L = self.levels[m]
+        return np.where(L.mask, L.f - self.Lu(m), 0.0)
+
+    def smooth(self, m):
+        """One smoothing sweep on all level-m block nodes; boundary ghosts refreshed
+        before the sweep and frozen during it (reading Z9).  Jacobi:
+        u += ω(f - Δu)/d.  RB (reading Z10): red = even (Jx+Jy+Jz) first, each
+        colour updated from a snapshot (Jacobi within colour)."""
+        L = self.levels[m]
+        vals = self.uvals()
+        X = self.lookup(m, vals)
+        d = diag_L(L.h, self.order)
+        if self.smoother == JACOBI:
+            Lx = apply_L(X, L.h, self.order)
+            U = X + self.omega * (self._pad(L.f, 0.0) - Lx) / d
+            L.u = np.where(L.mask, self._interior(U, L), L.u)
+            return
+        ghosts = np.where(L.mask_ext, np.nan, X)      # frozen boundary ghosts
+        Fext = self._pad(L.f, 0.0)
+        for colour in (True, False):
+            Lx = apply_L(X, L.h, self.order)
+            U = X + self.omega * (Fext - Lx) / d
+            sel = L.mask_ext & (L.parity_ext == colour)
+            Unew = np.where(sel, U, X)
+            # re-impose periodic images of the updated interior, keep frozen ghosts
+            newu = self._interior(Unew, L)
+            L.u = np.where(L.mask, newu, L.u)
+            X = np.where(L.mask_ext, self._pad(L.u), ghosts)
+
+    def restrict(self, m):
+        """Alg. 1: on the Ω_m-covered nodes of level m-1
+        u_{m-1} <- Î u_m (E7), r_{m-1} <- I r_m (E6, r := 0 outside level m, reading Z14),
+        then f_{m-1} <- r_{m-1} + Δ u_{m-1} (after the level-(m-1) refresh);
+        finally û_{m-1} <- u_{m-1} on every level-(m-1) node (reading Z13-W)."""
+        L, C = self.levels[m], self.levels[m - 1]
+        r = self.residual(m)
+        C.u = np.where(C.cov, L.u[::2, ::2, ::2], C.u)
+        R = self._pad(np.where(L.mask, r, 0.0), fill=0.0)
+        for ax in range(3):
+            R = 0.25 * _shift(R, ax, -1) + 0.5 * R + 0.25 * _shift(R, ax, 1)
+        Rint = self._interior(R, L)[::2, ::2, ::2]
+        C.r = np.where(C.cov, Rint, 0.0)
+        Lc = self.Lu(m - 1)
+        C.f = np.where(C.cov, C.r + Lc, C.f)
+        C.uhat = np.where(C.mask, C.u, 0.0)
+
+    def prolong(self, m):
+        """u_m += I ε_{m-1}, ε = u - û on level-(m-1) nodes (correction sign: reading
+        Z12; whole-level snapshot: reading Z13-W); I = trilinear (Alg. 1):
+        per axis, fine J even -> coarse J/2, J odd -> mean of (J-1)/2 and (J+1)/2."""
+        L, C = self.levels[m], self.levels[m - 1]
+        eps = np.where(C.mask, C.u - C.uhat, 0.0)
+        X = self._pad(eps, fill=0.0)
+        for ax in range(3):
+            Xm = np.moveaxis(X, ax, 0)
+            nce = Xm.shape[0]
+            nf = int(L.N[ax])
+            out = np.full((nf + 2 * E,) + Xm.shape[1:], np.nan)
+            pe = np.arange(0, nf + 2 * E, 2)
+            qe = (pe - E) // 2 + E
+            ok = (qe >= 0) & (qe < nce)
+            out[pe[ok]] = Xm[qe[ok]]
+            po = np.arange(1, nf + 2 * E, 2)
+            qo = (po - E - 1) // 2 + E
+            ok = (qo >= 0) & (qo + 1 < nce)
+            out[po[ok]] = 0.5 * (Xm[qo[ok]] + Xm[qo[ok] + 1])
+            X = np.moveaxis(out, 0, ax)
+        L.u = np.where(L.mask, L.u + self._interior(X, L), L.u)
+
+    def inject_up(self):
+        """u_{m-1}[covered] <- u_m(2i), finest to coarsest (E7; canonical state)."""
+        for m in range(len(self.levels) - 1, 0, -1):
+            L, C = self.levels[m], self.levels[m - 1]
+            C.u = np.where(C.cov, L.u[::2, ::2, ::2], C.u)
+
+    # --------------------------------------------------------------- coarse solve (a6)
+    def _coarse_setup(self):
+        c = self.levels[0]
+        N = [int(n) for n in c.N]
+        self.unb = [ax for ax in range(3) if not self.per[ax]]
+        if len(self.unb) == 0:
+            self.coarse_kind = "PPP"
+            return
+        shape = [N[ax] if self.per[ax] else LGF.pad_size(N[ax], GE) for ax in range(3)]
+        self.coarse_shape = shape
+        if len(self.unb) == 3:
+            self.coarse_kind = "UUU"
+            R = LGF.box_radius(max(shape))
+            G = LGF.box_lgf(3, self.order, R)
+            T = LGF.wrapped_table(G, R, shape)
+            self.coarse_mult = np.fft.fftn(T).real * c.h * c.h
+        elif len(self.unb) == 2 and self.per[0]:
+            self.coarse_kind = "PUU"
+            R = LGF.box_radius(max(shape[1:]))
+            G2 = LGF.box_lgf(2, self.order, R)
+            T2 = LGF.wrapped_table(G2, R, shape[1:])
+            K = np.empty(shape)
+            th = [2 * np.pi * np.fft.fftfreq(s) for s in shape]
+            TH = np.meshgrid(*th, indexing="ij")
+            sig = symbol(self.order, TH, c.h)
+            sig[0] = 1.0
+            K[...] = 1.0 / sig
+            K[0] = np.fft.fft2(T2).real * c.h * c.h      # E14: k_per = 0 -> 2D LGF
+            self.coarse_mult = K
+        else:
+            raise NotImplementedError("boundary combination not supported by the oracle")
+
+    def coarse_solve(self):
+        """u_0 <- S_0 f_0 (Alg. 1).  PPP: F^-1[F f / σ_M], zero mode -> 0
+        (zero average).  Unbounded: zero-padded convolution with the LGF
+        of Δ_h^M, computed on [-GE, N+GE) for the exterior band."""
+        c = self.levels[0]
+        N = [int(n) for n in c.N]
+        if self.coarse_kind == "PPP":
+            F = np.fft.fftn(c.f)
+            th = [2 * np.pi * np.fft.fftfreq(n) for n in N]
+            TH = np.meshgrid(*th, indexing="ij")
+            sig = symbol(self.order, TH, c.h)
+            sig[0, 0, 0] = 1.0
+            U = F / sig
+            U[0, 0, 0] = 0.0
+            c.u = np.fft.ifftn(U).real
+            return
+        shape = self.coarse_shape
+        Fp = np.zeros(shape)
+        Fp[:N[0], :N[1], :N[2]] = c.f
+        U = np.fft.ifftn(np.fft.fftn(Fp) * self.coarse_mult).real
+        c.u = U[:N[0], :N[1], :N[2]].copy()
+        # exterior band: outputs at J in [-GE, N+GE) along unbounded axes
+        band = np.full(tuple(c.N + 2 * E), np.nan)
+        idx = []
+        for ax in range(3):
+            if self.per[ax]:
+                idx.append(np.arange(-E, N[ax] + E) % N[ax])
+            else:
+                J = np.arange(-E, N[ax] + E)
+                ok = (J >= -GE) & (J < N[ax] + GE)
+                idx.append(np.where(ok, J % shape[ax], -1))
+        sub = U[np.ix_(*[np.where(i < 0, 0, i) for i in idx])]
+        valid = np.ones(band.shape, dtype=bool)
+        for ax in range(3):
+            sh = [1, 1, 1]
+            sh[ax] = -1
+            valid &= (idx[ax] >= 0).reshape(sh)
+        band[valid] = sub[valid]
+        c.band = band
+
+    # --------------------------------------------------------------- API-level ops
+    def set_rhs(self, f_leaves):
+        """O5: place f on leaf nodes, inject up the tree (f2c), f* = R_h^M f on
+        leaves via the lookup with f := 0 beyond unbounded faces (Z16)."""
+        B = self.B
+        fraw = [np.zeros(tuple(L.N)) for L in self.levels]
+        for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
+            L = fraw[self.nsub + lev]
+            L[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B] = \
+                np.asarray(f_leaves[n]).transpose(2, 1, 0)
+        for m in range(len(self.levels) - 1, 0, -1):
+            C = self.levels[m - 1]
+            fraw[m - 1] = np.where(C.cov, fraw[m][::2, ::2, ::2], fraw[m - 1])
+        for m, L in enumerate(self.levels):
+            X = self.lookup(m, fraw, exterior="zero")
+            fs = self._interior(apply_R(X, self.order), L)
+            L.f = np.where(L.leaf, fs, fraw[m])
+        self.fstar_norm = max(float(np.abs(L.f[L.leaf]).max()) if L.leaf.any() else 0.0
+                              for L in self.levels)
+
+    def set_solution(self, u_leaves):
+        B = self.B
+        for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
+            L = self.levels[self.nsub + lev]
+            L.u[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B] = \
+                np.asarray(u_leaves[n]).transpose(2, 1, 0)
+        self.inject_up()
+
+    def get_solution(self):
+        B = self.B
+        out = np.empty((len(self.leaves), B, B, B))
+        for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
+            L = self.levels[self.nsub + lev]
+            out[n] = L.u[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B].transpose(2, 1, 0)
+        return out
+
+    def vcycle(self, n=1):
+        """Alg. 1 with readings Z9-Z15, then inject-up."""
+        top = len(self.levels) - 1
+        for _ in range(n):
+            for m in range(top, 0, -1):
+                for _ in range(self.eta1):
+                    self.smooth(m)
+                self.restrict(m)
+            self.coarse_solve()
+            for m in range(1, top + 1):
+                self.prolong(m)
+                for _ in range(self.eta2):
+                    self.smooth(m)
+            self.inject_up()
+
+    def residual_norm(self):
+        """a9: max over leaf nodes of all levels of |f - Δu|, and relative to ‖f*‖∞."""
+        mx = 0.0
+        for m, L in enumerate(self.levels):
+            if not L.leaf.any():
+                continue
+            r = L.f - self.Lu(m)
+            mx = max(mx, float(np.abs(r[L.leaf]).max()))
+        rel = mx / self.fstar_norm if self.fstar_norm else mx
+        return mx, rel
+
+    def solve(self, tol, max_cycles=50, criterion="residual"):
+        """Cycle until rel. residual <= tol (configs) or the Cauchy criterion E20."""
+        hist = []
+        prev = None
+        for c in range(1, max_cycles + 1):
+            if criterion == "cauchy":
+                prev = self.get_solution()
+            self.vcycle(1)
+            a, r = self.residual_norm()
+            if criterion == "cauchy":
+                cur = self.get_solution()
+                num = np.abs(cur - prev).max()
+                den = np.abs(cur).max()
+                r = num / den if den > 0 else num
+            hist.append(r)
+            if r <= tol:
+                return c, hist
+        return max_cycles, hist

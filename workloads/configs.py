@@ -1,0 +1,117 @@
+"""The five BASELINE.json configurations (+ reduced-size variants for tests).
+
+A config is a plain dict; `build(cfg)` returns (Domain, leaves[n,4], f[n,B,B,B]).
+Recipes are stated in DESIGN.md §Inputs; seeds are fixed here.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import sources as S
+from .layouts import (PERIODIC, UNBOUNDED, Domain, bisect_tau, block_node_coords,
+                      uniform_leaves)
+
+RBGS = 1
+JACOBI = 0
+
+
+def cfg1():
+    """Uniform periodic 32^3 (8 blocks of 16^3), f = sin sin sin, M=2, Jacobi 2/3,
+    V(3,3) to a 4^3 coarse level, 10 V-cycles (BASELINE configs[0])."""
+    return dict(name="cfg1", origin=(0.0, 0.0, 0.0), h0=1 / 32, base_blocks=(2, 2, 2), B=16,
+                bc=(PERIODIC,) * 3, order=2, smoother=JACOBI, omega=2 / 3, eta1=3, eta2=3,
+                coarse_n=4, max_level=0, source="sines", cycles=10, tol=0.0)
+
+
+def cfg2(N=256, seed=2):
+    """Uniform periodic N^3, M=4 Mehrstellen, RB V(2,2), 64 seeded Fourier modes
+    |k|<=8, mean removed, to rel. residual 1e-10 (BASELINE configs[1])."""
+    return dict(name="cfg2" if N == 256 else f"cfg2_N{N}", origin=(0.0, 0.0, 0.0), h0=1 / N,
+                base_blocks=(N // 16,) * 3, B=16, bc=(PERIODIC,) * 3, order=4, smoother=RBGS,
+                omega=1.0, eta1=2, eta2=2, coarse_n=min(32, N // 2), max_level=0,
+                source="fourier", seed=seed, cycles=0, tol=1e-10)
+
+
+def cfg3(N=256, coarse_n=32):
+    """Fully unbounded N^3 on [-1,1)^3, M=4, Gaussian sigma=0.08 unit charge at the
+    origin, RB V(2,2), coarse level by zero-padded LGF convolution (configs[2])."""
+    return dict(name="cfg3" if N == 256 else f"cfg3_N{N}", origin=(-1.0, -1.0, -1.0), h0=2 / N,
+                base_blocks=(N // 16,) * 3, B=16, bc=(UNBOUNDED,) * 3, order=4, smoother=RBGS,
+                omega=1.0, eta1=2, eta2=2, coarse_n=coarse_n, max_level=0, source="gaussian",
+                cycles=0, tol=1e-10, allow_unbounded_refined=1)
+
+
+def cfg4(base=8, max_level=2, target=2000):
+    """Adaptive 3-level grid (~2000 leaf blocks) around 3 seeded Gaussian blobs, x
+    periodic, y/z unbounded, M=4, RB V(2,2), to 1e-10 (configs[3])."""
+    return dict(name="cfg4" if base == 8 else f"cfg4_b{base}", origin=(0.0, 0.0, 0.0),
+                h0=1 / (16 * base), base_blocks=(base,) * 3, B=16,
+                bc=(PERIODIC, UNBOUNDED, UNBOUNDED), order=4, smoother=RBGS, omega=1.0,
+                eta1=2, eta2=2, coarse_n=0, max_level=max_level, source="blobs", seed=4,
+                target_leaves=target, cycles=0, tol=1e-10)
+
+
+def cfg5(base=8, max_level=4, target=30000):
+    """Adaptive 5-level grid (~30k leaf blocks) around a perturbed torus, x periodic,
+    y/z unbounded on [-1,1)^3, M=4, RB V(2,2), to 1e-10 (configs[4])."""
+    return dict(name="cfg5" if base == 8 else f"cfg5_b{base}", origin=(-1.0, -1.0, -1.0),
+                h0=2 / (16 * base), base_blocks=(base,) * 3, B=16,
+                bc=(PERIODIC, UNBOUNDED, UNBOUNDED), order=4, smoother=RBGS, omega=1.0,
+                eta1=2, eta2=2, coarse_n=0, max_level=max_level, source="torus", seed=5,
+                target_leaves=target, cycles=0, tol=1e-10)
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+
+
+def domain(cfg) -> Domain:
+    return Domain(origin=tuple(cfg["origin"]), h0=cfg["h0"], base_blocks=tuple(cfg["base_blocks"]),
+                  B=cfg["B"], bc=tuple(cfg["bc"]))
+
+
+def source_fn(cfg):
+    s = cfg["source"]
+    if s == "sines":
+        return S.sines
+    if s == "gaussian":
+        return S.gaussian_charge
+    if s == "blobs":
+        p = S.blobs(cfg.get("seed", 4))
+        L = cfg["h0"] * cfg["B"] * cfg["base_blocks"][0]
+        return lambda x, y, z: S.blobs_eval(p, x, y, z, Lx=L)
+    if s == "torus":
+        p = S.torus_params(cfg.get("seed", 5))
+        return lambda x, y, z: S.torus_eval(p, x, y, z)
+    raise KeyError(s)
+
+
+def leaves_for(cfg) -> np.ndarray:
+    dom = domain(cfg)
+    if cfg["max_level"] == 0:
+        return uniform_leaves(dom, 0)
+    fn = source_fn(cfg)
+
+    def score(lev, coords):
+        out = np.empty(len(coords))
+        for s in range(0, len(coords), 256):
+            x, y, z = block_node_coords(dom, lev, coords[s:s + 256])
+            v = fn(x[:, None, None, :], y[:, None, :, None], z[:, :, None, None])
+            out[s:s + 256] = np.abs(v).reshape(len(x), -1).max(axis=1) * dom.h(lev) ** 2
+        return out
+
+    tau, n, leaves = bisect_tau(dom, cfg["max_level"], score, cfg["target_leaves"])
+    cfg["tau"] = tau
+    return leaves
+
+
+def build(cfg):
+    """Return (Domain, leaves, f) for a config; f sampled at leaf nodes [n,B,B,B]."""
+    dom = domain(cfg)
+    leaves = leaves_for(cfg)
+    if cfg["source"] == "fourier":
+        N = cfg["base_blocks"][0] * cfg["B"]
+        dense = S.fourier_dense(N, S.fourier_modes(cfg.get("seed", 2)))
+        f = S.dense_to_blocks(dom, leaves, dense)
+    else:
+        f = S.sample_on_leaves(dom, leaves, source_fn(cfg))
+    return dom, leaves, f
