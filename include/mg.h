@@ -1,0 +1,144 @@
+/*
+ * mg.h — C-ABI of the B200-native adaptive multigrid Poisson solver (libmg.so).
+ *
+ * Solves the Poisson equation ∇²u = f (PAPER.md E1) in 3D on a
+ * block-structured, collocated (node-centred) multiresolution grid (§2.1,
+ * P:58-65) with per-axis periodic or unbounded directions (§2.2), by
+ * the adaptive FAS V(η1,η2)-cycle of Alg. 1, the compact
+ * Mehrstellen stencils Δ_h^M u = R_h^M f (E10-E12; M = 2 uses the
+ * cross stencil E8), full-weighting restriction (E6),
+ * injection (E7), trilinear prolongation, ghost
+ * interpolation of order M+2 at resolution jumps, and an FFT /
+ * lattice-Green's-function direct solve of the coarsest level (P:67-100,
+ * P:245; the 2-unbounded kernel is E14).
+ *
+ * Conventions (all entry points):
+ *  - Return value: MG_OK (0) on success, a negative MG_ERR_* on error, a
+ *    positive MG_WARN_* warning (the call did its work).  No C++ exception
+ *    crosses the ABI.  mg_last_error() gives a message for the last failure.
+ *  - Device pointers (suffix _dev) are CUDA device addresses of fp64 arrays the
+ *    CALLER owns (e.g. torch tensors); the library never keeps them after the
+ *    call returns.  Host pointers (suffix _host or plain const int32_t*) are
+ *    ordinary host memory, also caller-owned and not retained.
+ *  - Field layout on leaves: [n_leaf][B][B][B], x fastest, i.e. element
+ *    (leaf n, node (ix,iy,iz)) is at n*B^3 + (iz*B + iy)*B + ix; leaves in the
+ *    order given to mg_create.  Leaf (level, bi, bj, bk) owns the level-global
+ *    nodes J = B*(bi,bj,bk) + [0,B)^3, at x = origin + J * h0 / 2^level.
+ *  - A handle is bound to one CUDA stream (the one given to mg_create); every
+ *    call enqueues work on that stream.  Calls that return host scalars
+ *    (mg_residual_norm, mg_solve) synchronise that stream.  Handles are not
+ *    thread-safe.
+ *  - Only fp64.  There is no CPU fallback: without a CUDA device every call
+ *    that needs one returns MG_ERR_CUDA.
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mg_handle mg_handle;
+
+/* boundary conditions, per face (-x,+x,-y,+y,-z,+z); both faces of an axis must match */
+enum { MG_BC_PERIODIC = 0, MG_BC_UNBOUNDED = 1, MG_BC_EVEN = 2, MG_BC_ODD = 3 /* reserved */ };
+/* smoother ("an iteration of the Gauss-Seidel method"; readings Z10) */
+enum { MG_SMOOTHER_JACOBI = 0, MG_SMOOTHER_RBGS = 1 };
+/* stopping criterion of mg_solve: relative ∞-norm residual or Cauchy (E20) */
+enum { MG_CRIT_RESIDUAL = 0, MG_CRIT_CAUCHY = 1 };
+
+enum {
+  MG_OK = 0,
+  MG_WARN_NOT_CONVERGED = 1,     /* mg_solve hit max_cycles; the partial solution is kept */
+  MG_ERR_ARG = -1,               /* null pointer, bad size or enum */
+  MG_ERR_LAYOUT_NESTING = -2,    /* leaves overlap, partial refinement, level 0 not covered */
+  MG_ERR_LAYOUT_2TO1 = -3,       /* 26-neighbour 2:1 constraint violated */
+  MG_ERR_UNBOUNDED_REFINED = -4, /* refined block touches an unbounded face */
+  MG_ERR_BC = -5,                /* unpaired periodic faces or EVEN/ODD requested */
+  MG_ERR_ORDER = -6,             /* order not in {2,4} */
+  MG_ERR_STATE = -7,             /* e.g. mg_vcycle before mg_set_rhs */
+  MG_ERR_CUDA = -8,              /* CUDA / cuFFT failure or no device */
+  MG_ERR_OOM = -9,               /* device allocation failed */
+  MG_ERR_NONFINITE = -10,        /* NaN/Inf met in a norm */
+  MG_ERR_LAYOUT_GHOST = -11      /* a ghost interpolation stencil leaves the coarse level */
+};
+
+typedef struct mg_desc {
+  double origin[3];          /* physical position of level-global node 0 */
+  double h0;                 /* grid spacing of AMR level 0 (isotropic) */
+  int32_t base_blocks[3];    /* level-0 blocks per axis */
+  int32_t block_size;        /* B: nodes per block edge; 16 (also 8) */
+  int32_t bc[6];             /* per face, MG_BC_* */
+  int32_t order;             /* M = 2 (cross stencil E8) or 4 (Mehrstellen E12) */
+  int32_t coarse_n;          /* nodes along x of the coarsest MG level (uniform sub-base
+                                coarsening N0/2^j, reading Z5); 0 = AMR level 0 is coarsest */
+  int32_t smoother;          /* MG_SMOOTHER_* */
+  double omega;              /* relaxation factor (Jacobi ω; RB uses it too, 1 = Gauss-Seidel) */
+  int32_t eta1, eta2;        /* pre-/post-smoothing sweeps */
+  int32_t allow_unbounded_refined; /* accept refined levels touching unbounded faces (reading U1) */
+  int64_t n_leaf;            /* number of leaf blocks */
+  const int32_t* leaves;     /* host array [n_leaf][4] = (level, bi, bj, bk) */
+} mg_desc;
+
+/* Validate the layout (nesting, 2:1, unbounded-face rule), build the level
+ * hierarchy, ghost/transfer tables and coarse-solve kernels, allocate device
+ * memory.  `cuda_stream` is a cudaStream_t (NULL = legacy default stream).
+ * On success *out owns everything; release with mg_destroy. */
+int mg_create(const mg_desc* d, void* cuda_stream, mg_handle** out);
+void mg_destroy(mg_handle* h);
+/* Thread-local message of the last failing call (never NULL). */
+const char* mg_last_error(const mg_handle* h);
+
+/* f on the leaves (device, leaf layout).  Injects f up the tree, fills its ghosts
+ * (f := 0 beyond unbounded faces), stores f* = R_h^M f on leaf nodes and
+ * ‖f*‖∞.  Resets u to 0 (Alg. 1 initial solution, reading Z28). */
+int mg_set_rhs(mg_handle* h, const double* f_dev);
+/* Initial guess / read-back of u on the leaves (device, leaf layout). */
+int mg_set_solution(mg_handle* h, const double* u_dev);
+int mg_get_solution(mg_handle* h, double* u_dev);
+/* n V(η1,η2)-cycles in place (Alg. 1), asynchronous on the handle's stream. */
+int mg_vcycle(mg_handle* h, int n);
+/* Composite residual max|f* - Δ_h^M u| over leaf nodes of all levels, and that
+ * divided by ‖f*‖∞.  Synchronises.  Does not change the solution. */
+int mg_residual_norm(mg_handle* h, double* abs_inf, double* rel_inf);
+/* Cycle until the criterion value <= tol or max_cycles (MG_WARN_NOT_CONVERGED). */
+int mg_solve(mg_handle* h, double tol, int max_cycles, int criterion,
+             int* cycles_out, double* value_out);
+/* End-to-end call on HOST buffers: copies f_host (leaf layout) to the device,
+ * mg_set_rhs, runs `ncycles` V-cycles, copies u back into u_host, returns the
+ * relative residual.  Buffers are caller-owned host memory (pinned is faster). */
+int mg_run_host(mg_handle* h, const double* f_host, double* u_host, int ncycles, double* rel_out);
+/* Capture each V-cycle as one CUDA graph (1) or launch kernels directly (0). */
+int mg_use_graph(mg_handle* h, int enable);
+
+/* ---- introspection / debug (tests and benchmarks) ---- */
+enum { MG_INFO_NLEVELS = 0 };
+/* info[0..9] = B, n_real, n_ghost, N[3], amr_level, n_c2f, n_inject, n_leaf_blocks */
+int mg_level_info(mg_handle* h, int level, int64_t* info);
+/* host int32[n_real][3]: block coordinates of the level's real blocks (storage order) */
+int mg_level_blocks(mg_handle* h, int level, int32_t* coords_host);
+int mg_num_levels(mg_handle* h);
+
+enum { MG_FIELD_U = 0, MG_FIELD_F = 1, MG_FIELD_R = 2, MG_FIELD_UHAT = 3 };
+/* dir 0: export the level's real blocks [n_real][B^3] into dev; 1: import from dev */
+int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev);
+enum {
+  MG_OP_REFRESH = 0,        /* ghost fill of `level` (f2c injection + c2f / band) */
+  MG_OP_SMOOTH = 1,         /* refresh + one smoothing sweep */
+  MG_OP_RESIDUAL = 2,       /* refresh + r = f - Δu on all level nodes */
+  MG_OP_RESTRICT = 3,       /* level -> level-1: residual, inject u, FW r, FAS rhs, û */
+  MG_OP_PROLONG = 4,        /* u_level += P(u - û)_{level-1} */
+  MG_OP_INJECT_UP = 5,      /* canonicalise: u_{k-1}[covered] <- u_k, all levels */
+  MG_OP_COARSE_SOLVE = 6,   /* direct solve of the coarsest level */
+  MG_OP_SMOOTH_RESIDUAL = 7 /* fused last pre-sweep + residual (ghost-free levels) */
+};
+int mg_debug_apply(mg_handle* h, int op, int level);
+/* Time one operator: runs it `reps` times between CUDA events, returns ms per rep. */
+int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MG_H */

@@ -1,0 +1,1082 @@
+// mg_host.cpp — host runtime and C-ABI of the B200 adaptive multigrid solver.
+//
+// Builds the multigrid level hierarchy from a leaf list (§2.1, P:58-65;
+// §3), the per-level neighbour / ghost / transfer tables, the coarse
+// FFT-LGF solver, and runs Alg. 1 as a fixed
+// schedule of sm_100a kernel launches (optionally one CUDA graph per V-cycle).
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "mg_internal.h"
+
+namespace mg {
+std::vector<double> box_lgf(int dim, int order, int R);
+}
+
+using namespace mg;
+
+namespace {
+
+constexpr int GE = 5;  // exterior band width produced by the coarse solve (reading Z21/U1)
+
+struct MgError : std::runtime_error {
+  int code;
+  MgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CUDA_OK(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess)                                                                      \
+      throw MgError(e_ == cudaErrorMemoryAllocation ? MG_ERR_OOM : MG_ERR_CUDA,                 \
+                    std::string(#x) + ": " + cudaGetErrorString(e_));                           \
+  } while (0)
+#define CUFFT_OK(x)                                                                             \
+  do {                                                                                          \
+    cufftResult r_ = (x);                                                                       \
+    if (r_ != CUFFT_SUCCESS) throw MgError(MG_ERR_CUDA, std::string(#x) + " failed: " + std::to_string(r_)); \
+  } while (0)
+
+thread_local std::string g_err = "";
+
+inline int64_t key3(int x, int y, int z) {
+  return (((int64_t)(z + 4096)) << 40) | (((int64_t)(y + 4096)) << 20) | (int64_t)(x + 4096);
+}
+
+inline int fdiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+uint64_t morton(int x, int y, int z) {
+  uint64_t m = 0;
+  for (int i = 0; i < 21; ++i) {
+    m |= (uint64_t)((x >> i) & 1) << (3 * i);
+    m |= (uint64_t)((y >> i) & 1) << (3 * i + 1);
+    m |= (uint64_t)((z >> i) & 1) << (3 * i + 2);
+  }
+  return m;
+}
+
+template <class T>
+T* dev_upload(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = nullptr;
+  CUDA_OK(cudaMalloc(&p, v.size() * sizeof(T)));
+  CUDA_OK(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+struct Level {
+  int B = 0, B3 = 0, nreal = 0, nghost = 0, amr = 0;
+  int N[3] = {0, 0, 0};
+  double h = 0;
+  std::vector<std::array<int, 3>> coords;  // real, then ghost
+  std::unordered_map<int64_t, int> index;
+  std::vector<std::vector<uint64_t>> need;  // per ghost block: B^3 bitset of needed nodes
+  std::vector<uint8_t> ghost_ext;           // per ghost block: beyond an unbounded face
+  bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
+  // host tables
+  std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src;
+  std::vector<uint32_t> nbr_real;
+  std::vector<uint8_t> covmask, c2f_ext;
+  int bmap_lo[3] = {0, 0, 0}, bmap_n[3] = {1, 1, 1};
+  // device
+  double* u[2] = {nullptr, nullptr};
+  double *f = nullptr, *r = nullptr, *uhat = nullptr;
+  int cur = 0;
+  int32_t *d_nbr = nullptr, *d_parent = nullptr, *d_bmap = nullptr, *d_c2f_dst = nullptr, *d_c2f_J = nullptr,
+          *d_inj_dst = nullptr, *d_inj_src = nullptr;
+  uint32_t* d_nbr_real = nullptr;
+  uint8_t *d_covmask = nullptr, *d_c2f_ext = nullptr;
+
+  int ntot() const { return nreal + nghost; }
+  int find(int x, int y, int z) const {
+    auto it = index.find(key3(x, y, z));
+    return it == index.end() ? -1 : it->second;
+  }
+};
+
+}  // namespace
+
+struct mg_handle {
+  mg_desc d{};
+  int per[3] = {1, 1, 1};
+  int order = 4, I = 6, smoother = 1, eta1 = 2, eta2 = 2;
+  double omega = 1.0;
+  int nsub = 0;
+  std::vector<Level> L;
+  std::vector<std::array<int, 4>> leaves;
+  cudaStream_t s = nullptr;
+  int64_t* d_leafmap = nullptr;
+  double** d_lvl_ptrs = nullptr;  // per-level pointer table for the leaf scatter
+  std::vector<double*> h_lvl_ptrs;
+  unsigned long long* d_norm = nullptr;
+  double* d_leafbuf = nullptr;   // [n_leaf][B^3] scratch (host e2e path, Cauchy)
+  double* d_leafbuf2 = nullptr;
+  bool rhs_set = false;
+  double fstar_norm = 0.0;
+  // coarse solve
+  int coarse_kind = 0;  // 0 PPP, 1 UUU, 2 PUU
+  int P[3] = {0, 0, 0};
+  cufftHandle plan_f = 0, plan_b = 0;
+  double* d_dense = nullptr;
+  void* d_spec = nullptr;
+  double* d_mult = nullptr;  // UUU: full table; PUU: 2D table
+  // graph
+  bool use_graph = false;
+  cudaGraphExec_t gexec = nullptr;
+  int graph_cur_sig = -1;
+  std::string err;
+};
+
+namespace {
+
+LevelView view(mg_handle* h, int m) {
+  Level& l = h->L[m];
+  LevelView v{};
+  v.B = l.B;
+  v.B3 = l.B3;
+  v.nreal = l.nreal;
+  v.ntot = l.ntot();
+  for (int a = 0; a < 3; ++a) {
+    v.N[a] = l.N[a];
+    v.bmap_lo[a] = l.bmap_lo[a];
+    v.bmap_n[a] = l.bmap_n[a];
+    v.per[a] = h->per[a];
+  }
+  v.h = l.h;
+  v.u = l.u[l.cur];
+  v.u_out = l.u[1 - l.cur];
+  v.f = l.f;
+  v.r = l.r;
+  v.uhat = l.uhat;
+  v.nbr = l.d_nbr;
+  v.nbr_real = l.d_nbr_real;
+  v.covmask = l.d_covmask;
+  v.parent = l.d_parent;
+  v.bmap = l.d_bmap;
+  return v;
+}
+
+C2FList c2f_list(Level& l) {
+  C2FList g{};
+  g.n = (int)l.c2f_dst.size();
+  g.dst = l.d_c2f_dst;
+  g.J = l.d_c2f_J;
+  g.ext = l.d_c2f_ext;
+  return g;
+}
+
+InjList inj_list(Level& l) {
+  InjList g{};
+  g.n = (int)l.inj_dst.size();
+  g.dst = l.d_inj_dst;
+  g.src = l.d_inj_src;
+  return g;
+}
+
+// ----------------------------------------------------------------------------------
+// hierarchy construction
+// ----------------------------------------------------------------------------------
+void validate_and_build(mg_handle* h) {
+  const mg_desc& d = h->d;
+  const int B = d.block_size;
+  if (!(B == 16 || B == 8)) throw MgError(MG_ERR_ARG, "block_size must be 8 or 16");
+  if (d.order != 2 && d.order != 4) throw MgError(MG_ERR_ORDER, "order must be 2 or 4");
+  if (d.smoother != MG_SMOOTHER_JACOBI && d.smoother != MG_SMOOTHER_RBGS) throw MgError(MG_ERR_ARG, "bad smoother");
+  if (d.n_leaf <= 0 || !d.leaves) throw MgError(MG_ERR_ARG, "no leaves");
+  if (d.eta1 < 0 || d.eta2 < 0 || !(d.h0 > 0)) throw MgError(MG_ERR_ARG, "bad eta/h0");
+  for (int a = 0; a < 3; ++a) {
+    if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
+    if (d.bc[2 * a] != d.bc[2 * a + 1]) throw MgError(MG_ERR_BC, "both faces of an axis must have the same bc");
+    if (d.bc[2 * a] != MG_BC_PERIODIC && d.bc[2 * a] != MG_BC_UNBOUNDED)
+      throw MgError(MG_ERR_BC, "EVEN/ODD boundary conditions are reserved");
+    h->per[a] = d.bc[2 * a] == MG_BC_PERIODIC;
+  }
+  h->order = d.order;
+  h->I = d.order + 2;
+  h->smoother = d.smoother;
+  h->omega = d.omega;
+  h->eta1 = d.eta1;
+  h->eta2 = d.eta2;
+
+  // ---- AMR tree from the leaves
+  int amax = 0;
+  for (int64_t i = 0; i < d.n_leaf; ++i) {
+    std::array<int, 4> lf = {d.leaves[4 * i], d.leaves[4 * i + 1], d.leaves[4 * i + 2], d.leaves[4 * i + 3]};
+    if (lf[0] < 0 || lf[0] > 20) throw MgError(MG_ERR_ARG, "bad leaf level");
+    for (int a = 0; a < 3; ++a)
+      if (lf[a + 1] < 0 || lf[a + 1] >= (d.base_blocks[a] << lf[0])) throw MgError(MG_ERR_ARG, "leaf out of range");
+    amax = std::max(amax, lf[0]);
+    h->leaves.push_back(lf);
+  }
+  std::vector<std::unordered_set<int64_t>> nodes(amax + 1), leafset(amax + 1);
+  for (auto& lf : h->leaves) {
+    if (!leafset[lf[0]].insert(key3(lf[1], lf[2], lf[3])).second) throw MgError(MG_ERR_LAYOUT_NESTING, "duplicate leaf");
+    int x = lf[1], y = lf[2], z = lf[3];
+    for (int a = lf[0]; a >= 0; --a) {
+      nodes[a].insert(key3(x, y, z));
+      x >>= 1; y >>= 1; z >>= 1;
+    }
+  }
+  for (int a = 0; a <= amax; ++a)
+    for (int64_t k : leafset[a]) {
+      // a leaf may not have descendants
+      if (a < amax) {
+        const int x = (int)(k & 0xfffff) - 4096, y = (int)((k >> 20) & 0xfffff) - 4096, z = (int)(k >> 40) - 4096;
+        if (nodes[a + 1].count(key3(2 * x, 2 * y, 2 * z))) throw MgError(MG_ERR_LAYOUT_NESTING, "leaf is also refined");
+      }
+    }
+  if ((int64_t)nodes[0].size() != (int64_t)d.base_blocks[0] * d.base_blocks[1] * d.base_blocks[2])
+    throw MgError(MG_ERR_LAYOUT_NESTING, "level 0 is not fully covered by the leaves");
+  for (int a = 0; a < amax; ++a)
+    for (int64_t k : nodes[a]) {
+      const int x = (int)(k & 0xfffff) - 4096, y = (int)((k >> 20) & 0xfffff) - 4096, z = (int)(k >> 40) - 4096;
+      int cnt = 0;
+      for (int o = 0; o < 8; ++o) cnt += (int)nodes[a + 1].count(key3(2 * x + (o & 1), 2 * y + ((o >> 1) & 1), 2 * z + (o >> 2)));
+      if (cnt != 0 && cnt != 8) throw MgError(MG_ERR_LAYOUT_NESTING, "partially refined block");
+    }
+  // 26-neighbour 2:1 balance and the unbounded-face rule
+  for (auto& lf : h->leaves) {
+    const int a = lf[0];
+    for (int ax = 0; ax < 3; ++ax)
+      if (a > 0 && !h->per[ax] && (lf[ax + 1] == 0 || lf[ax + 1] == (d.base_blocks[ax] << a) - 1) &&
+          !d.allow_unbounded_refined)
+        throw MgError(MG_ERR_UNBOUNDED_REFINED, "a refined block touches an unbounded face");
+    if (a < 2) continue;
+    for (int o = 0; o < 27; ++o) {
+      if (o == 13) continue;
+      int c[3] = {lf[1] + o % 3 - 1, lf[2] + (o / 3) % 3 - 1, lf[3] + o / 9 - 1};
+      bool out = false;
+      for (int ax = 0; ax < 3; ++ax) {
+        const int n = d.base_blocks[ax] << a;
+        if (h->per[ax]) c[ax] = ((c[ax] % n) + n) % n;
+        else if (c[ax] < 0 || c[ax] >= n) out = true;
+      }
+      if (out) continue;
+      if (!nodes[a - 1].count(key3(c[0] >> 1, c[1] >> 1, c[2] >> 1)))
+        throw MgError(MG_ERR_LAYOUT_2TO1, "2:1 constraint violated");
+    }
+  }
+
+  // ---- multigrid levels: uniform sub-base coarsenings (reading Z5) + AMR levels
+  int N0[3];
+  for (int a = 0; a < 3; ++a) N0[a] = d.base_blocks[a] * B;
+  int nsub = 0;
+  if (d.coarse_n > 0) {
+    int n = N0[0];
+    while (n > d.coarse_n && n % 2 == 0) { n /= 2; ++nsub; }
+    if (n != d.coarse_n) throw MgError(MG_ERR_ARG, "coarse_n must be N0 / 2^j");
+    for (int a = 0; a < 3; ++a)
+      if ((N0[a] >> nsub) << nsub != N0[a]) throw MgError(MG_ERR_ARG, "coarse_n: axes not divisible");
+  }
+  h->nsub = nsub;
+  const int nlev = nsub + amax + 1;
+  h->L.resize(nlev);
+  for (int m = 0; m < nlev; ++m) {
+    Level& l = h->L[m];
+    const int a = m - nsub;
+    l.amr = a;
+    int nmin = 1 << 30;
+    for (int ax = 0; ax < 3; ++ax) {
+      l.N[ax] = a < 0 ? (N0[ax] >> (-a)) : (N0[ax] << a);
+      nmin = std::min(nmin, l.N[ax]);
+    }
+    l.B = std::min(B, nmin);
+    if (!(l.B == 16 || l.B == 8 || l.B == 4)) throw MgError(MG_ERR_ARG, "coarse level too small (block size < 4)");
+    for (int ax = 0; ax < 3; ++ax)
+      if (l.N[ax] % l.B) throw MgError(MG_ERR_ARG, "level size not divisible by its block size");
+    l.B3 = l.B * l.B * l.B;
+    l.h = d.h0 * std::pow(2.0, -a);
+    std::vector<std::array<int, 3>> cs;
+    if (a < 0) {
+      for (int z = 0; z < l.N[2] / l.B; ++z)
+        for (int y = 0; y < l.N[1] / l.B; ++y)
+          for (int x = 0; x < l.N[0] / l.B; ++x) cs.push_back({x, y, z});
+    } else {
+      for (int64_t k : nodes[a])
+        cs.push_back({(int)(k & 0xfffff) - 4096, (int)((k >> 20) & 0xfffff) - 4096, (int)(k >> 40) - 4096});
+    }
+    std::sort(cs.begin(), cs.end(), [](const std::array<int, 3>& p, const std::array<int, 3>& q) {
+      return morton(p[0], p[1], p[2]) < morton(q[0], q[1], q[2]);
+    });
+    l.coords = cs;
+    l.nreal = (int)cs.size();
+    for (int i = 0; i < l.nreal; ++i) l.index[key3(cs[i][0], cs[i][1], cs[i][2])] = i;
+  }
+
+  // ---- parents (fine block -> covered sub-box of its coarse block) and covered octants
+  for (int m = 0; m < nlev; ++m) h->L[m].covmask.assign(h->L[m].nreal, 0);
+  for (int m = 1; m < nlev; ++m) {
+    Level &F = h->L[m], &C = h->L[m - 1];
+    F.parent.assign(4 * F.nreal, 0);
+    for (int i = 0; i < F.nreal; ++i) {
+      int cb[3], off[3];
+      for (int a = 0; a < 3; ++a) {
+        const int s = F.B * F.coords[i][a] / 2;
+        cb[a] = s / C.B;
+        off[a] = s % C.B;
+      }
+      const int p = C.find(cb[0], cb[1], cb[2]);
+      if (p < 0) throw MgError(MG_ERR_LAYOUT_NESTING, "fine block without parent");
+      F.parent[4 * i] = p;
+      F.parent[4 * i + 1] = off[0];
+      F.parent[4 * i + 2] = off[1];
+      F.parent[4 * i + 3] = off[2];
+      if (F.B / 2 == C.B) C.covmask[p] = 0xff;
+      else C.covmask[p] |= (uint8_t)(1u << ((off[0] >= C.B / 2) | ((off[1] >= C.B / 2) << 1) | ((off[2] >= C.B / 2) << 2)));
+    }
+  }
+}
+
+// Mark node (J) of level m as a needed boundary ghost; creates the ghost block.
+void need_node(mg_handle* h, Level& l, int Jx, int Jy, int Jz) {
+  int J[3] = {Jx, Jy, Jz};
+  bool ext = false;
+  for (int a = 0; a < 3; ++a) {
+    if (h->per[a]) J[a] = ((J[a] % l.N[a]) + l.N[a]) % l.N[a];
+    else if (J[a] < 0 || J[a] >= l.N[a]) ext = true;
+  }
+  const int bx = fdiv(J[0], l.B), by = fdiv(J[1], l.B), bz = fdiv(J[2], l.B);
+  int idx = l.find(bx, by, bz);
+  if (idx >= 0 && idx < l.nreal) return;  // a real node, not a ghost
+  if (idx < 0) {
+    idx = l.nreal + l.nghost++;
+    l.coords.push_back({bx, by, bz});
+    l.index[key3(bx, by, bz)] = idx;
+    l.need.emplace_back((l.B3 + 63) / 64, 0ull);
+    l.ghost_ext.push_back(ext ? 1 : 0);
+  }
+  const int g = idx - l.nreal;
+  const int loc = ((J[2] - bz * l.B) * l.B + (J[1] - by * l.B)) * l.B + (J[0] - bx * l.B);
+  l.need[g][loc >> 6] |= 1ull << (loc & 63);
+}
+
+bool is_real_node(const mg_handle* h, const Level& l, int Jx, int Jy, int Jz, int* flat) {
+  int J[3] = {Jx, Jy, Jz};
+  for (int a = 0; a < 3; ++a) {
+    if (h->per[a]) J[a] = ((J[a] % l.N[a]) + l.N[a]) % l.N[a];
+    else if (J[a] < 0 || J[a] >= l.N[a]) return false;
+  }
+  const int bx = J[0] / l.B, by = J[1] / l.B, bz = J[2] / l.B;
+  const int idx = l.find(bx, by, bz);
+  if (idx < 0 || idx >= l.nreal) return false;
+  if (flat) *flat = idx * l.B3 + ((J[2] - bz * l.B) * l.B + (J[1] - by * l.B)) * l.B + (J[0] - bx * l.B);
+  return true;
+}
+
+void build_ghosts(mg_handle* h) {
+  const int nlev = (int)h->L.size();
+  const int g = h->smoother == MG_SMOOTHER_RBGS ? 2 : 1;  // halo read by one sweep
+  for (int m = nlev - 1; m >= 0; --m) {
+    Level& l = h->L[m];
+    // halo ghosts: nodes within Chebyshev distance g of a real block, not in one
+    for (int i = 0; i < l.nreal; ++i) {
+      const auto c = l.coords[i];
+      for (int o = 0; o < 27; ++o) {
+        if (o == 13) continue;
+        const int dx = o % 3 - 1, dy = (o / 3) % 3 - 1, dz = o / 9 - 1;
+        int nc[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
+        bool ext = false;
+        for (int a = 0; a < 3; ++a) {
+          const int nb = l.N[a] / l.B;
+          if (h->per[a]) nc[a] = ((nc[a] % nb) + nb) % nb;
+          else if (nc[a] < 0 || nc[a] >= nb) ext = true;
+        }
+        (void)ext;
+        const int idx = l.find(nc[0], nc[1], nc[2]);
+        if (idx >= 0 && idx < l.nreal) continue;
+        const int lo[3] = {dx < 0 ? l.B - g : 0, dy < 0 ? l.B - g : 0, dz < 0 ? l.B - g : 0};
+        const int hi[3] = {dx > 0 ? g : l.B, dy > 0 ? g : l.B, dz > 0 ? g : l.B};
+        for (int z = lo[2]; z < hi[2]; ++z)
+          for (int y = lo[1]; y < hi[1]; ++y)
+            for (int x = lo[0]; x < hi[0]; ++x)
+              need_node(h, l, (c[0] + dx) * l.B + x, (c[1] + dy) * l.B + y, (c[2] + dz) * l.B + z);
+      }
+    }
+    if (m == 0) {
+      // coarsest: every ghost is an exterior node filled from the coarse-solve band
+      for (int gi = 0; gi < l.nghost; ++gi)
+        if (!l.ghost_ext[gi]) throw MgError(MG_ERR_LAYOUT_NESTING, "coarsest level has interior ghosts");
+    }
+    // list the needed ghost nodes; for m >= 1 derive the c2f taps on level m-1
+    Level* C = m > 0 ? &h->L[m - 1] : nullptr;
+    std::unordered_set<int64_t> injset;
+    for (int gi = 0; gi < l.nghost; ++gi) {
+      const auto c = l.coords[l.nreal + gi];
+      int bb_lo[3] = {1 << 30, 1 << 30, 1 << 30}, bb_hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
+      for (int loc = 0; loc < l.B3; ++loc) {
+        if (!((l.need[gi][loc >> 6] >> (loc & 63)) & 1)) continue;
+        const int J[3] = {c[0] * l.B + loc % l.B, c[1] * l.B + (loc / l.B) % l.B, c[2] * l.B + loc / (l.B * l.B)};
+        bool ext = false;
+        for (int a = 0; a < 3; ++a)
+          if (!h->per[a] && (J[a] < 0 || J[a] >= l.N[a])) ext = true;
+        if (ext && m > 0 && !h->d.allow_unbounded_refined)
+          throw MgError(MG_ERR_UNBOUNDED_REFINED, "refined level needs exterior ghosts");
+        if (ext && m > 0) l.ext_chain = true;
+        if (m == 0) {
+          for (int a = 0; a < 3; ++a)
+            if (!h->per[a] && (J[a] < -GE || J[a] >= l.N[a] + GE))
+              throw MgError(MG_ERR_LAYOUT_GHOST, "exterior ghost beyond the coarse-solve band");
+        }
+        l.c2f_dst.push_back((l.nreal + gi) * l.B3 + loc);
+        for (int a = 0; a < 3; ++a) l.c2f_J.push_back(J[a]);
+        l.c2f_ext.push_back(ext ? 1 : 0);
+        for (int a = 0; a < 3; ++a) {
+          bb_lo[a] = std::min(bb_lo[a], J[a]);
+          bb_hi[a] = std::max(bb_hi[a], J[a]);
+        }
+        if (m > 0) {
+          // coarse tap range per axis (centred I-point rule for odd J)
+          int t0[3], t1[3];
+          for (int a = 0; a < 3; ++a) {
+            if ((J[a] & 1) == 0) { t0[a] = J[a] >> 1; t1[a] = t0[a]; }
+            else { t0[a] = ((J[a] - 1) >> 1) - h->I / 2 + 1; t1[a] = t0[a] + h->I - 1; }
+          }
+          if (ext) {
+            for (int z = t0[2]; z <= t1[2]; ++z)
+              for (int y = t0[1]; y <= t1[1]; ++y)
+                for (int x = t0[0]; x <= t1[0]; ++x)
+                  if (!is_real_node(h, *C, x, y, z, nullptr)) need_node(h, *C, x, y, z);
+          } else {
+            for (int k = 0; k < 8; ++k) {
+              const int x = (k & 1) ? t1[0] : t0[0], y = (k & 2) ? t1[1] : t0[1], z = (k & 4) ? t1[2] : t0[2];
+              if (!is_real_node(h, *C, x, y, z, nullptr))
+                throw MgError(MG_ERR_LAYOUT_GHOST, "ghost interpolation stencil leaves the coarse level (2:1?)");
+            }
+          }
+        }
+      }
+      if (m > 0 && bb_lo[0] <= bb_hi[0]) {
+        // f2c injection of every covered coarse node in the tap hull of this ghost block
+        for (int z = fdiv(bb_lo[2], 2) - h->I / 2; z <= fdiv(bb_hi[2], 2) + h->I / 2; ++z)
+          for (int y = fdiv(bb_lo[1], 2) - h->I / 2; y <= fdiv(bb_hi[1], 2) + h->I / 2; ++y)
+            for (int x = fdiv(bb_lo[0], 2) - h->I / 2; x <= fdiv(bb_hi[0], 2) + h->I / 2; ++x) {
+              int cflat, fflat;
+              if (!is_real_node(h, *C, x, y, z, &cflat)) continue;
+              if (!is_real_node(h, l, 2 * x, 2 * y, 2 * z, &fflat)) continue;
+              if (injset.insert(cflat).second) {
+                l.inj_dst.push_back(cflat);
+                l.inj_src.push_back(fflat);
+              }
+            }
+      }
+    }
+  }
+  // neighbour tables and block maps
+  for (int m = 0; m < nlev; ++m) {
+    Level& l = h->L[m];
+    l.nbr.assign(27 * (size_t)l.nreal, -1);
+    l.nbr_real.assign(l.nreal, 0);
+    for (int i = 0; i < l.nreal; ++i) {
+      const auto c = l.coords[i];
+      for (int o = 0; o < 27; ++o) {
+        int nc[3] = {c[0] + o % 3 - 1, c[1] + (o / 3) % 3 - 1, c[2] + o / 9 - 1};
+        for (int a = 0; a < 3; ++a) {
+          const int nb = l.N[a] / l.B;
+          if (h->per[a]) nc[a] = ((nc[a] % nb) + nb) % nb;
+        }
+        const int idx = l.find(nc[0], nc[1], nc[2]);
+        if (idx < 0) throw MgError(MG_ERR_LAYOUT_GHOST, "missing neighbour block");
+        l.nbr[27 * (size_t)i + o] = idx;
+        if (idx < l.nreal) l.nbr_real[i] |= 1u << o;
+      }
+    }
+    int lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) { lo[a] = 0; hi[a] = l.N[a] / l.B - 1; }
+    for (auto& c : l.coords)
+      for (int a = 0; a < 3; ++a) { lo[a] = std::min(lo[a], c[a]); hi[a] = std::max(hi[a], c[a]); }
+    size_t n = 1;
+    for (int a = 0; a < 3; ++a) { l.bmap_lo[a] = lo[a]; l.bmap_n[a] = hi[a] - lo[a] + 1; n *= l.bmap_n[a]; }
+    l.bmap.assign(n, -1);
+    for (int i = 0; i < l.ntot(); ++i) {
+      const auto c = l.coords[i];
+      l.bmap[((size_t)(c[2] - lo[2]) * l.bmap_n[1] + (c[1] - lo[1])) * l.bmap_n[0] + (c[0] - lo[0])] = i;
+    }
+  }
+}
+
+void alloc_device(mg_handle* h) {
+  for (auto& l : h->L) {
+    const size_t n = (size_t)l.ntot() * l.B3;
+    for (double** p : {&l.u[0], &l.u[1], &l.f, &l.r, &l.uhat}) {
+      CUDA_OK(cudaMalloc(p, n * sizeof(double)));
+      CUDA_OK(cudaMemsetAsync(*p, 0, n * sizeof(double), h->s));
+    }
+    l.d_nbr = dev_upload(l.nbr);
+    l.d_nbr_real = dev_upload(l.nbr_real);
+    l.d_covmask = dev_upload(l.covmask);
+    l.d_parent = dev_upload(l.parent);
+    l.d_bmap = dev_upload(l.bmap);
+    l.d_c2f_dst = dev_upload(l.c2f_dst);
+    l.d_c2f_J = dev_upload(l.c2f_J);
+    l.d_c2f_ext = dev_upload(l.c2f_ext);
+    l.d_inj_dst = dev_upload(l.inj_dst);
+    l.d_inj_src = dev_upload(l.inj_src);
+  }
+  // leaf map: leaf n -> (level, block)
+  std::vector<int64_t> map(h->leaves.size());
+  for (size_t n = 0; n < h->leaves.size(); ++n) {
+    const auto& lf = h->leaves[n];
+    const int m = h->nsub + lf[0];
+    const int idx = h->L[m].find(lf[1], lf[2], lf[3]);
+    map[n] = ((int64_t)m << 32) | (int64_t)idx;
+  }
+  h->d_leafmap = dev_upload(map);
+  h->h_lvl_ptrs.assign(h->L.size(), nullptr);
+  CUDA_OK(cudaMalloc(&h->d_lvl_ptrs, h->L.size() * sizeof(double*)));
+  CUDA_OK(cudaMalloc(&h->d_norm, 2 * sizeof(unsigned long long)));
+  const size_t nl = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
+  CUDA_OK(cudaMalloc(&h->d_leafbuf, nl * sizeof(double)));
+  CUDA_OK(cudaMalloc(&h->d_leafbuf2, nl * sizeof(double)));
+}
+
+int smooth7(int n) {
+  for (int m = std::max(n, 1);; ++m) {
+    int r = m;
+    for (int p : {2, 3, 5, 7})
+      while (r % p == 0) r /= p;
+    if (r == 1) return m;
+  }
+}
+
+void setup_coarse(mg_handle* h) {
+  Level& c = h->L[0];
+  int nunb = 0;
+  for (int a = 0; a < 3; ++a) {
+    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * c.N[a] + 2 * GE - 1);
+    nunb += !h->per[a];
+  }
+  if (nunb == 0) h->coarse_kind = 0;
+  else if (nunb == 3) h->coarse_kind = 1;
+  else if (nunb == 2 && h->per[0]) h->coarse_kind = 2;
+  else throw MgError(MG_ERR_BC, "boundary combination not supported yet (PPP, UUU, x-periodic PUU)");
+  const int Px = h->P[0], Py = h->P[1], Pz = h->P[2];
+  const int64_t nd = (int64_t)Px * Py * Pz, nc = (int64_t)(Px / 2 + 1) * Py * Pz;
+  CUDA_OK(cudaMalloc(&h->d_dense, nd * sizeof(double)));
+  CUDA_OK(cudaMalloc(&h->d_spec, nc * sizeof(cufftDoubleComplex)));
+  CUFFT_OK(cufftPlan3d(&h->plan_f, Pz, Py, Px, CUFFT_D2Z));
+  CUFFT_OK(cufftPlan3d(&h->plan_b, Pz, Py, Px, CUFFT_Z2D));
+  CUFFT_OK(cufftSetStream(h->plan_f, h->s));
+  CUFFT_OK(cufftSetStream(h->plan_b, h->s));
+  const double sc = c.h * c.h / (double)nd;
+  if (h->coarse_kind == 1) {
+    const int R = std::max(Px, std::max(Py, Pz)) / 2 + 8;
+    std::vector<double> G = box_lgf(3, h->order, R);
+    const int n = 2 * R + 1;
+    std::vector<double> T(nd);
+    for (int z = 0; z < Pz; ++z)
+      for (int y = 0; y < Py; ++y)
+        for (int x = 0; x < Px; ++x) {
+          const int nx = x <= Px / 2 ? x : x - Px, ny = y <= Py / 2 ? y : y - Py, nz = z <= Pz / 2 ? z : z - Pz;
+          T[((size_t)z * Py + y) * Px + x] = G[((size_t)(nz + R) * n + (ny + R)) * n + (nx + R)];
+        }
+    CUDA_OK(cudaMemcpy(h->d_dense, T.data(), nd * sizeof(double), cudaMemcpyHostToDevice));
+    CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
+    CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
+    launch_real_part_scale(h->d_spec, h->d_mult, nc, sc, h->s);
+  } else if (h->coarse_kind == 2) {
+    const int R = std::max(Py, Pz) / 2 + 8;
+    std::vector<double> G = box_lgf(2, h->order, R);
+    const int n = 2 * R + 1;
+    std::vector<cufftDoubleComplex> T((size_t)Py * Pz);
+    for (int z = 0; z < Pz; ++z)
+      for (int y = 0; y < Py; ++y) {
+        const int ny = y <= Py / 2 ? y : y - Py, nz = z <= Pz / 2 ? z : z - Pz;
+        T[(size_t)z * Py + y] = make_cuDoubleComplex(G[(size_t)(nz + R) * n + (ny + R)], 0.0);
+      }
+    cufftDoubleComplex* dT = nullptr;
+    CUDA_OK(cudaMalloc(&dT, T.size() * sizeof(cufftDoubleComplex)));
+    CUDA_OK(cudaMemcpy(dT, T.data(), T.size() * sizeof(cufftDoubleComplex), cudaMemcpyHostToDevice));
+    cufftHandle p2;
+    CUFFT_OK(cufftPlan2d(&p2, Pz, Py, CUFFT_Z2Z));
+    CUFFT_OK(cufftSetStream(p2, h->s));
+    CUFFT_OK(cufftExecZ2Z(p2, dT, dT, CUFFT_FORWARD));
+    CUDA_OK(cudaMalloc(&h->d_mult, T.size() * sizeof(double)));
+    launch_real_part_scale(dT, h->d_mult, (int64_t)T.size(), sc, h->s);
+    CUDA_OK(cudaStreamSynchronize(h->s));
+    cufftDestroy(p2);
+    cudaFree(dT);
+  }
+  CUDA_OK(cudaStreamSynchronize(h->s));
+}
+
+// ----------------------------------------------------------------------------------
+// V-cycle building blocks
+// ----------------------------------------------------------------------------------
+void swap_u(Level& l) { l.cur = 1 - l.cur; }
+
+// boundary-ghost refresh of level m (reading Z9): f2c injection into level m-1,
+// then c2f; exterior chains (reading U1) refresh every coarser level first.
+void refresh(mg_handle* h, int m) {
+  if (m <= 0) return;
+  const int lo = h->L[m].ext_chain ? 1 : m;
+  for (int j = m; j >= lo; --j) {
+    Level &F = h->L[j], &C = h->L[j - 1];
+    if (!F.inj_dst.empty()) launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->s);
+  }
+  for (int j = lo; j <= m; ++j) {
+    Level& F = h->L[j];
+    if (F.c2f_dst.empty()) continue;
+    LevelView fv = view(h, j), cv = view(h, j - 1);
+    launch_c2f(fv, cv, c2f_list(F), F.u[F.cur], cv.u, h->I, false, h->s);
+  }
+}
+
+bool has_ghosts(mg_handle* h, int m) { return m > 0 && !h->L[m].c2f_dst.empty(); }
+
+void sweep(mg_handle* h, int m, bool with_res) {
+  refresh(h, m);
+  Level& l = h->L[m];
+  const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
+  if (with_res && !has_ghosts(h, m)) {
+    launch_smooth(view(h, m), h->order, mode, h->omega, true, h->s);
+    swap_u(l);
+    return;
+  }
+  launch_smooth(view(h, m), h->order, mode, h->omega, false, h->s);
+  swap_u(l);
+  if (with_res) {
+    refresh(h, m);
+    launch_residual(view(h, m), h->order, h->s);
+  }
+}
+
+void restrict_level(mg_handle* h, int m) {
+  Level& C = h->L[m - 1];
+  launch_restrict(view(h, m), view(h, m - 1), h->s);
+  refresh(h, m - 1);
+  launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
+  CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+}
+
+void coarse_solve(mg_handle* h) {
+  LevelView c = view(h, 0);
+  launch_coarse_gather(c, h->d_dense, h->P, h->s);
+  CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
+  if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
+  else if (h->coarse_kind == 1)
+    launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
+  else launch_coarse_mul_puu(h->d_spec, h->P, h->order, h->L[0].h, h->d_mult, h->s);
+  CUFFT_OK(cufftExecZ2D(h->plan_b, (cufftDoubleComplex*)h->d_spec, h->d_dense));
+  launch_coarse_scatter(c, h->d_dense, h->P, c2f_list(h->L[0]), h->s);
+}
+
+void inject_up_all(mg_handle* h) {
+  for (int m = (int)h->L.size() - 1; m >= 1; --m)
+    launch_inject_up(view(h, m), view(h, m - 1), h->L[m - 1].u[h->L[m - 1].cur], h->s);
+}
+
+void vcycle_body(mg_handle* h) {
+  const int top = (int)h->L.size() - 1;
+  for (int m = top; m >= 1; --m) {
+    for (int k = 1; k <= h->eta1; ++k) sweep(h, m, k == h->eta1);
+    if (h->eta1 == 0) {
+      refresh(h, m);
+      launch_residual(view(h, m), h->order, h->s);
+    }
+    restrict_level(h, m);
+  }
+  coarse_solve(h);
+  for (int m = 1; m <= top; ++m) {
+    launch_prolong(view(h, m), view(h, m - 1), h->s);
+    for (int k = 0; k < h->eta2; ++k) sweep(h, m, false);
+  }
+  inject_up_all(h);
+  if ((h->eta1 + h->eta2) & 1) {
+    // keep the buffer parity fixed per cycle (so one captured graph can be replayed)
+    for (int m = 1; m <= top; ++m) {
+      Level& l = h->L[m];
+      CUDA_OK(cudaMemcpyAsync(l.u[1 - l.cur], l.u[l.cur], (size_t)l.ntot() * l.B3 * sizeof(double),
+                              cudaMemcpyDeviceToDevice, h->s));
+      swap_u(l);
+    }
+  }
+}
+
+void run_vcycles(mg_handle* h, int n) {
+  if (!h->use_graph) {
+    for (int i = 0; i < n; ++i) vcycle_body(h);
+    return;
+  }
+  if (!h->gexec) {
+    // capture on a private stream (the caller's may be the legacy default stream,
+    // which cannot be captured), replay on the caller's stream
+    cudaStream_t orig = h->s, cap = nullptr;
+    CUDA_OK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamSynchronize(orig));
+    h->s = cap;
+    CUFFT_OK(cufftSetStream(h->plan_f, cap));
+    CUFFT_OK(cufftSetStream(h->plan_b, cap));
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      try {
+        vcycle_body(h);
+      } catch (...) {
+        cudaStreamEndCapture(cap, &g);
+        h->s = orig;
+        throw;
+      }
+      e = cudaStreamEndCapture(cap, &g);
+    }
+    h->s = orig;
+    cufftSetStream(h->plan_f, orig);
+    cufftSetStream(h->plan_b, orig);
+    cudaStreamDestroy(cap);
+    CUDA_OK(e);
+    CUDA_OK(cudaGraphInstantiate(&h->gexec, g, 0));
+    cudaGraphDestroy(g);
+  }
+  for (int i = 0; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->gexec, h->s));
+}
+
+double read_norm(mg_handle* h) {
+  unsigned long long bits = 0;
+  CUDA_OK(cudaMemcpyAsync(&bits, h->d_norm, sizeof(bits), cudaMemcpyDeviceToHost, h->s));
+  CUDA_OK(cudaStreamSynchronize(h->s));
+  double v;
+  std::memcpy(&v, &bits, sizeof(v));
+  if (!std::isfinite(v)) throw MgError(MG_ERR_NONFINITE, "non-finite value in norm");
+  return v;
+}
+
+double residual_abs(mg_handle* h) {
+  CUDA_OK(cudaMemsetAsync(h->d_norm, 0, sizeof(unsigned long long), h->s));
+  for (int m = 0; m < (int)h->L.size(); ++m) {
+    refresh(h, m);
+    launch_norm(view(h, m), h->order, true, h->d_norm, h->s);
+  }
+  return read_norm(h);
+}
+
+void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
+  for (size_t m = 0; m < h->L.size(); ++m) {
+    Level& l = h->L[m];
+    h->h_lvl_ptrs[m] = field == MG_FIELD_F ? l.f : l.u[l.cur];
+  }
+  CUDA_OK(cudaMemcpyAsync(h->d_lvl_ptrs, h->h_lvl_ptrs.data(), h->L.size() * sizeof(double*), cudaMemcpyHostToDevice,
+                          h->s));
+  launch_leaf_scatter((int)h->leaves.size(), h->d.block_size * h->d.block_size * h->d.block_size, h->d_leafmap,
+                      leafbuf, h->d_lvl_ptrs, (int)h->L.size(), to_levels, h->s);
+  // the pointer table is reused by the next call: order it on the stream
+  CUDA_OK(cudaStreamSynchronize(h->s));
+}
+
+void set_rhs(mg_handle* h, const double* f_dev) {
+  const int nlev = (int)h->L.size();
+  for (auto& l : h->L) {
+    const size_t n = (size_t)l.ntot() * l.B3;
+    CUDA_OK(cudaMemsetAsync(l.f, 0, n * sizeof(double), h->s));
+    CUDA_OK(cudaMemsetAsync(l.u[0], 0, n * sizeof(double), h->s));
+    CUDA_OK(cudaMemsetAsync(l.u[1], 0, n * sizeof(double), h->s));
+    CUDA_OK(cudaMemsetAsync(l.uhat, 0, n * sizeof(double), h->s));
+    CUDA_OK(cudaMemsetAsync(l.r, 0, n * sizeof(double), h->s));
+    l.cur = 0;
+  }
+  leaf_io(h, const_cast<double*>(f_dev), true, MG_FIELD_F);
+  // f2c: inject f up the tree (O5)
+  for (int m = nlev - 1; m >= 1; --m) {
+    LevelView fv = view(h, m), cv = view(h, m - 1);
+    fv.u = h->L[m].f;
+    launch_inject_up(fv, cv, h->L[m - 1].f, h->s);
+  }
+  // f ghosts: c2f of f, f := 0 beyond unbounded faces (reading Z16)
+  for (int m = 1; m < nlev; ++m) {
+    Level& F = h->L[m];
+    if (F.c2f_dst.empty()) continue;
+    LevelView fv = view(h, m), cv = view(h, m - 1);
+    launch_c2f(fv, cv, c2f_list(F), F.f, h->L[m - 1].f, h->I, true, h->s);
+  }
+  for (int m = 0; m < nlev; ++m) {
+    Level& l = h->L[m];
+    launch_correct_rhs(view(h, m), h->order, l.r, h->s);
+  }
+  for (auto& l : h->L)
+    CUDA_OK(cudaMemsetAsync(l.r, 0, (size_t)l.ntot() * l.B3 * sizeof(double), h->s));
+  CUDA_OK(cudaMemsetAsync(h->d_norm, 0, sizeof(unsigned long long), h->s));
+  for (int m = 0; m < nlev; ++m) launch_norm(view(h, m), h->order, false, h->d_norm, h->s);
+  h->fstar_norm = read_norm(h);
+  h->rhs_set = true;
+}
+
+void destroy(mg_handle* h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->s);
+  for (auto& l : h->L) {
+    for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
+                    (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
+                    (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src})
+      if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
+                  (void*)h->d_leafbuf2, (void*)h->d_dense, h->d_spec, (void*)h->d_mult})
+    if (p) cudaFree(p);
+  if (h->plan_f) cufftDestroy(h->plan_f);
+  if (h->plan_b) cufftDestroy(h->plan_b);
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  delete h;
+}
+
+template <class F>
+int guard(mg_handle* h, F&& fn) {
+  try {
+    fn();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw MgError(MG_ERR_CUDA, cudaGetErrorString(e));
+    return MG_OK;
+  } catch (const MgError& e) {
+    g_err = e.what();
+    if (h) h->err = g_err;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    if (h) h->err = g_err;
+    return MG_ERR_CUDA;
+  }
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------------------------
+// C-ABI
+// ----------------------------------------------------------------------------------
+extern "C" {
+
+int mg_create(const mg_desc* d, void* stream, mg_handle** out) {
+  if (!d || !out) {
+    g_err = "null argument";
+    return MG_ERR_ARG;
+  }
+  *out = nullptr;
+  mg_handle* h = new mg_handle();
+  h->d = *d;
+  h->s = (cudaStream_t)stream;
+  const int rc = guard(h, [&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw MgError(MG_ERR_CUDA, "no CUDA device");
+    prepare_kernels();
+    validate_and_build(h);
+    build_ghosts(h);
+    alloc_device(h);
+    setup_coarse(h);
+  });
+  if (rc != MG_OK) {
+    destroy(h);
+    return rc;
+  }
+  *out = h;
+  return MG_OK;
+}
+
+void mg_destroy(mg_handle* h) { destroy(h); }
+
+const char* mg_last_error(const mg_handle* h) {
+  if (h && !h->err.empty()) return h->err.c_str();
+  return g_err.c_str();
+}
+
+int mg_set_rhs(mg_handle* h, const double* f_dev) {
+  if (!h || !f_dev) return MG_ERR_ARG;
+  return guard(h, [&] { set_rhs(h, f_dev); });
+}
+
+int mg_set_solution(mg_handle* h, const double* u_dev) {
+  if (!h || !u_dev) return MG_ERR_ARG;
+  return guard(h, [&] {
+    leaf_io(h, const_cast<double*>(u_dev), true, MG_FIELD_U);
+    inject_up_all(h);
+  });
+}
+
+int mg_get_solution(mg_handle* h, double* u_dev) {
+  if (!h || !u_dev) return MG_ERR_ARG;
+  return guard(h, [&] { leaf_io(h, u_dev, false, MG_FIELD_U); });
+}
+
+int mg_vcycle(mg_handle* h, int n) {
+  if (!h || n < 0) return MG_ERR_ARG;
+  if (!h->rhs_set) {
+    h->err = "mg_vcycle before mg_set_rhs";
+    return MG_ERR_STATE;
+  }
+  return guard(h, [&] { run_vcycles(h, n); });
+}
+
+int mg_residual_norm(mg_handle* h, double* abs_inf, double* rel_inf) {
+  if (!h) return MG_ERR_ARG;
+  if (!h->rhs_set) return MG_ERR_STATE;
+  return guard(h, [&] {
+    const double a = residual_abs(h);
+    if (abs_inf) *abs_inf = a;
+    if (rel_inf) *rel_inf = h->fstar_norm > 0 ? a / h->fstar_norm : a;
+  });
+}
+
+int mg_solve(mg_handle* h, double tol, int max_cycles, int criterion, int* cycles_out, double* value_out) {
+  if (!h || max_cycles < 0) return MG_ERR_ARG;
+  if (!h->rhs_set) return MG_ERR_STATE;
+  int conv = 0;
+  const int rc = guard(h, [&] {
+    double val = 0.0;
+    int c = 0;
+    for (c = 1; c <= max_cycles; ++c) {
+      if (criterion == MG_CRIT_CAUCHY) leaf_io(h, h->d_leafbuf2, false, MG_FIELD_U);
+      run_vcycles(h, 1);
+      if (criterion == MG_CRIT_CAUCHY) {
+        leaf_io(h, h->d_leafbuf, false, MG_FIELD_U);
+        // max |u_new - u_old| / max |u_new| over leaf nodes (E20), on the host copy
+        const size_t n = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
+        std::vector<double> a(n), b(n);
+        CUDA_OK(cudaMemcpy(a.data(), h->d_leafbuf, n * sizeof(double), cudaMemcpyDeviceToHost));
+        CUDA_OK(cudaMemcpy(b.data(), h->d_leafbuf2, n * sizeof(double), cudaMemcpyDeviceToHost));
+        double dm = 0, um = 0;
+        for (size_t i = 0; i < n; ++i) {
+          dm = std::max(dm, std::fabs(a[i] - b[i]));
+          um = std::max(um, std::fabs(a[i]));
+        }
+        val = um > 0 ? dm / um : dm;   // zero-norm guard (absolute increment)
+      } else {
+        const double a = residual_abs(h);
+        val = h->fstar_norm > 0 ? a / h->fstar_norm : a;
+      }
+      if (val <= tol) {
+        conv = 1;
+        break;
+      }
+    }
+    if (cycles_out) *cycles_out = std::min(c, max_cycles);
+    if (value_out) *value_out = val;
+  });
+  if (rc != MG_OK) return rc;
+  return conv ? MG_OK : MG_WARN_NOT_CONVERGED;
+}
+
+int mg_run_host(mg_handle* h, const double* f_host, double* u_host, int ncycles, double* rel_out) {
+  if (!h || !f_host || !u_host || ncycles < 0) return MG_ERR_ARG;
+  return guard(h, [&] {
+    const size_t n = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
+    CUDA_OK(cudaMemcpyAsync(h->d_leafbuf, f_host, n * sizeof(double), cudaMemcpyHostToDevice, h->s));
+    set_rhs(h, h->d_leafbuf);
+    run_vcycles(h, ncycles);
+    leaf_io(h, h->d_leafbuf, false, MG_FIELD_U);
+    CUDA_OK(cudaMemcpyAsync(u_host, h->d_leafbuf, n * sizeof(double), cudaMemcpyDeviceToHost, h->s));
+    const double a = residual_abs(h);
+    if (rel_out) *rel_out = h->fstar_norm > 0 ? a / h->fstar_norm : a;
+  });
+}
+
+int mg_use_graph(mg_handle* h, int enable) {
+  if (!h) return MG_ERR_ARG;
+  h->use_graph = enable != 0;
+  return MG_OK;
+}
+
+int mg_num_levels(mg_handle* h) { return h ? (int)h->L.size() : MG_ERR_ARG; }
+
+int mg_level_info(mg_handle* h, int level, int64_t* info) {
+  if (!h || !info || level < 0 || level >= (int)h->L.size()) return MG_ERR_ARG;
+  Level& l = h->L[level];
+  int64_t nleaf_blocks = 0;
+  for (int i = 0; i < l.nreal; ++i) nleaf_blocks += l.covmask[i] == 0;
+  const int64_t v[10] = {l.B, l.nreal, l.nghost, l.N[0], l.N[1], l.N[2], l.amr,
+                         (int64_t)l.c2f_dst.size(), (int64_t)l.inj_dst.size(), nleaf_blocks};
+  std::memcpy(info, v, sizeof(v));
+  return MG_OK;
+}
+
+int mg_level_blocks(mg_handle* h, int level, int32_t* coords) {
+  if (!h || !coords || level < 0 || level >= (int)h->L.size()) return MG_ERR_ARG;
+  Level& l = h->L[level];
+  for (int i = 0; i < l.nreal; ++i)
+    for (int a = 0; a < 3; ++a) coords[3 * i + a] = l.coords[i][a];
+  return MG_OK;
+}
+
+int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev) {
+  if (!h || !dev || level < 0 || level >= (int)h->L.size()) return MG_ERR_ARG;
+  return guard(h, [&] {
+    Level& l = h->L[level];
+    double* p = field == MG_FIELD_U ? l.u[l.cur] : field == MG_FIELD_F ? l.f : field == MG_FIELD_R ? l.r : l.uhat;
+    const size_t n = (size_t)l.nreal * l.B3 * sizeof(double);
+    if (dir == 0) CUDA_OK(cudaMemcpyAsync(dev, p, n, cudaMemcpyDeviceToDevice, h->s));
+    else CUDA_OK(cudaMemcpyAsync(p, dev, n, cudaMemcpyDeviceToDevice, h->s));
+    CUDA_OK(cudaStreamSynchronize(h->s));
+  });
+}
+
+static void apply_op(mg_handle* h, int op, int level) {
+  const int top = (int)h->L.size() - 1;
+  if (level < 0 || level > top) throw MgError(MG_ERR_ARG, "bad level");
+  switch (op) {
+    case MG_OP_REFRESH: refresh(h, level); break;
+    case MG_OP_SMOOTH: sweep(h, level, false); break;
+    case MG_OP_SMOOTH_RESIDUAL: sweep(h, level, true); break;
+    case MG_OP_RESIDUAL:
+      refresh(h, level);
+      launch_residual(view(h, level), h->order, h->s);
+      break;
+    case MG_OP_RESTRICT:
+      if (level < 1) throw MgError(MG_ERR_ARG, "restrict needs level >= 1");
+      refresh(h, level);
+      launch_residual(view(h, level), h->order, h->s);
+      restrict_level(h, level);
+      break;
+    case MG_OP_PROLONG:
+      if (level < 1) throw MgError(MG_ERR_ARG, "prolong needs level >= 1");
+      launch_prolong(view(h, level), view(h, level - 1), h->s);
+      break;
+    case MG_OP_INJECT_UP: inject_up_all(h); break;
+    case MG_OP_COARSE_SOLVE: coarse_solve(h); break;
+    default: throw MgError(MG_ERR_ARG, "bad op");
+  }
+}
+
+int mg_debug_apply(mg_handle* h, int op, int level) {
+  if (!h) return MG_ERR_ARG;
+  return guard(h, [&] {
+    apply_op(h, op, level);
+    CUDA_OK(cudaStreamSynchronize(h->s));
+  });
+}
+
+int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out) {
+  if (!h || reps <= 0) return MG_ERR_ARG;
+  return guard(h, [&] {
+    cudaEvent_t a, b;
+    CUDA_OK(cudaEventCreate(&a));
+    CUDA_OK(cudaEventCreate(&b));
+    CUDA_OK(cudaEventRecord(a, h->s));
+    for (int i = 0; i < reps; ++i) {
+      if (op < 0) {
+        // op -1: the bare smoother kernel (fused RB+residual if `level` is ghost-free)
+        const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
+        launch_smooth(view(h, level), h->order, mode, h->omega, true, h->s);
+      } else if (op == 100) {
+        run_vcycles(h, 1);
+      } else {
+        apply_op(h, op, level);
+      }
+    }
+    CUDA_OK(cudaEventRecord(b, h->s));
+    CUDA_OK(cudaEventSynchronize(b));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, a, b));
+    if (ms_out) *ms_out = ms / reps;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+}  // extern "C"

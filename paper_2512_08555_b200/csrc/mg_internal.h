@@ -1,0 +1,73 @@
+// mg_internal.h — device-side level description shared by the host runtime
+// (mg_host.cpp) and the sm_100a kernels (mg_kernels.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mg {
+
+enum SmoothMode { SM_JACOBI = 0, SM_RB = 1 };
+
+// One multigrid level in HBM.  Every field array is [ntot][B^3] fp64, x fastest;
+// blocks [0, nreal) are the level's real blocks (leaves + parents, Morton order),
+// blocks [nreal, ntot) are ghost blocks whose needed nodes hold boundary-ghost
+// values (resolution-jump c2f, exterior band).  See DESIGN.md §Layout.
+struct LevelView {
+  int B, B3, nreal, ntot;
+  int N[3];             // nodes per axis of the level lattice
+  double h;
+  double* u;            // current solution buffer (ping-pong, see mg_host.cpp)
+  double* u_out;        // the other buffer (smoother output)
+  double* f;
+  double* r;
+  double* uhat;
+  const int32_t* nbr;       // [nreal][27], slot (dx+1)+3(dy+1)+9(dz+1) -> block index
+  const uint32_t* nbr_real; // [nreal] bit s set iff slot s is a real block
+  const uint8_t* covmask;   // [nreal] octant o covered by the finer level (bit o)
+  const int32_t* parent;    // [nreal][4] (parent block in level-1, ox, oy, oz); m >= 1
+  const int32_t* bmap;      // dense block-coordinate map (real+ghost) of this level
+  int bmap_lo[3], bmap_n[3];
+  int per[3];               // periodic axes
+};
+
+struct C2FList {           // boundary-ghost entries of one level
+  int n;
+  const int32_t* dst;      // flat index into the level arrays
+  const int32_t* J;        // [n][3] level-global node index (exterior allowed)
+  const uint8_t* ext;      // 1 = beyond an unbounded face
+};
+
+struct InjList {           // f2c injection pairs feeding a level's c2f stencils
+  int n;
+  const int32_t* dst;      // flat index into level m-1 arrays
+  const int32_t* src;      // flat index into level m arrays
+};
+
+// ---- launchers (mg_kernels.cu) ----
+void prepare_kernels();  // constants + shared-memory attributes (call before any capture)
+void launch_smooth(const LevelView& L, int order, int mode, double omega, bool with_residual,
+                   cudaStream_t s);
+void launch_residual(const LevelView& L, int order, cudaStream_t s);
+void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
+                const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
+void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);
+void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
+void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
+void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
+void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s);
+void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s);
+void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s);
+void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
+                         int nlev, bool to_levels, cudaStream_t s);
+void launch_zero(double* p, int64_t n, cudaStream_t s);
+// coarse solve helpers
+void launch_coarse_gather(const LevelView& L, double* dense, const int* P, cudaStream_t s);
+void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const C2FList& band,
+                           cudaStream_t s);
+void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s);
+void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s);
+void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s);
+void launch_scale(double* p, int64_t n, double a, cudaStream_t s);
+void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s);
+
+}  // namespace mg

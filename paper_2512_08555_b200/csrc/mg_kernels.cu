@@ -1,0 +1,660 @@
+// mg_kernels.cu — sm_100a kernels of the adaptive FAS V-cycle (Alg. 1).
+//
+// Data layout: each level stores fields as [ntot][B^3] fp64
+// blocks, x fastest.  A block's 26 neighbours come from a per-block table; a
+// neighbour that is not a real block of the level is a *ghost block* whose
+// needed nodes hold boundary-ghost values (c2f at resolution jumps, exterior
+// band), so every stencil kernel reads halos uniformly through the table.
+//
+// All arithmetic is fp64 on the CUDA cores: the path is HBM-bound (≈1 flop/B),
+// so there is no tensor-core work here by design (north star).
+#include <cuComplex.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mg_internal.h"
+
+namespace mg {
+
+__constant__ double c_w4[4];
+__constant__ double c_w6[6];
+
+static bool g_weights_ready = false;
+
+static void upload_weights() {
+  if (g_weights_ready) return;
+  // I-point centred Lagrange midpoint weights (reading Z7), I = M + 2
+  const double w4[4] = {-1.0 / 16, 9.0 / 16, 9.0 / 16, -1.0 / 16};
+  const double w6[6] = {3.0 / 256, -25.0 / 256, 150.0 / 256, 150.0 / 256, -25.0 / 256, 3.0 / 256};
+  cudaMemcpyToSymbol(c_w4, w4, sizeof(w4));
+  cudaMemcpyToSymbol(c_w6, w6, sizeof(w6));
+  g_weights_ready = true;
+}
+
+__device__ __forceinline__ int region(int x, int B) { return x < 0 ? -1 : (x >= B ? 1 : 0); }
+
+// Value of a level field at block-local coords (x,y,z) in [-B, 2B) of block `b`.
+__device__ __forceinline__ double fetch(const double* __restrict__ a, const int32_t* __restrict__ nb, int B,
+                                        int x, int y, int z) {
+  const int dx = region(x, B), dy = region(y, B), dz = region(z, B);
+  const int blk = __ldg(nb + (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1));
+  return a[(size_t)blk * (B * B * B) + ((z - dz * B) * B + (y - dy * B)) * B + (x - dx * B)];
+}
+
+__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// ---------------------------------------------------------------------------------
+// Stencils on a shared-memory tile (strides 1, T, T*T).  M=2: cross stencil E8;
+// M=4: 19-point Mehrstellen E12 (fig:stencils, weights {-24, 2, 1}/6).
+// ---------------------------------------------------------------------------------
+template <int ORDER, int T>
+__device__ __forceinline__ double lap_tile(const double* t, int i, double inv_h2) {
+  constexpr int SY = T, SZ = T * T;
+  const double c = t[i];
+  const double F = ((t[i - 1] + t[i + 1]) + (t[i - SY] + t[i + SY])) + (t[i - SZ] + t[i + SZ]);
+  if (ORDER == 2) return (F - 6.0 * c) * inv_h2;
+  const double E = (((t[i - 1 - SY] + t[i + 1 - SY]) + (t[i - 1 + SY] + t[i + 1 + SY])) +
+                    ((t[i - 1 - SZ] + t[i + 1 - SZ]) + (t[i - 1 + SZ] + t[i + 1 + SZ]))) +
+                   ((t[i - SY - SZ] + t[i + SY - SZ]) + (t[i - SY + SZ] + t[i + SY + SZ]));
+  return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+}
+
+template <int ORDER>
+__device__ __forceinline__ double lap_fetch(const double* __restrict__ u, const int32_t* __restrict__ nb, int B,
+                                            int x, int y, int z, double inv_h2) {
+  auto g = [&](int a, int b, int c) { return fetch(u, nb, B, x + a, y + b, z + c); };
+  const double c = g(0, 0, 0);
+  const double F = ((g(-1, 0, 0) + g(1, 0, 0)) + (g(0, -1, 0) + g(0, 1, 0))) + (g(0, 0, -1) + g(0, 0, 1));
+  if (ORDER == 2) return (F - 6.0 * c) * inv_h2;
+  const double E = (((g(-1, -1, 0) + g(1, -1, 0)) + (g(-1, 1, 0) + g(1, 1, 0))) +
+                    ((g(-1, 0, -1) + g(1, 0, -1)) + (g(-1, 0, 1) + g(1, 0, 1)))) +
+                   ((g(0, -1, -1) + g(0, 1, -1)) + (g(0, -1, 1) + g(0, 1, 1)));
+  return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+}
+
+// ---------------------------------------------------------------------------------
+// Fused smoother (+ residual).  One CTA per real block.  The block and a halo of
+// H = (#update passes) + (residual ? 1 : 0) nodes are staged in shared memory;
+// each pass updates the live nodes (own block or real neighbour block; ghost-block
+// nodes are frozen, reading Z9) of a region that shrinks by one node per pass, so
+// red, black and the residual all come out of one HBM read of u and f.
+// Jacobi: u += ω (f - Δu)/d on all nodes of the region from the snapshot.
+// RB:     red (even level-global parity) then black, each from a snapshot (Z10).
+// The smoothed block goes to u_out (ping-pong: neighbours read the old u).
+// ---------------------------------------------------------------------------------
+template <int B, int ORDER, int MODE, bool RES, int NT>
+__global__ void __launch_bounds__(NT) k_smooth(LevelView L, double omega, double inv_h2, double inv_d) {
+  constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
+  constexpr int H = NS + (RES ? 1 : 0);
+  constexpr int T = B + 2 * H;
+  constexpr int B3 = B * B * B;
+  // staged updates per thread for the largest pass
+  constexpr int R0 = B + 2 * (H - 1);
+  constexpr int MAXU = MODE == SM_RB ? (R0 * R0 * R0 / 2 + NT - 1) / NT : (R0 * R0 * R0 + NT - 1) / NT;
+  extern __shared__ double tile[];
+  const int b = blockIdx.x;
+  const int32_t* nb = L.nbr + (size_t)b * 27;
+  const uint32_t realbits = L.nbr_real[b];
+
+  for (int i = threadIdx.x; i < T * T * T; i += NT) {
+    const int x = i % T - H, y = (i / T) % T - H, z = i / (T * T) - H;
+    tile[i] = fetch(L.u, nb, B, x, y, z);
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int p = 0; p < NS; ++p) {
+    const int e = H - 1 - p;  // region [-e, B+e)^3
+    const int R = B + 2 * e;
+    const int colour = p;     // RB: pass 0 = red (even), pass 1 = black (odd)
+    const int cnt = MODE == SM_RB ? R * R * R / 2 : R * R * R;
+    double stage[MAXU];
+#pragma unroll
+    for (int k = 0; k < MAXU; ++k) {
+      const int i = threadIdx.x + k * NT;
+      stage[k] = 0.0;
+      if (i < cnt) {
+        int x, y, z;
+        if (MODE == SM_RB) {
+          const int R2 = R / 2;
+          z = i / (R * R2);
+          const int rem = i - z * R * R2;
+          y = rem / R2;
+          const int xi = rem - y * R2;
+          x = 2 * xi + ((colour + y + z + e) & 1);
+        } else {
+          z = i / (R * R);
+          const int rem = i - z * R * R;
+          y = rem / R;
+          x = rem - y * R;
+        }
+        x -= e; y -= e; z -= e;
+        const int s = (region(x, B) + 1) + 3 * (region(y, B) + 1) + 9 * (region(z, B) + 1);
+        if ((realbits >> s) & 1u) {
+          const int ti = ((z + H) * T + (y + H)) * T + (x + H);
+          const double c = tile[ti];
+          const double f = fetch(L.f, nb, B, x, y, z);
+          stage[k] = c + omega * (f - lap_tile<ORDER, T>(tile, ti, inv_h2)) * inv_d;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MAXU; ++k) {
+      const int i = threadIdx.x + k * NT;
+      if (i < cnt) {
+        int x, y, z;
+        if (MODE == SM_RB) {
+          const int R2 = R / 2;
+          z = i / (R * R2);
+          const int rem = i - z * R * R2;
+          y = rem / R2;
+          const int xi = rem - y * R2;
+          x = 2 * xi + ((colour + y + z + e) & 1);
+        } else {
+          z = i / (R * R);
+          const int rem = i - z * R * R;
+          y = rem / R;
+          x = rem - y * R;
+        }
+        x -= e; y -= e; z -= e;
+        const int s = (region(x, B) + 1) + 3 * (region(y, B) + 1) + 9 * (region(z, B) + 1);
+        if ((realbits >> s) & 1u) tile[((z + H) * T + (y + H)) * T + (x + H)] = stage[k];
+      }
+    }
+    __syncthreads();
+  }
+
+  double* uo = (NS > 0) ? L.u_out + (size_t)b * B3 : nullptr;
+  for (int i = threadIdx.x; i < B3; i += NT) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int ti = ((z + H) * T + (y + H)) * T + (x + H);
+    if (NS > 0) uo[i] = tile[ti];
+    if (RES) L.r[(size_t)b * B3 + i] = L.f[(size_t)b * B3 + i] - lap_tile<ORDER, T>(tile, ti, inv_h2);
+  }
+}
+
+template <int B, int ORDER, int MODE, bool RES>
+static void smooth_inst(const LevelView& L, double omega, double inv_h2, double inv_d, cudaStream_t s,
+                        bool prepare_only = false) {
+  constexpr int NT = B >= 16 ? 256 : (B >= 8 ? 128 : 64);
+  constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
+  constexpr int H = NS + (RES ? 1 : 0);
+  constexpr int T = B + 2 * H;
+  const size_t smem = sizeof(double) * T * T * T;
+  auto k = k_smooth<B, ORDER, MODE, RES, NT>;
+  if (prepare_only) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return;
+  }
+  if (L.nreal > 0) k<<<L.nreal, NT, smem, s>>>(L, omega, inv_h2, inv_d);
+}
+
+template <int B, int ORDER>
+static void prepare_b() {
+  LevelView L{};
+  smooth_inst<B, ORDER, SM_RB, true>(L, 0, 0, 0, 0, true);
+  smooth_inst<B, ORDER, SM_RB, false>(L, 0, 0, 0, 0, true);
+  smooth_inst<B, ORDER, SM_JACOBI, true>(L, 0, 0, 0, 0, true);
+  smooth_inst<B, ORDER, SM_JACOBI, false>(L, 0, 0, 0, 0, true);
+  smooth_inst<B, ORDER, -1, true>(L, 0, 0, 0, 0, true);
+}
+
+template <int B, int ORDER>
+static void smooth_dispatch_b(const LevelView& L, int mode, double omega, bool res, double inv_h2, double inv_d,
+                              cudaStream_t s) {
+  if (mode == SM_RB) {
+    if (res) smooth_inst<B, ORDER, SM_RB, true>(L, omega, inv_h2, inv_d, s);
+    else smooth_inst<B, ORDER, SM_RB, false>(L, omega, inv_h2, inv_d, s);
+  } else if (mode == SM_JACOBI) {
+    if (res) smooth_inst<B, ORDER, SM_JACOBI, true>(L, omega, inv_h2, inv_d, s);
+    else smooth_inst<B, ORDER, SM_JACOBI, false>(L, omega, inv_h2, inv_d, s);
+  } else {
+    smooth_inst<B, ORDER, -1, true>(L, omega, inv_h2, inv_d, s);
+  }
+}
+
+template <int ORDER>
+static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res, cudaStream_t s) {
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  const double d = (ORDER == 2 ? -6.0 : -4.0) * inv_h2;  // centre coefficient of Δ_h^M
+  const double inv_d = 1.0 / d;
+  switch (L.B) {
+    case 16: smooth_dispatch_b<16, ORDER>(L, mode, omega, res, inv_h2, inv_d, s); break;
+    case 8: smooth_dispatch_b<8, ORDER>(L, mode, omega, res, inv_h2, inv_d, s); break;
+    case 4: smooth_dispatch_b<4, ORDER>(L, mode, omega, res, inv_h2, inv_d, s); break;
+    default: break;
+  }
+}
+
+void prepare_kernels() {
+  upload_weights();
+  prepare_b<16, 2>(); prepare_b<16, 4>();
+  prepare_b<8, 2>(); prepare_b<8, 4>();
+  prepare_b<4, 2>(); prepare_b<4, 4>();
+}
+
+void launch_smooth(const LevelView& L, int order, int mode, double omega, bool with_residual, cudaStream_t s) {
+  if (order == 2) smooth_dispatch<2>(L, mode, omega, with_residual, s);
+  else smooth_dispatch<4>(L, mode, omega, with_residual, s);
+}
+
+void launch_residual(const LevelView& L, int order, cudaStream_t s) {
+  if (order == 2) smooth_dispatch<2>(L, -1, 0.0, true, s);
+  else smooth_dispatch<4>(L, -1, 0.0, true, s);
+}
+
+// ---------------------------------------------------------------------------------
+// Boundary ghosts: c2f tensor-product Lagrange interpolation (a1-iii) from the
+// coarse level's current values (already f2c-injected), one thread per entry.
+// Summation order x, then y, then z (mirrors the separable definition).
+// ---------------------------------------------------------------------------------
+template <int I>
+__global__ void k_c2f(C2FList g, double* __restrict__ ff, const double* __restrict__ cf, LevelView C, bool ext_zero) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  if (ext_zero && g.ext[i]) {
+    ff[g.dst[i]] = 0.0;
+    return;
+  }
+  int nt[3], cb[3][I], cl[3][I];
+  double w[3][I];
+  for (int a = 0; a < 3; ++a) {
+    const int J = g.J[3 * i + a];
+    int base, n;
+    if ((J & 1) == 0) {
+      n = 1;
+      base = J >> 1;  // arithmetic shift = floor(J/2) for even J
+      w[a][0] = 1.0;
+    } else {
+      n = I;
+      base = ((J - 1) >> 1) - I / 2 + 1;
+      for (int t = 0; t < I; ++t) w[a][t] = (I == 4) ? c_w4[t] : c_w6[t];
+    }
+    nt[a] = n;
+    for (int t = 0; t < n; ++t) {
+      int ci = base + t;
+      if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
+      const int blk = floordiv(ci, C.B);
+      cb[a][t] = blk - C.bmap_lo[a];
+      cl[a][t] = ci - blk * C.B;
+    }
+  }
+  double sz = 0.0;
+  for (int tz = 0; tz < nt[2]; ++tz) {
+    double sy = 0.0;
+    for (int ty = 0; ty < nt[1]; ++ty) {
+      double sx = 0.0;
+      const int rowmap = (cb[2][tz] * C.bmap_n[1] + cb[1][ty]) * C.bmap_n[0];
+      for (int tx = 0; tx < nt[0]; ++tx) {
+        const int blk = __ldg(C.bmap + rowmap + cb[0][tx]);
+        const double v = cf[(size_t)blk * C.B3 + (cl[2][tz] * C.B + cl[1][ty]) * C.B + cl[0][tx]];
+        sx += w[0][tx] * v;
+      }
+      sy += w[1][ty] * sx;
+    }
+    sz += w[2][tz] * sy;
+  }
+  ff[g.dst[i]] = sz;
+}
+
+void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
+                const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
+  if (g.n == 0) return;
+  const int nt = 128, nb = (g.n + nt - 1) / nt;
+  if (I == 4) k_c2f<4><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero);
+  else k_c2f<6><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero);
+}
+
+__global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                            double* __restrict__ d, const double* __restrict__ sv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[dst[i]] = sv[src[i]];
+}
+
+void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s) {
+  if (l.n == 0) return;
+  k_copy_list<<<(l.n + 255) / 256, 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field);
+}
+
+// ---------------------------------------------------------------------------------
+// Restriction (Alg. 1): per fine real block, over the coarse sub-box it
+// covers in its parent: u_c <- u_f(2i) (E7), r_c <- FW(r_f) (E6); r of ghost blocks
+// is never written and stays 0 (reading Z14).
+// ---------------------------------------------------------------------------------
+__global__ void k_restrict(LevelView F, LevelView C) {
+  const int b = blockIdx.x;
+  const int B = F.B, Bh = B / 2;
+  const int32_t* nb = F.nbr + (size_t)b * 27;
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  for (int i = threadIdx.x; i < Bh * Bh * Bh; i += blockDim.x) {
+    const int cx = i % Bh, cy = (i / Bh) % Bh, cz = i / (Bh * Bh);
+    const int x = 2 * cx, y = 2 * cy, z = 2 * cz;
+    const size_t ci = (size_t)p * C.B3 + ((oz + cz) * C.B + (oy + cy)) * C.B + (ox + cx);
+    C.u[ci] = F.u[(size_t)b * F.B3 + (z * B + y) * B + x];
+    double sz = 0.0;
+    for (int dz = -1; dz <= 1; ++dz) {
+      double sy = 0.0;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const double sx = 0.25 * fetch(F.r, nb, B, x - 1, y + dy, z + dz) + 0.5 * fetch(F.r, nb, B, x, y + dy, z + dz) +
+                          0.25 * fetch(F.r, nb, B, x + 1, y + dy, z + dz);
+        sy += (dy == 0 ? 0.5 : 0.25) * sx;
+      }
+      sz += (dz == 0 ? 0.5 : 0.25) * sy;
+    }
+    C.r[ci] = sz;
+  }
+}
+
+void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
+  if (fine.nreal) k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse);
+}
+
+// FAS right-hand side on the covered coarse nodes (Alg. 1): f = r + Δ u.
+template <int ORDER>
+__global__ void k_fas_rhs(LevelView F, LevelView C) {
+  const int b = blockIdx.x;
+  const int Bh = F.B / 2;
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  const int32_t* nb = C.nbr + (size_t)p * 27;
+  const double inv_h2 = 1.0 / (C.h * C.h);
+  for (int i = threadIdx.x; i < Bh * Bh * Bh; i += blockDim.x) {
+    const int x = ox + i % Bh, y = oy + (i / Bh) % Bh, z = oz + i / (Bh * Bh);
+    const size_t ci = (size_t)p * C.B3 + (z * C.B + y) * C.B + x;
+    C.f[ci] = C.r[ci] + lap_fetch<ORDER>(C.u, nb, C.B, x, y, z, inv_h2);
+  }
+}
+
+void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
+  if (!fine.nreal) return;
+  if (order == 2) k_fas_rhs<2><<<fine.nreal, 256, 0, s>>>(fine, coarse);
+  else k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse);
+}
+
+// Prolongation of the correction (Alg. 1): u_f += trilinear(u_c - û_c).
+__global__ void k_prolong(LevelView F, LevelView C) {
+  const int b = blockIdx.x;
+  const int B = F.B;
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  const int32_t* nb = C.nbr + (size_t)p * 27;
+  for (int i = threadIdx.x; i < F.B3; i += blockDim.x) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int cx = ox + (x >> 1), cy = oy + (y >> 1), cz = oz + (z >> 1);
+    const int nx = (x & 1) ? 2 : 1, ny = (y & 1) ? 2 : 1, nzc = (z & 1) ? 2 : 1;
+    double vz[2];
+    for (int tz = 0; tz < nzc; ++tz) {
+      double vy[2];
+      for (int ty = 0; ty < ny; ++ty) {
+        double vx[2];
+        for (int tx = 0; tx < nx; ++tx)
+          vx[tx] = fetch(C.u, nb, C.B, cx + tx, cy + ty, cz + tz) - fetch(C.uhat, nb, C.B, cx + tx, cy + ty, cz + tz);
+        vy[ty] = nx == 2 ? 0.5 * (vx[0] + vx[1]) : vx[0];
+      }
+      vz[tz] = ny == 2 ? 0.5 * (vy[0] + vy[1]) : vy[0];
+    }
+    const double e = nzc == 2 ? 0.5 * (vz[0] + vz[1]) : vz[0];
+    double* uf = F.u + (size_t)b * F.B3 + i;
+    *uf = *uf + e;
+  }
+}
+
+void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
+  if (fine.nreal) k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse);
+}
+
+__global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
+  const int b = blockIdx.x;
+  const int B = F.B, Bh = B / 2;
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  for (int i = threadIdx.x; i < Bh * Bh * Bh; i += blockDim.x) {
+    const int cx = i % Bh, cy = (i / Bh) % Bh, cz = i / (Bh * Bh);
+    cu[(size_t)p * C.B3 + ((oz + cz) * C.B + (oy + cy)) * C.B + (ox + cx)] =
+        F.u[(size_t)b * F.B3 + ((2 * cz) * B + 2 * cy) * B + 2 * cx];
+  }
+}
+
+void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s) {
+  if (fine.nreal) k_inject_up<<<fine.nreal, 256, 0, s>>>(fine, coarse, coarse_u);
+}
+
+// ---------------------------------------------------------------------------------
+// Norms over leaf nodes (a9): max |f - Δu| (residual) or max |f| (‖f*‖∞); warp
+// shuffle max, one 64-bit atomicMax per CTA on the bit pattern (non-negative
+// doubles order like their bit patterns; NaN patterns sort above +Inf).
+// ---------------------------------------------------------------------------------
+template <int ORDER>
+__global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
+  const int b = blockIdx.x;
+  const int B = L.B, Bh = B / 2;
+  const int32_t* nb = L.nbr + (size_t)b * 27;
+  const uint8_t cov = L.covmask[b];
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  unsigned long long m = 0ull;
+  for (int i = threadIdx.x; i < L.B3; i += blockDim.x) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int oct = (x >= Bh) | ((y >= Bh) << 1) | ((z >= Bh) << 2);
+    if ((cov >> oct) & 1) continue;
+    double v = L.f[(size_t)b * L.B3 + i];
+    if (residual) v -= lap_fetch<ORDER>(L.u, nb, B, x, y, z, inv_h2);
+    v = fabs(v);
+    unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+    if (v != v) bits = 0x7ff8000000000000ull;
+    m = bits > m ? bits : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+    m = t > m ? t : m;
+  }
+  __shared__ unsigned long long sm[32];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = 0ull;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = sm[w] > r ? sm[w] : r;
+    atomicMax(out, r);
+  }
+}
+
+void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s) {
+  if (!L.nreal) return;
+  if (order == 2) k_norm<2><<<L.nreal, 256, 0, s>>>(L, residual, out);
+  else k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out);
+}
+
+// R_h^M f on all real nodes into tmp (M=4: f + (1/12)Σδ²f, right side of E12), then
+// f <- tmp on leaf nodes only (reading Z16).
+__global__ void k_rhs_apply(LevelView L, double* tmp) {
+  const int b = blockIdx.x;
+  const int B = L.B;
+  const int32_t* nb = L.nbr + (size_t)b * 27;
+  for (int i = threadIdx.x; i < L.B3; i += blockDim.x) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const double c = L.f[(size_t)b * L.B3 + i];
+    const double dx = (fetch(L.f, nb, B, x - 1, y, z) - 2.0 * c) + fetch(L.f, nb, B, x + 1, y, z);
+    const double dy = (fetch(L.f, nb, B, x, y - 1, z) - 2.0 * c) + fetch(L.f, nb, B, x, y + 1, z);
+    const double dz = (fetch(L.f, nb, B, x, y, z - 1) - 2.0 * c) + fetch(L.f, nb, B, x, y, z + 1);
+    tmp[(size_t)b * L.B3 + i] = c + ((dx + dy) + dz) / 12.0;
+  }
+}
+
+__global__ void k_rhs_commit(LevelView L, const double* tmp) {
+  const int b = blockIdx.x;
+  const int B = L.B, Bh = B / 2;
+  const uint8_t cov = L.covmask[b];
+  for (int i = threadIdx.x; i < L.B3; i += blockDim.x) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int oct = (x >= Bh) | ((y >= Bh) << 1) | ((z >= Bh) << 2);
+    if (!((cov >> oct) & 1)) L.f[(size_t)b * L.B3 + i] = tmp[(size_t)b * L.B3 + i];
+  }
+}
+
+void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s) {
+  if (!L.nreal || order == 2) return;
+  k_rhs_apply<<<L.nreal, 256, 0, s>>>(L, tmp);
+  k_rhs_commit<<<L.nreal, 256, 0, s>>>(L, tmp);
+}
+
+// leaf-ordered [n_leaf][B^3] <-> level block storage
+__global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const double* __restrict__ src,
+                               double* const* __restrict__ dst, bool to_levels) {
+  const int n = blockIdx.x;
+  const int64_t m = map[n];
+  const int lev = (int)(m >> 32), blk = (int)(m & 0xffffffff);
+  double* d = dst[lev] + (size_t)blk * B3;
+  const double* sl = src + (size_t)n * B3;
+  if (to_levels) {
+    for (int i = threadIdx.x; i < B3; i += blockDim.x) d[i] = sl[i];
+  } else {
+    double* o = const_cast<double*>(sl);
+    for (int i = threadIdx.x; i < B3; i += blockDim.x) o[i] = d[i];
+  }
+}
+
+void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
+                         int nlev, bool to_levels, cudaStream_t s) {
+  (void)nlev;
+  if (nleaf) k_leaf_scatter<<<nleaf, 256, 0, s>>>(B3, map, src, dst_by_level, to_levels);
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+
+void launch_zero(double* p, int64_t n, cudaStream_t s) {
+  if (n) k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, 0.0);
+}
+
+// ---------------------------------------------------------------------------------
+// Coarse direct solve (a6) around cuFFT (library call, timed separately).
+// ---------------------------------------------------------------------------------
+__global__ void k_coarse_gather(LevelView L, double* dense, int Px, int Py, int Pz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Px * Py * Pz;
+  if (i >= n) return;
+  const int x = (int)(i % Px), y = (int)((i / Px) % Py), z = (int)(i / ((int64_t)Px * Py));
+  double v = 0.0;
+  if (x < L.N[0] && y < L.N[1] && z < L.N[2]) {
+    const int bx = x / L.B, by = y / L.B, bz = z / L.B;
+    const int blk = L.bmap[((bz - L.bmap_lo[2]) * L.bmap_n[1] + (by - L.bmap_lo[1])) * L.bmap_n[0] + (bx - L.bmap_lo[0])];
+    v = L.f[(size_t)blk * L.B3 + ((z - bz * L.B) * L.B + (y - by * L.B)) * L.B + (x - bx * L.B)];
+  }
+  dense[i] = v;
+}
+
+void launch_coarse_gather(const LevelView& L, double* dense, const int* P, cudaStream_t s) {
+  const int64_t n = (int64_t)P[0] * P[1] * P[2];
+  k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1], P[2]);
+}
+
+__global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, int Px, int Py) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
+  if (i >= n) return;
+  const int x = (int)(i % L.N[0]), y = (int)((i / L.N[0]) % L.N[1]), z = (int)(i / ((int64_t)L.N[0] * L.N[1]));
+  const int bx = x / L.B, by = y / L.B, bz = z / L.B;
+  const int blk = L.bmap[((bz - L.bmap_lo[2]) * L.bmap_n[1] + (by - L.bmap_lo[1])) * L.bmap_n[0] + (bx - L.bmap_lo[0])];
+  L.u[(size_t)blk * L.B3 + ((z - bz * L.B) * L.B + (y - by * L.B)) * L.B + (x - bx * L.B)] =
+      dense[((int64_t)z * Py + y) * Px + x];
+}
+
+__global__ void k_coarse_band(C2FList g, double* u, const double* __restrict__ dense, int Px, int Py, int Pz) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int P[3] = {Px, Py, Pz};
+  int q[3];
+  for (int a = 0; a < 3; ++a) q[a] = ((g.J[3 * i + a] % P[a]) + P[a]) % P[a];
+  u[g.dst[i]] = dense[((int64_t)q[2] * Py + q[1]) * Px + q[0]];
+}
+
+void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const C2FList& band,
+                           cudaStream_t s) {
+  const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
+  k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1]);
+  if (band.n) k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, P[0], P[1], P[2]);
+}
+
+// spectral symbol σ_M(θ) h² from ŝ = 2cosθ - 2
+__device__ __forceinline__ double symbol_h2(int order, double sx, double sy, double sz) {
+  double s = sx + sy + sz;
+  if (order >= 4) s += (sx * sy + sy * sz + sz * sx) * (1.0 / 6.0);
+  return s;
+}
+
+// periodic: û /= σ, zero mode -> 0; includes the 1/(PxPyPz) inverse scale
+__global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, int order, double h2) {
+  const int Hx = Px / 2 + 1;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Hx * Py * Pz;
+  if (i >= n) return;
+  const int kx = (int)(i % Hx), ky = (int)((i / Hx) % Py), kz = (int)(i / ((int64_t)Hx * Py));
+  const double tw = 6.283185307179586476925286766559;
+  const double sx = 2.0 * cos(tw * kx / Px) - 2.0, sy = 2.0 * cos(tw * ky / Py) - 2.0, sz = 2.0 * cos(tw * kz / Pz) - 2.0;
+  const double sig = symbol_h2(order, sx, sy, sz);
+  const double scale = 1.0 / ((double)Px * Py * Pz);
+  const double m = (kx == 0 && ky == 0 && kz == 0) ? 0.0 : h2 / sig * scale;
+  spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
+}
+
+void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s) {
+  const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
+  k_mul_periodic<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h);
+}
+
+__global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mult, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double m = mult[i];
+  spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
+}
+
+void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s) {
+  k_mul_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n);
+}
+
+// x periodic, y/z unbounded (E14 with the periodic axis x, reading Z22):
+// k_x = 0 -> 2D LGF multiplier table (already × h² / (PxPyPz)); else 1/σ on the padded lattice
+__global__ void k_mul_puu(cuDoubleComplex* spec, int Px, int Py, int Pz, int order, double h2,
+                          const double* __restrict__ tab2) {
+  const int Hx = Px / 2 + 1;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Hx * Py * Pz;
+  if (i >= n) return;
+  const int kx = (int)(i % Hx), ky = (int)((i / Hx) % Py), kz = (int)(i / ((int64_t)Hx * Py));
+  double m;
+  if (kx == 0) {
+    m = tab2[(int64_t)kz * Py + ky];
+  } else {
+    const double tw = 6.283185307179586476925286766559;
+    const double sx = 2.0 * cos(tw * kx / Px) - 2.0, sy = 2.0 * cos(tw * ky / Py) - 2.0,
+                 sz = 2.0 * cos(tw * kz / Pz) - 2.0;
+    m = h2 / symbol_h2(order, sx, sy, sz) / ((double)Px * Py * Pz);
+  }
+  spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
+}
+
+void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s) {
+  const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
+  k_mul_puu<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h, tab2);
+}
+
+__global__ void k_scale(double* p, int64_t n, double a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] *= a;
+}
+
+void launch_scale(double* p, int64_t n, double a, cudaStream_t s) {
+  if (n) k_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, a);
+}
+
+__global__ void k_real_part_scale(const cuDoubleComplex* c, double* out, int64_t n, double a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = cuCreal(c[i]) * a;
+}
+
+void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s) {
+  if (n) k_real_part_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const cuDoubleComplex*)cplx, out, n, a);
+}
+
+}  // namespace mg

@@ -1,0 +1,213 @@
+"""Thin ctypes binding of libmg.so (include/mg.h): argument marshalling only.
+
+Every step of the solve runs in the library's CUDA kernels (plus cuFFT for the
+coarse level).  There is no CPU fallback: if libmg.so or a CUDA device is
+missing, construction raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmg.so")
+
+MG_BC_PERIODIC, MG_BC_UNBOUNDED = 0, 1
+MG_SMOOTHER_JACOBI, MG_SMOOTHER_RBGS = 0, 1
+MG_CRIT_RESIDUAL, MG_CRIT_CAUCHY = 0, 1
+MG_FIELD_U, MG_FIELD_F, MG_FIELD_R, MG_FIELD_UHAT = 0, 1, 2, 3
+OPS = dict(refresh=0, smooth=1, residual=2, restrict=3, prolong=4, inject_up=5, coarse_solve=6,
+           smooth_residual=7)
+MG_OK, MG_WARN_NOT_CONVERGED = 0, 1
+
+EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
+           "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
+           "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op"]
+
+
+class MgDesc(C.Structure):
+    _fields_ = [("origin", C.c_double * 3), ("h0", C.c_double), ("base_blocks", C.c_int32 * 3),
+                ("block_size", C.c_int32), ("bc", C.c_int32 * 6), ("order", C.c_int32),
+                ("coarse_n", C.c_int32), ("smoother", C.c_int32), ("omega", C.c_double),
+                ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
+                ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32))]
+
+
+class MgError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"libmg error {code}: {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def load_library(path: str = _LIB_PATH):
+    """Load libmg.so (fails loudly when the CUDA extension has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} missing: run `python -m paper_2512_08555_b200.build` (nvcc, sm_100a)")
+    lib = C.CDLL(path)
+    P, I, D = C.c_void_p, C.c_int, C.c_double
+    lib.mg_create.argtypes = [C.POINTER(MgDesc), P, C.POINTER(P)]
+    lib.mg_destroy.argtypes = [P]
+    lib.mg_destroy.restype = None
+    lib.mg_last_error.argtypes = [P]
+    lib.mg_last_error.restype = C.c_char_p
+    for name in ("mg_set_rhs", "mg_set_solution", "mg_get_solution"):
+        getattr(lib, name).argtypes = [P, P]
+    lib.mg_vcycle.argtypes = [P, I]
+    lib.mg_residual_norm.argtypes = [P, C.POINTER(D), C.POINTER(D)]
+    lib.mg_solve.argtypes = [P, D, I, I, C.POINTER(I), C.POINTER(D)]
+    lib.mg_run_host.argtypes = [P, P, P, I, C.POINTER(D)]
+    lib.mg_use_graph.argtypes = [P, I]
+    lib.mg_level_info.argtypes = [P, I, C.POINTER(C.c_int64)]
+    lib.mg_level_blocks.argtypes = [P, I, C.POINTER(C.c_int32)]
+    lib.mg_num_levels.argtypes = [P]
+    lib.mg_debug_field.argtypes = [P, I, I, I, P]
+    lib.mg_debug_apply.argtypes = [P, I, I]
+    lib.mg_time_op.argtypes = [P, I, I, I, C.POINTER(D)]
+    for name in EXPORTS:
+        if name not in ("mg_destroy", "mg_last_error"):
+            getattr(lib, name).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _ptr(t):
+    """Device pointer of a CUDA tensor (contiguous fp64)."""
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+class Solver:
+    """Handle of one solver instance (mg_create ... mg_destroy)."""
+
+    def __init__(self, cfg: dict, leaves: np.ndarray, stream=None):
+        import torch
+        self.lib = load_library()
+        self.torch = torch
+        lv = np.ascontiguousarray(np.asarray(leaves, dtype=np.int32).reshape(-1, 4))
+        self._leaves = lv
+        d = MgDesc()
+        d.origin[:] = [float(v) for v in cfg["origin"]]
+        d.h0 = float(cfg["h0"])
+        d.base_blocks[:] = [int(v) for v in cfg["base_blocks"]]
+        d.block_size = int(cfg["B"])
+        bc = [int(v) for v in cfg["bc"]]
+        d.bc[:] = [bc[0], bc[0], bc[1], bc[1], bc[2], bc[2]]
+        d.order = int(cfg["order"])
+        d.coarse_n = int(cfg.get("coarse_n", 0) or 0)
+        d.smoother = int(cfg["smoother"])
+        d.omega = float(cfg["omega"])
+        d.eta1 = int(cfg["eta1"])
+        d.eta2 = int(cfg["eta2"])
+        d.allow_unbounded_refined = int(cfg.get("allow_unbounded_refined", 0))
+        d.n_leaf = len(lv)
+        d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))
+        self.B = int(cfg["B"])
+        self.n_leaf = len(lv)
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        self.stream = stream
+        h = C.c_void_p()
+        self._check(self.lib.mg_create(C.byref(d), C.c_void_p(stream.cuda_stream), C.byref(h)), None)
+        self.h = h
+
+    # ---------------------------------------------------------------- helpers
+    def _check(self, rc, h="self"):
+        if rc < 0:
+            hh = self.h if h == "self" else None
+            raise MgError(rc, self.lib.mg_last_error(hh).decode())
+        return rc
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def leaf_shape(self):
+        return (self.n_leaf, self.B, self.B, self.B)
+
+    # ---------------------------------------------------------------- API
+    def set_rhs(self, f):
+        self._check(self.lib.mg_set_rhs(self.h, _ptr(f)))
+
+    def set_solution(self, u):
+        self._check(self.lib.mg_set_solution(self.h, _ptr(u)))
+
+    def get_solution(self, out=None):
+        t = self.torch
+        if out is None:
+            out = t.empty(self.leaf_shape(), dtype=t.float64, device="cuda")
+        self._check(self.lib.mg_get_solution(self.h, _ptr(out)))
+        return out
+
+    def vcycle(self, n=1):
+        self._check(self.lib.mg_vcycle(self.h, int(n)))
+
+    def residual_norm(self):
+        a, r = C.c_double(), C.c_double()
+        self._check(self.lib.mg_residual_norm(self.h, C.byref(a), C.byref(r)))
+        return a.value, r.value
+
+    def solve(self, tol, max_cycles=50, criterion=MG_CRIT_RESIDUAL):
+        c, v = C.c_int(), C.c_double()
+        rc = self._check(self.lib.mg_solve(self.h, float(tol), int(max_cycles), int(criterion), C.byref(c),
+                                           C.byref(v)))
+        return c.value, v.value, rc == MG_OK
+
+    def run_host(self, f_host: np.ndarray, u_host: np.ndarray, ncycles: int) -> float:
+        r = C.c_double()
+        self._check(self.lib.mg_run_host(self.h, C.c_void_p(f_host.ctypes.data), C.c_void_p(u_host.ctypes.data),
+                                         int(ncycles), C.byref(r)))
+        return r.value
+
+    def use_graph(self, on=True):
+        self._check(self.lib.mg_use_graph(self.h, 1 if on else 0))
+
+    def num_levels(self):
+        return self._check(self.lib.mg_num_levels(self.h))
+
+    def level_info(self, m):
+        info = (C.c_int64 * 10)()
+        self._check(self.lib.mg_level_info(self.h, int(m), info))
+        keys = ["B", "nreal", "nghost", "Nx", "Ny", "Nz", "amr", "n_c2f", "n_inject", "n_leaf_blocks"]
+        return dict(zip(keys, list(info)))
+
+    def level_blocks(self, m):
+        n = self.level_info(m)["nreal"]
+        out = np.zeros((n, 3), dtype=np.int32)
+        self._check(self.lib.mg_level_blocks(self.h, int(m), out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
+    def debug_field(self, field, m, tensor=None):
+        """Export (tensor None) or import a level field [nreal, B, B, B]."""
+        t = self.torch
+        info = self.level_info(m)
+        if tensor is None:
+            out = t.empty((info["nreal"], info["B"], info["B"], info["B"]), dtype=t.float64, device="cuda")
+            self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 0, _ptr(out)))
+            return out
+        self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 1, _ptr(tensor)))
+
+    def debug_apply(self, op, m):
+        self._check(self.lib.mg_debug_apply(self.h, OPS[op] if isinstance(op, str) else int(op), int(m)))
+
+    def time_op(self, op, m, reps):
+        ms = C.c_double()
+        code = {"smooth_kernel": -1, "vcycle": 100}.get(op, OPS.get(op, op)) if isinstance(op, str) else op
+        self._check(self.lib.mg_time_op(self.h, int(code), int(m), int(reps), C.byref(ms)))
+        return ms.value

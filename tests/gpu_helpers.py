@@ -1,0 +1,68 @@
+"""Helpers shared by the -m gpu parity tests: map between the GPU's per-level block
+storage (exported through mg_debug_field) and the oracle's dense level lattices."""
+import numpy as np
+
+
+def blocks_to_dense(blocks, coords, B, N, fill=np.nan):
+    """blocks [n, B, B, B] ([b, z, y, x]) at block coords -> dense [Nx, Ny, Nz]."""
+    out = np.full(tuple(N), fill)
+    for b, (i, j, k) in enumerate(coords.tolist()):
+        out[i * B:(i + 1) * B, j * B:(j + 1) * B, k * B:(k + 1) * B] = blocks[b].transpose(2, 1, 0)
+    return out
+
+
+def dense_to_blocks(dense, coords, B):
+    out = np.empty((len(coords), B, B, B))
+    for b, (i, j, k) in enumerate(coords.tolist()):
+        out[b] = dense[i * B:(i + 1) * B, j * B:(j + 1) * B, k * B:(k + 1) * B].transpose(2, 1, 0)
+    return out
+
+
+def rel_err(a, b, denom=None):
+    a = np.asarray(a)
+    b = np.asarray(b)
+    d = np.abs(a - b).max()
+    s = np.abs(b).max() if denom is None else denom
+    return d / s if s > 0 else d
+
+
+class Pair:
+    """An oracle and a GPU solver built from the same config, leaves and f."""
+
+    def __init__(self, cfg, leaves, f):
+        import torch
+
+        from oracle.mg_oracle import Oracle
+        from paper_2512_08555_b200 import Solver
+
+        self.torch = torch
+        self.o = Oracle(cfg, leaves)
+        self.g = Solver(cfg, leaves)
+        self.f = f
+        self.o.set_rhs(f)
+        self.g.set_rhs(torch.from_numpy(np.ascontiguousarray(f)).cuda())
+        assert self.g.num_levels() == len(self.o.levels)
+        self.coords = [self.g.level_blocks(m) for m in range(self.g.num_levels())]
+        self.B = [self.g.level_info(m)["B"] for m in range(self.g.num_levels())]
+
+    def gpu_field(self, field, m):
+        from paper_2512_08555_b200 import MG_FIELD_F, MG_FIELD_R, MG_FIELD_U, MG_FIELD_UHAT
+        code = dict(u=MG_FIELD_U, f=MG_FIELD_F, r=MG_FIELD_R, uhat=MG_FIELD_UHAT)[field]
+        t = self.g.debug_field(code, m).cpu().numpy()
+        return blocks_to_dense(t, self.coords[m], self.B[m], self.o.levels[m].N)
+
+    def push(self, field, m, dense):
+        from paper_2512_08555_b200 import MG_FIELD_F, MG_FIELD_R, MG_FIELD_U, MG_FIELD_UHAT
+        code = dict(u=MG_FIELD_U, f=MG_FIELD_F, r=MG_FIELD_R, uhat=MG_FIELD_UHAT)[field]
+        t = self.torch.from_numpy(dense_to_blocks(dense, self.coords[m], self.B[m])).cuda()
+        self.g.debug_field(code, m, t)
+
+    def push_state(self):
+        """Copy the oracle's u, f, uhat on every level into the GPU level storage."""
+        for m, L in enumerate(self.o.levels):
+            self.push("u", m, L.u)
+            self.push("f", m, L.f)
+            self.push("uhat", m, L.uhat)
+
+    def solution(self):
+        return self.g.get_solution().cpu().numpy()
