@@ -138,6 +138,16 @@ int mg_debug_apply(mg_handle* h, int op, int level);
 /* Time one operator: runs it `reps` times between CUDA events, returns ms per rep. */
 int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out);
 
+/* Per-stage CUDA-event profiling of non-graph launches.  mg_profile(h, 1) clears
+ * and starts; mg_profile_read fills ms[stage*nlev + level] and counts[...] for the
+ * stages MG_ST_* below (nlev = mg_num_levels).  Synchronises the stream. */
+enum { MG_ST_SMOOTH = 0, MG_ST_SMOOTH_RES = 1, MG_ST_RESIDUAL = 2, MG_ST_GHOST = 3, MG_ST_RESTRICT = 4,
+       MG_ST_PROLONG = 5, MG_ST_COARSE = 6, MG_ST_INJECT_UP = 7, MG_ST_NORM = 8, MG_ST_COUNT = 9 };
+int mg_profile(mg_handle* h, int enable);
+int mg_profile_read(mg_handle* h, double* ms, int64_t* counts);
+/* Number of kernels this library has launched so far in the process (all handles). */
+int64_t mg_kernel_launches(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -133,6 +133,13 @@ struct mg_handle {
   double* d_dense = nullptr;
   void* d_spec = nullptr;
   double* d_mult = nullptr;  // UUU: full table; PUU: 2D table
+  // per-stage CUDA-event profiling (non-graph launches only)
+  bool prof_on = false;
+  struct Ev { cudaEvent_t a, b; int st, lv; };
+  std::vector<Ev> prof_pending;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<double> prof_ms;      // [stage][level]
+  std::vector<int64_t> prof_n;
   // graph
   bool use_graph = false;
   cudaGraphExec_t gexec = nullptr;
@@ -141,6 +148,55 @@ struct mg_handle {
 };
 
 namespace {
+
+enum Stage { ST_SMOOTH = 0, ST_SMOOTH_RES, ST_RESIDUAL, ST_GHOST, ST_RESTRICT, ST_PROLONG, ST_COARSE, ST_INJECT_UP,
+             ST_NORM, ST_COUNT };
+
+cudaEvent_t get_ev(mg_handle* h) {
+  if (!h->evpool.empty()) {
+    cudaEvent_t e = h->evpool.back();
+    h->evpool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_OK(cudaEventCreate(&e));
+  return e;
+}
+
+// RAII event pair around one stage on the handle's stream (only when profiling).
+struct Prof {
+  mg_handle* h;
+  int st, lv;
+  cudaEvent_t a = nullptr;
+  bool on;
+  Prof(mg_handle* hh, int stage, int level) : h(hh), st(stage), lv(level), on(hh->prof_on) {
+    if (on) {
+      a = get_ev(h);
+      cudaEventRecord(a, h->s);
+    }
+  }
+  ~Prof() {
+    if (!on) return;
+    cudaEvent_t b = get_ev(h);
+    cudaEventRecord(b, h->s);
+    h->prof_pending.push_back({a, b, st, lv});
+  }
+};
+
+void prof_flush(mg_handle* h) {
+  if (h->prof_pending.empty()) return;
+  CUDA_OK(cudaStreamSynchronize(h->s));
+  const int nl = (int)h->L.size();
+  for (auto& e : h->prof_pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    h->prof_ms[e.st * nl + e.lv] += ms;
+    h->prof_n[e.st * nl + e.lv] += 1;
+    h->evpool.push_back(e.a);
+    h->evpool.push_back(e.b);
+  }
+  h->prof_pending.clear();
+}
 
 LevelView view(mg_handle* h, int m) {
   Level& l = h->L[m];
@@ -622,6 +678,7 @@ void swap_u(Level& l) { l.cur = 1 - l.cur; }
 void refresh(mg_handle* h, int m) {
   if (m <= 0) return;
   const int lo = h->L[m].ext_chain ? 1 : m;
+  Prof pr(h, ST_GHOST, m);
   for (int j = m; j >= lo; --j) {
     Level &F = h->L[j], &C = h->L[j - 1];
     if (!F.inj_dst.empty()) launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->s);
@@ -641,27 +698,37 @@ void sweep(mg_handle* h, int m, bool with_res) {
   Level& l = h->L[m];
   const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
   if (with_res && !has_ghosts(h, m)) {
+    Prof pr(h, ST_SMOOTH_RES, m);
     launch_smooth(view(h, m), h->order, mode, h->omega, true, h->s);
     swap_u(l);
     return;
   }
-  launch_smooth(view(h, m), h->order, mode, h->omega, false, h->s);
-  swap_u(l);
+  {
+    Prof pr(h, ST_SMOOTH, m);
+    launch_smooth(view(h, m), h->order, mode, h->omega, false, h->s);
+    swap_u(l);
+  }
   if (with_res) {
     refresh(h, m);
+    Prof pr(h, ST_RESIDUAL, m);
     launch_residual(view(h, m), h->order, h->s);
   }
 }
 
 void restrict_level(mg_handle* h, int m) {
   Level& C = h->L[m - 1];
-  launch_restrict(view(h, m), view(h, m - 1), h->s);
+  {
+    Prof pr(h, ST_RESTRICT, m);
+    launch_restrict(view(h, m), view(h, m - 1), h->s);
+  }
   refresh(h, m - 1);
+  Prof pr(h, ST_RESTRICT, m);
   launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
   CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
 }
 
 void coarse_solve(mg_handle* h) {
+  Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
   launch_coarse_gather(c, h->d_dense, h->P, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
@@ -674,6 +741,7 @@ void coarse_solve(mg_handle* h) {
 }
 
 void inject_up_all(mg_handle* h) {
+  Prof pr(h, ST_INJECT_UP, 0);
   for (int m = (int)h->L.size() - 1; m >= 1; --m)
     launch_inject_up(view(h, m), view(h, m - 1), h->L[m - 1].u[h->L[m - 1].cur], h->s);
 }
@@ -684,13 +752,17 @@ void vcycle_body(mg_handle* h) {
     for (int k = 1; k <= h->eta1; ++k) sweep(h, m, k == h->eta1);
     if (h->eta1 == 0) {
       refresh(h, m);
+      Prof pr(h, ST_RESIDUAL, m);
       launch_residual(view(h, m), h->order, h->s);
     }
     restrict_level(h, m);
   }
   coarse_solve(h);
   for (int m = 1; m <= top; ++m) {
-    launch_prolong(view(h, m), view(h, m - 1), h->s);
+    {
+      Prof pr(h, ST_PROLONG, m);
+      launch_prolong(view(h, m), view(h, m - 1), h->s);
+    }
     for (int k = 0; k < h->eta2; ++k) sweep(h, m, false);
   }
   inject_up_all(h);
@@ -720,6 +792,8 @@ void run_vcycles(mg_handle* h, int n) {
     CUFFT_OK(cufftSetStream(h->plan_f, cap));
     CUFFT_OK(cufftSetStream(h->plan_b, cap));
     cudaGraph_t g = nullptr;
+    const bool prof = h->prof_on;
+    h->prof_on = false;
     cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
     if (e == cudaSuccess) {
       try {
@@ -732,6 +806,7 @@ void run_vcycles(mg_handle* h, int n) {
       e = cudaStreamEndCapture(cap, &g);
     }
     h->s = orig;
+    h->prof_on = prof;
     cufftSetStream(h->plan_f, orig);
     cufftSetStream(h->plan_b, orig);
     cudaStreamDestroy(cap);
@@ -756,6 +831,7 @@ double residual_abs(mg_handle* h) {
   CUDA_OK(cudaMemsetAsync(h->d_norm, 0, sizeof(unsigned long long), h->s));
   for (int m = 0; m < (int)h->L.size(); ++m) {
     refresh(h, m);
+    Prof pr(h, ST_NORM, m);
     launch_norm(view(h, m), h->order, true, h->d_norm, h->s);
   }
   return read_norm(h);
@@ -814,6 +890,8 @@ void set_rhs(mg_handle* h, const double* f_dev) {
 void destroy(mg_handle* h) {
   if (!h) return;
   cudaStreamSynchronize(h->s);
+  prof_flush(h);
+  for (auto e : h->evpool) cudaEventDestroy(e);
   for (auto& l : h->L) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
                     (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
@@ -982,6 +1060,32 @@ int mg_use_graph(mg_handle* h, int enable) {
   h->use_graph = enable != 0;
   return MG_OK;
 }
+
+int mg_profile(mg_handle* h, int enable) {
+  if (!h) return MG_ERR_ARG;
+  return guard(h, [&] {
+    prof_flush(h);
+    h->prof_on = enable != 0;
+    h->prof_ms.assign((size_t)ST_COUNT * h->L.size(), 0.0);
+    h->prof_n.assign((size_t)ST_COUNT * h->L.size(), 0);
+  });
+}
+
+int mg_profile_read(mg_handle* h, double* ms, int64_t* counts) {
+  if (!h) return MG_ERR_ARG;
+  return guard(h, [&] {
+    prof_flush(h);
+    const size_t n = (size_t)ST_COUNT * h->L.size();
+    if (h->prof_ms.size() != n) {
+      h->prof_ms.assign(n, 0.0);
+      h->prof_n.assign(n, 0);
+    }
+    if (ms) std::memcpy(ms, h->prof_ms.data(), n * sizeof(double));
+    if (counts) std::memcpy(counts, h->prof_n.data(), n * sizeof(int64_t));
+  });
+}
+
+int64_t mg_kernel_launches(void) { return (int64_t)launches_issued(); }
 
 int mg_num_levels(mg_handle* h) { return h ? (int)h->L.size() : MG_ERR_ARG; }
 

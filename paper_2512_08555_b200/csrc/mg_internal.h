@@ -45,6 +45,7 @@ struct InjList {           // f2c injection pairs feeding a level's c2f stencils
 
 // ---- launchers (mg_kernels.cu) ----
 void prepare_kernels();  // constants + shared-memory attributes (call before any capture)
+unsigned long long launches_issued();  // running count of this library's kernel launches
 void launch_smooth(const LevelView& L, int order, int mode, double omega, bool with_residual,
                    cudaStream_t s);
 void launch_residual(const LevelView& L, int order, cudaStream_t s);

@@ -21,6 +21,9 @@ __constant__ double c_w4[4];
 __constant__ double c_w6[6];
 
 static bool g_weights_ready = false;
+static unsigned long long g_nlaunch = 0;  // kernels launched by this library (bench evidence)
+
+unsigned long long launches_issued() { return g_nlaunch; }
 
 static void upload_weights() {
   if (g_weights_ready) return;
@@ -188,7 +191,7 @@ static void smooth_inst(const LevelView& L, double omega, double inv_h2, double 
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return;
   }
-  if (L.nreal > 0) k<<<L.nreal, NT, smem, s>>>(L, omega, inv_h2, inv_d);
+  if (L.nreal > 0) { k<<<L.nreal, NT, smem, s>>>(L, omega, inv_h2, inv_d); ++g_nlaunch; }
 }
 
 template <int B, int ORDER>
@@ -303,8 +306,8 @@ void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g
                 const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
   if (g.n == 0) return;
   const int nt = 128, nb = (g.n + nt - 1) / nt;
-  if (I == 4) k_c2f<4><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero);
-  else k_c2f<6><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero);
+  if (I == 4) { k_c2f<4><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero); ++g_nlaunch; }
+  else { k_c2f<6><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero); ++g_nlaunch; }
 }
 
 __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
@@ -315,7 +318,7 @@ __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_
 
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s) {
   if (l.n == 0) return;
-  k_copy_list<<<(l.n + 255) / 256, 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field);
+  { k_copy_list<<<(l.n + 255) / 256, 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -348,7 +351,7 @@ __global__ void k_restrict(LevelView F, LevelView C) {
 }
 
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
-  if (fine.nreal) k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse);
+  if (fine.nreal) { k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // FAS right-hand side on the covered coarse nodes (Alg. 1): f = r + Δ u.
@@ -368,8 +371,8 @@ __global__ void k_fas_rhs(LevelView F, LevelView C) {
 
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (order == 2) k_fas_rhs<2><<<fine.nreal, 256, 0, s>>>(fine, coarse);
-  else k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse);
+  if (order == 2) { k_fas_rhs<2><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // Prolongation of the correction (Alg. 1): u_f += trilinear(u_c - û_c).
@@ -400,7 +403,7 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 }
 
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
-  if (fine.nreal) k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse);
+  if (fine.nreal) { k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
@@ -415,7 +418,7 @@ __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
 }
 
 void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s) {
-  if (fine.nreal) k_inject_up<<<fine.nreal, 256, 0, s>>>(fine, coarse, coarse_u);
+  if (fine.nreal) { k_inject_up<<<fine.nreal, 256, 0, s>>>(fine, coarse, coarse_u); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -458,8 +461,8 @@ __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
 
 void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s) {
   if (!L.nreal) return;
-  if (order == 2) k_norm<2><<<L.nreal, 256, 0, s>>>(L, residual, out);
-  else k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out);
+  if (order == 2) { k_norm<2><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else { k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
 }
 
 // R_h^M f on all real nodes into tmp (M=4: f + (1/12)Σδ²f, right side of E12), then
@@ -491,8 +494,8 @@ __global__ void k_rhs_commit(LevelView L, const double* tmp) {
 
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s) {
   if (!L.nreal || order == 2) return;
-  k_rhs_apply<<<L.nreal, 256, 0, s>>>(L, tmp);
-  k_rhs_commit<<<L.nreal, 256, 0, s>>>(L, tmp);
+  { k_rhs_apply<<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  { k_rhs_commit<<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
 }
 
 // leaf-ordered [n_leaf][B^3] <-> level block storage
@@ -514,7 +517,7 @@ __global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const do
 void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
                          int nlev, bool to_levels, cudaStream_t s) {
   (void)nlev;
-  if (nleaf) k_leaf_scatter<<<nleaf, 256, 0, s>>>(B3, map, src, dst_by_level, to_levels);
+  if (nleaf) { k_leaf_scatter<<<nleaf, 256, 0, s>>>(B3, map, src, dst_by_level, to_levels); ++g_nlaunch; }
 }
 
 __global__ void k_fill(double* p, int64_t n, double v) {
@@ -523,7 +526,7 @@ __global__ void k_fill(double* p, int64_t n, double v) {
 }
 
 void launch_zero(double* p, int64_t n, cudaStream_t s) {
-  if (n) k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, 0.0);
+  if (n) { k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, 0.0); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -545,7 +548,7 @@ __global__ void k_coarse_gather(LevelView L, double* dense, int Px, int Py, int 
 
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, cudaStream_t s) {
   const int64_t n = (int64_t)P[0] * P[1] * P[2];
-  k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1], P[2]);
+  { k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1], P[2]); ++g_nlaunch; }
 }
 
 __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, int Px, int Py) {
@@ -571,8 +574,8 @@ __global__ void k_coarse_band(C2FList g, double* u, const double* __restrict__ d
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const C2FList& band,
                            cudaStream_t s) {
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
-  k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1]);
-  if (band.n) k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, P[0], P[1], P[2]);
+  { k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1]); ++g_nlaunch; }
+  if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, P[0], P[1], P[2]); ++g_nlaunch; }
 }
 
 // spectral symbol σ_M(θ) h² from ŝ = 2cosθ - 2
@@ -599,7 +602,7 @@ __global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, in
 
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  k_mul_periodic<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h);
+  { k_mul_periodic<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h); ++g_nlaunch; }
 }
 
 __global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mult, int64_t n) {
@@ -610,7 +613,7 @@ __global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mu
 }
 
 void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s) {
-  k_mul_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n);
+  { k_mul_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
 }
 
 // x periodic, y/z unbounded (E14 with the periodic axis x, reading Z22):
@@ -636,7 +639,7 @@ __global__ void k_mul_puu(cuDoubleComplex* spec, int Px, int Py, int Pz, int ord
 
 void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  k_mul_puu<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h, tab2);
+  { k_mul_puu<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h, tab2); ++g_nlaunch; }
 }
 
 __global__ void k_scale(double* p, int64_t n, double a) {
@@ -645,7 +648,7 @@ __global__ void k_scale(double* p, int64_t n, double a) {
 }
 
 void launch_scale(double* p, int64_t n, double a, cudaStream_t s) {
-  if (n) k_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, a);
+  if (n) { k_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, a); ++g_nlaunch; }
 }
 
 __global__ void k_real_part_scale(const cuDoubleComplex* c, double* out, int64_t n, double a) {
@@ -654,7 +657,7 @@ __global__ void k_real_part_scale(const cuDoubleComplex* c, double* out, int64_t
 }
 
 void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s) {
-  if (n) k_real_part_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const cuDoubleComplex*)cplx, out, n, a);
+  if (n) { k_real_part_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const cuDoubleComplex*)cplx, out, n, a); ++g_nlaunch; }
 }
 
 }  // namespace mg

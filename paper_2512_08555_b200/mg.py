@@ -24,7 +24,9 @@ MG_OK, MG_WARN_NOT_CONVERGED = 0, 1
 
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
-           "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op"]
+           "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
+           "mg_profile_read", "mg_kernel_launches"]
+STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm"]
 
 
 class MgDesc(C.Structure):
@@ -71,6 +73,10 @@ def load_library(path: str = _LIB_PATH):
     lib.mg_debug_field.argtypes = [P, I, I, I, P]
     lib.mg_debug_apply.argtypes = [P, I, I]
     lib.mg_time_op.argtypes = [P, I, I, I, C.POINTER(D)]
+    lib.mg_profile.argtypes = [P, I]
+    lib.mg_profile_read.argtypes = [P, C.POINTER(D), C.POINTER(C.c_int64)]
+    lib.mg_kernel_launches.argtypes = []
+    lib.mg_kernel_launches.restype = C.c_int64
     for name in EXPORTS:
         if name not in ("mg_destroy", "mg_last_error"):
             getattr(lib, name).restype = C.c_int
@@ -205,6 +211,21 @@ class Solver:
 
     def debug_apply(self, op, m):
         self._check(self.lib.mg_debug_apply(self.h, OPS[op] if isinstance(op, str) else int(op), int(m)))
+
+    def profile(self, on=True):
+        """Start (clears) / stop per-stage CUDA-event timing of non-graph launches."""
+        self._check(self.lib.mg_profile(self.h, 1 if on else 0))
+
+    def profile_read(self):
+        """{stage: (ms[level], count[level])} accumulated since profile(True)."""
+        nl = self.num_levels()
+        ms = (C.c_double * (len(STAGES) * nl))()
+        n = (C.c_int64 * (len(STAGES) * nl))()
+        self._check(self.lib.mg_profile_read(self.h, ms, n))
+        return {s: (list(ms[i * nl:(i + 1) * nl]), list(n[i * nl:(i + 1) * nl])) for i, s in enumerate(STAGES)}
+
+    def kernel_launches(self):
+        return int(self.lib.mg_kernel_launches())
 
     def time_op(self, op, m, reps):
         ms = C.c_double()
