@@ -219,9 +219,21 @@ def run_mine(args, ws, rank, local, dist):
     alg_bytes = bytes_per_unknown.get(st, 24) * Nl
     achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
     peak, peak_src = peak_hbm()
-    fused = prof["smooth_res"]
-    fused_ms = fused[0][top] / max(1, fused[1][top])
-    fused_gbs = 32 * Nf / (fused_ms * 1e-3) / 1e9 if fused[1][top] else None
+    # per-kernel algorithmic GB/s on the finest level (SURVEY §8(d) byte counts)
+    kernels = {}
+    for st_name, bpu in (("smooth", 24), ("smooth_res", 32), ("residual", 24), ("prolong", 18), ("restrict", 13)):
+        tot, cnt = prof[st_name][0][top], prof[st_name][1][top]
+        if cnt:
+            kms = tot / cnt
+            kernels[st_name] = {"avg_ms": kms, "alg_bytes_per_unknown": bpu, "gbs": bpu * Nf / (kms * 1e-3) / 1e9,
+                                "frac": bpu * Nf / (kms * 1e-3) / 1e9 / peak_hbm()[0], "launches_per_cycle": cnt / kp}
+    # the smoother+residual pair of the last pre-smoothing step (fused or sweep + residual)
+    if "smooth_res" in kernels:
+        fused_ms = kernels["smooth_res"]["avg_ms"]
+    else:
+        fused_ms = kernels["smooth"]["avg_ms"] + kernels.get("residual", {"avg_ms": 0.0})["avg_ms"]
+    fused = (None, [1] * nlev)
+    fused_gbs = 32 * Nf / (fused_ms * 1e-3) / 1e9
     coarse_ms = prof["coarse"][0][0] / max(1, prof["coarse"][1][0])
     stage_ms = {s: round(sum(prof[s][0]) / kp, 5) for s in prof}
 
@@ -267,9 +279,11 @@ def run_mine(args, ws, rank, local, dist):
                          "kernel": f"{st} (level {lv}, {Nl} unknowns/launch)",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
                          "frac_of_8TBps": achieved / NORTH_STAR_PEAK_GBS},
-            "fused_smoother_residual": {"gbs": fused_gbs, "ms": fused_ms, "frac": (fused_gbs or 0) / peak,
-                                        "unknowns_per_s": Nf / (fused_ms * 1e-3) if fused[1][top] else None,
-                                        "alg_bytes_per_unknown": 32},
+            "smoother_residual": {"gbs": fused_gbs, "ms": fused_ms, "frac": fused_gbs / peak,
+                                  "unknowns_per_s": Nf / (fused_ms * 1e-3), "alg_bytes_per_unknown": 32,
+                                  "what": "last pre-smoothing RB sweep + residual on the finest level (one fused "
+                                          "kernel if MG_FUSE_RES, else sweep kernel + residual kernel)"},
+            "finest_level_kernels": kernels,
             "vcycle_roofline": {"stage_accounting_ms": rl_stage_ms, "fused_min_ms": rl_fused_ms,
                                 "frac_stage": rl_stage_ms / ms, "frac_fused_min": rl_fused_ms / ms,
                                 "excl_coarse_value": nleaf_unknowns / ((ms - coarse_ms) * 1e-3)},

@@ -11,6 +11,7 @@
 #include <array>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -140,6 +141,7 @@ struct mg_handle {
   std::vector<cudaEvent_t> evpool;
   std::vector<double> prof_ms;      // [stage][level]
   std::vector<int64_t> prof_n;
+  bool fuse_res = std::getenv("MG_FUSE_RES") != nullptr;  // force the fused sweep+residual kernel
   // graph
   bool use_graph = false;
   cudaGraphExec_t gexec = nullptr;
@@ -697,7 +699,11 @@ void sweep(mg_handle* h, int m, bool with_res) {
   refresh(h, m);
   Level& l = h->L[m];
   const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
-  if (with_res && !has_ghosts(h, m)) {
+  // Fuse the residual into the last sweep only on small-block levels: on B = 16
+  // levels the halo-3 fused tile is shared-memory-bound, so a
+  // halo-2 sweep plus a separate residual pass is faster there.
+  const bool fuse = l.B < 16 || h->fuse_res;
+  if (with_res && !has_ghosts(h, m) && fuse) {
     Prof pr(h, ST_SMOOTH_RES, m);
     launch_smooth(view(h, m), h->order, mode, h->omega, true, h->s);
     swap_u(l);

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "mg_internal.h"
 
@@ -178,9 +179,252 @@ __global__ void __launch_bounds__(NT) k_smooth(LevelView L, double omega, double
   }
 }
 
+// ---------------------------------------------------------------------------------
+// Optimised smoother for B = 16 blocks (the hot path).  Same semantics as k_smooth,
+// with: the 27-entry neighbour table in shared memory; the halo tile loaded with
+// cp.async (8-byte LDGSTS, no register staging); a colour-split tile layout (each
+// tile row stores its even-x then its odd-x nodes) so that the red/black passes,
+// whose lanes walk same-colour nodes two apart in x, read shared memory without
+// bank conflicts; and f for each pass prefetched into registers before the barrier
+// that precedes the pass.
+// ---------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
+// Colour-split tile: the T^3 tile nodes are stored in two dense arrays by tile
+// parity (x+y+z)&1, each row-major in (z, y, x>>1) with row pitch T/2.  The odd
+// array starts at an offset ≡ 8 (mod 16) doubles, so a warp walking same-colour
+// nodes of consecutive rows, or all nodes of a row, hits distinct 8-byte banks.
+template <int T>
+struct CTile {
+  static constexpr int W = T / 2;
+  static constexpr int HALF = T * T * T / 2;
+  static constexpr int BOFF = HALF + ((8 - HALF % 16) % 16 + 16) % 16;
+  static constexpr int SIZE = BOFF + HALF;  // doubles
+};
+
+// Δ_h^M at a node of a colour-split tile, given its packed position: rel = row-major
+// index (z*T+y)*W + (x>>1) inside its colour array, q = tile parity, xpar = x & 1.
+// All 19 operands are immediate offsets from four base pointers; same summation
+// order as lap_tile.
+template <int ORDER, int T>
+__device__ __forceinline__ double lap_t(const double* t, int rel, int q, int xpar, double inv_h2) {
+  constexpr int W = CTile<T>::W, SZ = T * W;
+  const double* S = t + (q ? CTile<T>::BOFF : 0) + rel;  // same colour: centre, edges
+  const double* O = t + (q ? 0 : CTile<T>::BOFF) + rel;  // other colour: faces
+  const double* Om = O + xpar - 1;                       // (x-1) at Om[0], (x+1) at Om[1]
+  const double* Sm = S + xpar - 1;
+  const double c = S[0];
+  const double F = ((Om[0] + Om[1]) + (O[-W] + O[W])) + (O[-SZ] + O[SZ]);
+  if (ORDER == 2) return (F - 6.0 * c) * inv_h2;
+  const double E = (((Sm[-W] + Sm[1 - W]) + (Sm[W] + Sm[1 + W])) + ((Sm[-SZ] + Sm[1 - SZ]) + (Sm[SZ] + Sm[1 + SZ]))) +
+                   ((S[-W - SZ] + S[W - SZ]) + (S[-W + SZ] + S[W + SZ]));
+  return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+}
+
+// ---- per-variant node tables (identical for every block, built once on the host) ----
+// node entry: rel (bits 0-12) | q (13) | xpar (14) | neighbour slot (15-19) | offset in
+// that neighbour block (20-31).  load entry: tile index (0-13) | slot (14-18) | offset (19-30).
+template <int B, int MODE, bool RES>
+struct SmoothShape {
+  static constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
+  static constexpr int H = NS + (RES ? 1 : 0);
+  static constexpr int T = B + 2 * H;
+  static constexpr int B3 = B * B * B;
+  // Pass p walks whole rows of the colour-split tile (RB: the W slots of the pass
+  // colour's array; Jacobi: all T slots) over the R(p)^2 rows of its region, so that
+  // consecutive lanes read consecutive shared-memory words; slots outside the region
+  // are idle (invalid table entries).
+  __host__ __device__ static constexpr int R(int p) { return B + 2 * (H - 1 - p); }
+  __host__ __device__ static constexpr int CNT(int p) { return R(p) * R(p) * (MODE == SM_RB ? T / 2 : T); }
+  __host__ __device__ static constexpr int OFF(int p) { return p == 0 ? 0 : OFF(p - 1) + CNT(p - 1); }
+  static constexpr int INT_OFF = NS > 0 ? OFF(NS - 1) + CNT(NS - 1) : 0;              // interior, x fastest
+  static constexpr int LOAD_OFF = INT_OFF + B3;
+  static constexpr int TOTAL = LOAD_OFF + T * T * T;
+};
+
+static int host_region(int x, int B) { return x < 0 ? -1 : (x >= B ? 1 : 0); }
+
+template <int B, int MODE, bool RES>
+static const uint32_t* smooth_table() {
+  using S = SmoothShape<B, MODE, RES>;
+  static uint32_t* d = nullptr;
+  if (d) return d;
+  constexpr int T = S::T, H = S::H, W = CTile<T>::W;
+  std::vector<uint32_t> t;
+  t.reserve(S::TOTAL);
+  auto node = [&](int x, int y, int z) {  // block-local coords (halo allowed)
+    const int tx = x + H, ty = y + H, tz = z + H;
+    const int dx = host_region(x, B), dy = host_region(y, B), dz = host_region(z, B);
+    const uint32_t rel = (uint32_t)((tz * T + ty) * W + (tx >> 1));
+    const uint32_t q = (uint32_t)((tx + ty + tz) & 1), xpar = (uint32_t)(tx & 1);
+    const uint32_t slot = (uint32_t)((dx + 1) + 3 * (dy + 1) + 9 * (dz + 1));
+    const uint32_t floc = (uint32_t)(((z - dz * B) * B + (y - dy * B)) * B + (x - dx * B));
+    return rel | (q << 13) | (xpar << 14) | (slot << 15) | (floc << 20);
+  };
+  for (int p = 0; p < S::NS; ++p) {
+    const int e = H - 1 - p;
+    for (int z = -e; z < B + e; ++z)
+      for (int y = -e; y < B + e; ++y) {
+        const int ty = y + H, tz = z + H;
+        for (int s = 0; s < (MODE == SM_RB ? W : T); ++s) {
+          // RB: slot s of the colour-p row holds tile x with parity making (x+y+z) even for
+          // red (p = 0, global parity) / odd for black; Jacobi: tile x = s
+          int tx = s;
+          if (MODE == SM_RB) {
+            const int want = ((p & 1) + H) & 1;  // tile parity of the pass colour
+            tx = 2 * s + ((want - ty - tz) & 1);
+          }
+          const int x = tx - H;
+          if (x >= -e && x < B + e) t.push_back(node(x, y, z));
+          else t.push_back(0xffffffffu);
+        }
+      }
+  }
+  for (int i = 0; i < S::B3; ++i) t.push_back(node(i % B, (i / B) % B, i / (B * B)));
+  for (int i = 0; i < T * T * T; ++i) {
+    const int tx = i % T, ty = (i / T) % T, tz = i / (T * T);
+    const uint32_t e = node(tx - H, ty - H, tz - H);
+    const uint32_t dst = ((e >> 13) & 1u ? CTile<T>::BOFF : 0) + (e & 0x1fffu);
+    t.push_back(dst | (((e >> 15) & 31u) << 14) | ((e >> 20) << 19));
+  }
+  if ((int)t.size() != S::TOTAL) return nullptr;
+  cudaMalloc(&d, t.size() * sizeof(uint32_t));
+  cudaMemcpy(d, t.data(), t.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  return d;
+}
+
+template <int B, int ORDER, int MODE, bool RES, int NT>
+__global__ void __launch_bounds__(NT, (MODE == SM_RB && RES) ? 2 : (MODE < 0 ? 4 : 3))
+    k_smooth2(LevelView L, const uint32_t* __restrict__ tab, double omega, double inv_h2, double inv_d) {
+  using SH = SmoothShape<B, MODE, RES>;
+  constexpr int NS = SH::NS, H = SH::H, T = SH::T, B3 = SH::B3;
+  constexpr int MAXU = (SH::CNT(0) + NT - 1) / NT;  // pass 0 is the largest
+  constexpr int MAXR = (B3 + NT - 1) / NT;
+  constexpr int MAXF = MAXU > MAXR ? MAXU : MAXR;
+  extern __shared__ double tile[];
+  __shared__ int snb[27];
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < 27) snb[tid] = L.nbr[(size_t)b * 27 + tid];
+  const uint32_t realbits = L.nbr_real[b];
+  __syncthreads();
+
+  // ---- async halo tile load (global reads coalesced along x)
+  {
+    const uint32_t* lt = tab + SH::LOAD_OFF;
+#pragma unroll 4
+    for (int i = tid; i < T * T * T; i += NT) {
+      const uint32_t e = __ldg(lt + i);
+      cp_async8(&tile[e & 0x3fffu], L.u + (size_t)snb[(e >> 14) & 31u] * B3 + (e >> 19));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+
+  double fv[MAXF];
+  auto prefetch = [&](int off, int cnt) {
+#pragma unroll
+    for (int k = 0; k < MAXF; ++k) {
+      const int i = tid + k * NT;
+      fv[k] = 0.0;
+      if (i < cnt) {
+        const uint32_t e = __ldg(tab + off + i);
+        const uint32_t s = (e >> 15) & 31u;
+        if (e != 0xffffffffu && ((realbits >> s) & 1u)) fv[k] = __ldg(L.f + (size_t)snb[s] * B3 + (e >> 20));
+      }
+    }
+  };
+  if (NS > 0) prefetch(SH::OFF(0), SH::CNT(0));
+  cp_async_wait_all();
+  __syncthreads();
+
+#pragma unroll
+  for (int p = 0; p < NS; ++p) {
+    const int cnt = SH::CNT(p);
+    const uint32_t* pt = tab + SH::OFF(p);
+    double stage[MAXU];
+    uint32_t ent[MAXU];
+#pragma unroll
+    for (int k = 0; k < MAXU; ++k) {
+      const int i = tid + k * NT;
+      stage[k] = 0.0;
+      ent[k] = 0xffffffffu;
+      if (i < cnt) {
+        const uint32_t e = __ldg(pt + i);
+        if (e != 0xffffffffu && ((realbits >> ((e >> 15) & 31u)) & 1u)) {
+          ent[k] = e;
+          const int rel = e & 0x1fff, q = (e >> 13) & 1, xp = (e >> 14) & 1;
+          const double c = tile[(q ? CTile<T>::BOFF : 0) + rel];
+          stage[k] = c + omega * (fv[k] - lap_t<ORDER, T>(tile, rel, q, xp, inv_h2)) * inv_d;
+        }
+      }
+    }
+    if (p + 1 < NS) prefetch(SH::OFF(p + 1), SH::CNT(p + 1));
+    else if (RES) {
+#pragma unroll
+      for (int k = 0; k < MAXF; ++k) {
+        const int i = tid + k * NT;
+        fv[k] = i < B3 ? __ldg(L.f + (size_t)b * B3 + i) : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MAXU; ++k) {
+      const uint32_t e = ent[k];
+      if (e != 0xffffffffu) tile[(((e >> 13) & 1u) ? CTile<T>::BOFF : 0) + (e & 0x1fffu)] = stage[k];
+    }
+    __syncthreads();
+  }
+
+  double* uo = L.u_out + (size_t)b * B3;
+  const uint32_t* it = tab + SH::INT_OFF;
+#pragma unroll
+  for (int k = 0; k < MAXR; ++k) {
+    const int i = tid + k * NT;
+    if (i < B3) {
+      const uint32_t e = __ldg(it + i);
+      const int rel = e & 0x1fff, q = (e >> 13) & 1, xp = (e >> 14) & 1;
+      if (NS > 0) uo[i] = tile[(q ? CTile<T>::BOFF : 0) + rel];
+      if (RES) {
+        const double fi = NS > 0 ? fv[k] : __ldg(L.f + (size_t)b * B3 + i);
+        L.r[(size_t)b * B3 + i] = fi - lap_t<ORDER, T>(tile, rel, q, xp, inv_h2);
+      }
+    }
+  }
+}
+
+template <int B, int ORDER, int MODE, bool RES>
+static void smooth_inst_v1(const LevelView& L, double omega, double inv_h2, double inv_d, cudaStream_t s,
+                           bool prepare_only);
+
 template <int B, int ORDER, int MODE, bool RES>
 static void smooth_inst(const LevelView& L, double omega, double inv_h2, double inv_d, cudaStream_t s,
                         bool prepare_only = false) {
+  if constexpr (B == 16) {
+    constexpr int NT = 256;
+    constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
+    constexpr int H = NS + (RES ? 1 : 0);
+    constexpr int T = B + 2 * H;
+    const size_t smem = sizeof(double) * CTile<T>::SIZE;
+    auto k = k_smooth2<B, ORDER, MODE, RES, NT>;
+    if (prepare_only) {
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smooth_table<B, MODE, RES>();
+      return;
+    }
+    const uint32_t* tab = smooth_table<B, MODE, RES>();
+    if (L.nreal > 0) { k<<<L.nreal, NT, smem, s>>>(L, tab, omega, inv_h2, inv_d); ++g_nlaunch; }
+    return;
+  }
+  smooth_inst_v1<B, ORDER, MODE, RES>(L, omega, inv_h2, inv_d, s, prepare_only);
+}
+
+template <int B, int ORDER, int MODE, bool RES>
+static void smooth_inst_v1(const LevelView& L, double omega, double inv_h2, double inv_d, cudaStream_t s,
+                           bool prepare_only) {
   constexpr int NT = B >= 16 ? 256 : (B >= 8 ? 128 : 64);
   constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
   constexpr int H = NS + (RES ? 1 : 0);
@@ -350,8 +594,63 @@ __global__ void k_restrict(LevelView F, LevelView C) {
   }
 }
 
+// Same operation with the fine residual tile (block + 1-node halo) staged in shared
+// memory by cp.async; FW evaluated with the same nesting/rounding as k_restrict.
+template <int B>
+__global__ void __launch_bounds__(256) k_restrict2(LevelView F, LevelView C) {
+  constexpr int T = B + 2, Bh = B / 2, B3 = B * B * B;
+  __shared__ double rt[T * T * T];
+  __shared__ int snb[27];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (tid < 27) snb[tid] = F.nbr[(size_t)b * 27 + tid];
+  __syncthreads();
+  for (int i = tid; i < T * T * T; i += 256) {
+    const int x = i % T - 1, y = (i / T) % T - 1, z = i / (T * T) - 1;
+    const int dx = region(x, B), dy = region(y, B), dz = region(z, B);
+    const int blk = snb[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)];
+    cp_async8(&rt[i], F.r + (size_t)blk * B3 + ((z - dz * B) * B + (y - dy * B)) * B + (x - dx * B));
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  double uinj[(Bh * Bh * Bh + 255) / 256];
+#pragma unroll
+  for (int k = 0; k < (Bh * Bh * Bh + 255) / 256; ++k) {
+    const int i = tid + k * 256;
+    if (i < Bh * Bh * Bh) {
+      const int cx = i % Bh, cy = (i / Bh) % Bh, cz = i / (Bh * Bh);
+      uinj[k] = __ldg(F.u + (size_t)b * B3 + ((2 * cz) * B + 2 * cy) * B + 2 * cx);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < (Bh * Bh * Bh + 255) / 256; ++k) {
+    const int i = tid + k * 256;
+    if (i >= Bh * Bh * Bh) continue;
+    const int cx = i % Bh, cy = (i / Bh) % Bh, cz = i / (Bh * Bh);
+    const int x = 2 * cx + 1, y = 2 * cy + 1, z = 2 * cz + 1;  // tile coords of the coincident fine node
+    double sz = 0.0;
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz) {
+      double sy = 0.0;
+#pragma unroll
+      for (int dy = -1; dy <= 1; ++dy) {
+        const double* row = rt + ((z + dz) * T + (y + dy)) * T + x;
+        const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
+        sy += (dy == 0 ? 0.5 : 0.25) * sx;
+      }
+      sz += (dz == 0 ? 0.5 : 0.25) * sy;
+    }
+    const size_t ci = (size_t)p * C.B3 + ((oz + cz) * C.B + (oy + cy)) * C.B + (ox + cx);
+    C.u[ci] = uinj[k];
+    C.r[ci] = sz;
+  }
+}
+
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
-  if (fine.nreal) { k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  if (!fine.nreal) return;
+  if (fine.B == 16) { k_restrict2<16><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // FAS right-hand side on the covered coarse nodes (Alg. 1): f = r + Δ u.
@@ -402,8 +701,54 @@ __global__ void k_prolong(LevelView F, LevelView C) {
   }
 }
 
+// Same operation with ε = u_c - û_c on the (B/2+1)^3 coarse nodes under the fine
+// block staged once in shared memory; same nesting/rounding as k_prolong.
+template <int B>
+__global__ void __launch_bounds__(256) k_prolong2(LevelView F, LevelView C) {
+  constexpr int E = B / 2 + 1, B3 = B * B * B;
+  __shared__ double eps[E * E * E];
+  __shared__ int snb[27];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
+  if (tid < 27) snb[tid] = C.nbr[(size_t)p * 27 + tid];
+  // prefetch the fine values this thread updates
+  double uf[B3 / 256];
+#pragma unroll
+  for (int k = 0; k < B3 / 256; ++k) uf[k] = F.u[(size_t)b * B3 + tid + k * 256];
+  __syncthreads();
+  const int CB = C.B;
+  for (int i = tid; i < E * E * E; i += 256) {
+    const int x = ox + i % E, y = oy + (i / E) % E, z = oz + i / (E * E);
+    const int dx = region(x, CB), dy = region(y, CB), dz = region(z, CB);
+    const size_t g = (size_t)snb[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] * C.B3 +
+                     ((z - dz * CB) * CB + (y - dy * CB)) * CB + (x - dx * CB);
+    eps[i] = __ldg(C.u + g) - __ldg(C.uhat + g);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < B3 / 256; ++k) {
+    const int i = tid + k * 256;
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int cx = x >> 1, cy = y >> 1, cz = z >> 1;
+    const int nx = (x & 1) ? 2 : 1, ny = (y & 1) ? 2 : 1, nzc = (z & 1) ? 2 : 1;
+    double vz[2];
+    for (int tz = 0; tz < nzc; ++tz) {
+      double vy[2];
+      for (int ty = 0; ty < ny; ++ty) {
+        const double* row = eps + ((cz + tz) * E + (cy + ty)) * E + cx;
+        vy[ty] = nx == 2 ? 0.5 * (row[0] + row[1]) : row[0];
+      }
+      vz[tz] = ny == 2 ? 0.5 * (vy[0] + vy[1]) : vy[0];
+    }
+    const double e = nzc == 2 ? 0.5 * (vz[0] + vz[1]) : vz[0];
+    F.u[(size_t)b * B3 + i] = uf[k] + e;
+  }
+}
+
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
-  if (fine.nreal) { k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  if (!fine.nreal) return;
+  if (fine.B == 16) { k_prolong2<16><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
