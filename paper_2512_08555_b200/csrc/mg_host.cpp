@@ -88,7 +88,8 @@ struct Level {
   std::vector<uint8_t> ghost_ext;           // per ghost block: beyond an unbounded face
   bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
   // host tables
-  std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src;
+  std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len;
+  int pen_lmax = 0;
   std::vector<uint32_t> nbr_real;
   std::vector<uint8_t> covmask, c2f_ext;
   int bmap_lo[3] = {0, 0, 0}, bmap_n[3] = {1, 1, 1};
@@ -97,7 +98,7 @@ struct Level {
   double *f = nullptr, *r = nullptr, *uhat = nullptr;
   int cur = 0;
   int32_t *d_nbr = nullptr, *d_parent = nullptr, *d_bmap = nullptr, *d_c2f_dst = nullptr, *d_c2f_J = nullptr,
-          *d_inj_dst = nullptr, *d_inj_src = nullptr;
+          *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr;
   uint32_t* d_nbr_real = nullptr;
   uint8_t *d_covmask = nullptr, *d_c2f_ext = nullptr;
 
@@ -224,6 +225,10 @@ LevelView view(mg_handle* h, int m) {
   v.covmask = l.d_covmask;
   v.parent = l.d_parent;
   v.bmap = l.d_bmap;
+  v.npen = (int)l.pen_len.size();
+  v.pen_lmax = l.pen_lmax;
+  v.pen_blk = l.d_pen_blk;
+  v.pen_len = l.d_pen_len;
   return v;
 }
 
@@ -565,6 +570,58 @@ void build_ghosts(mg_handle* h) {
   }
 }
 
+// Pencils of B = 16 levels: maximal runs of consecutive real blocks along z (same
+// bx, by; no periodic wrap inside a run), split into near-equal chunks of at most
+// `lmax` blocks, longest first.  The z-marching kernels (mg_pencil.cu) walk one
+// pencil per CTA; halos above/below a pencil come through the neighbour tables.
+void build_pencils(mg_handle* h) {
+  int lmax = 4;
+  if (const char* e = std::getenv("MG_PENCIL")) lmax = std::max(1, std::min(16, std::atoi(e)));
+  const bool off = std::getenv("MG_NO_PENCIL") != nullptr;
+  for (auto& l : h->L) {
+    l.pen_blk.clear();
+    l.pen_len.clear();
+    l.pen_lmax = lmax;
+    if (off || l.B != 16) continue;
+    std::vector<std::array<int, 4>> cols;  // (bx, by, bz, idx)
+    for (int i = 0; i < l.nreal; ++i) cols.push_back({l.coords[i][0], l.coords[i][1], l.coords[i][2], i});
+    std::sort(cols.begin(), cols.end());
+    std::vector<std::vector<int>> pens;
+    for (size_t a = 0; a < cols.size();) {
+      size_t b = a + 1;
+      while (b < cols.size() && cols[b][0] == cols[a][0] && cols[b][1] == cols[a][1] &&
+             cols[b][2] == cols[b - 1][2] + 1)
+        ++b;
+      const int n = (int)(b - a), nchunk = (n + lmax - 1) / lmax;
+      for (int c = 0, pos = 0; c < nchunk; ++c) {
+        const int len = n / nchunk + (c < n % nchunk ? 1 : 0);
+        std::vector<int> p;
+        for (int t = 0; t < len; ++t) p.push_back(cols[a + pos + t][3]);
+        pos += len;
+        pens.push_back(p);
+      }
+      a = b;
+    }
+    // launch order: longest first; then (order 1, default) by the z of the first block and
+    // Morton order of (bx, by), so that CTAs resident at the same time are spatial
+    // neighbours and re-read each other's halos from L2; (order 0) column-major.
+    const char* oe = std::getenv("MG_PEN_ORDER");
+    const int order = oe ? std::atoi(oe) : 1;
+    auto key = [&](const std::vector<int>& p) {
+      const auto& c = l.coords[p[0]];
+      return order == 1 ? ((uint64_t)c[2] << 42) | morton(c[0], c[1], 0) : (uint64_t)0;
+    };
+    std::stable_sort(pens.begin(), pens.end(), [&](const std::vector<int>& x, const std::vector<int>& y) {
+      if (x.size() != y.size()) return x.size() > y.size();
+      return key(x) < key(y);
+    });
+    for (auto& p : pens) {
+      l.pen_len.push_back((int32_t)p.size());
+      for (int t = 0; t < lmax; ++t) l.pen_blk.push_back(t < (int)p.size() ? p[t] : -1);
+    }
+  }
+}
+
 void alloc_device(mg_handle* h) {
   for (auto& l : h->L) {
     const size_t n = (size_t)l.ntot() * l.B3;
@@ -582,6 +639,8 @@ void alloc_device(mg_handle* h) {
     l.d_c2f_ext = dev_upload(l.c2f_ext);
     l.d_inj_dst = dev_upload(l.inj_dst);
     l.d_inj_src = dev_upload(l.inj_src);
+    l.d_pen_blk = dev_upload(l.pen_blk);
+    l.d_pen_len = dev_upload(l.pen_len);
   }
   // leaf map: leaf n -> (level, block)
   std::vector<int64_t> map(h->leaves.size());
@@ -695,6 +754,12 @@ void refresh(mg_handle* h, int m) {
 
 bool has_ghosts(mg_handle* h, int m) { return m > 0 && !h->L[m].c2f_dst.empty(); }
 
+// r = f - Δu on all level-m nodes (ghosts already refreshed)
+void residual_kernel(mg_handle* h, int m) {
+  const LevelView v = view(h, m);
+  if (!launch_res_pencil(v, h->order, h->s)) launch_residual(v, h->order, h->s);
+}
+
 void sweep(mg_handle* h, int m, bool with_res) {
   refresh(h, m);
   Level& l = h->L[m];
@@ -711,13 +776,15 @@ void sweep(mg_handle* h, int m, bool with_res) {
   }
   {
     Prof pr(h, ST_SMOOTH, m);
-    launch_smooth(view(h, m), h->order, mode, h->omega, false, h->s);
+    const LevelView v = view(h, m);
+    if (mode != SM_RB || !launch_rb_pencil(v, h->order, h->omega, h->s))
+      launch_smooth(v, h->order, mode, h->omega, false, h->s);
     swap_u(l);
   }
   if (with_res) {
     refresh(h, m);
     Prof pr(h, ST_RESIDUAL, m);
-    launch_residual(view(h, m), h->order, h->s);
+    residual_kernel(h, m);
   }
 }
 
@@ -759,7 +826,7 @@ void vcycle_body(mg_handle* h) {
     if (h->eta1 == 0) {
       refresh(h, m);
       Prof pr(h, ST_RESIDUAL, m);
-      launch_residual(view(h, m), h->order, h->s);
+      residual_kernel(h, m);
     }
     restrict_level(h, m);
   }
@@ -901,7 +968,8 @@ void destroy(mg_handle* h) {
   for (auto& l : h->L) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
                     (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
-                    (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src})
+                    (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src, (void*)l.d_pen_blk,
+                    (void*)l.d_pen_len})
       if (p) cudaFree(p);
   }
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
@@ -953,6 +1021,7 @@ int mg_create(const mg_desc* d, void* stream, mg_handle** out) {
     prepare_kernels();
     validate_and_build(h);
     build_ghosts(h);
+    build_pencils(h);
     alloc_device(h);
     setup_coarse(h);
   });
@@ -1135,12 +1204,12 @@ static void apply_op(mg_handle* h, int op, int level) {
     case MG_OP_SMOOTH_RESIDUAL: sweep(h, level, true); break;
     case MG_OP_RESIDUAL:
       refresh(h, level);
-      launch_residual(view(h, level), h->order, h->s);
+      residual_kernel(h, level);
       break;
     case MG_OP_RESTRICT:
       if (level < 1) throw MgError(MG_ERR_ARG, "restrict needs level >= 1");
       refresh(h, level);
-      launch_residual(view(h, level), h->order, h->s);
+      residual_kernel(h, level);
       restrict_level(h, level);
       break;
     case MG_OP_PROLONG:

@@ -28,6 +28,11 @@ struct LevelView {
   const int32_t* bmap;      // dense block-coordinate map (real+ghost) of this level
   int bmap_lo[3], bmap_n[3];
   int per[3];               // periodic axes
+  // pencils: runs of consecutive real blocks along z (same bx, by), <= pen_lmax long;
+  // the z-marching stencil kernels (mg_pencil.cu) walk one pencil per CTA
+  int npen, pen_lmax;
+  const int32_t* pen_blk;   // [npen][pen_lmax] real block indices, bottom to top (-1 padded)
+  const int32_t* pen_len;   // [npen]
 };
 
 struct C2FList {           // boundary-ghost entries of one level
@@ -46,9 +51,14 @@ struct InjList {           // f2c injection pairs feeding a level's c2f stencils
 // ---- launchers (mg_kernels.cu) ----
 void prepare_kernels();  // constants + shared-memory attributes (call before any capture)
 unsigned long long launches_issued();  // running count of this library's kernel launches
+void note_launch();                   // count one launch made outside mg_kernels.cu
 void launch_smooth(const LevelView& L, int order, int mode, double omega, bool with_residual,
                    cudaStream_t s);
 void launch_residual(const LevelView& L, int order, cudaStream_t s);
+// z-marching pencil kernels (B = 16 levels); return false if the level is not eligible
+bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s);
+bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
+void prepare_pencil_kernels();
 void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
                 const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);

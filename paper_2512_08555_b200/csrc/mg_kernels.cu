@@ -25,6 +25,7 @@ static bool g_weights_ready = false;
 static unsigned long long g_nlaunch = 0;  // kernels launched by this library (bench evidence)
 
 unsigned long long launches_issued() { return g_nlaunch; }
+void note_launch() { ++g_nlaunch; }
 
 static void upload_weights() {
   if (g_weights_ready) return;
@@ -477,6 +478,7 @@ static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res
 
 void prepare_kernels() {
   upload_weights();
+  prepare_pencil_kernels();
   prepare_b<16, 2>(); prepare_b<16, 4>();
   prepare_b<8, 2>(); prepare_b<8, 4>();
   prepare_b<4, 2>(); prepare_b<4, 4>();

@@ -1,0 +1,429 @@
+// mg_pencil.cu — z-marching stencil kernels for B = 16 levels (the hot path).
+//
+// Why: a 3-D halo tile per 16^3 block evaluated from shared memory costs 19
+// shared-memory reads per node and pass; on B200 that makes the red-black sweep
+// L1/shared-memory bound at ~1.7 TB/s (profiles/r01_s2_baseline_ncu.md).  These
+// kernels instead walk a *pencil* (a run of consecutive real blocks along z) one
+// z-plane at a time with one thread per (x,y) column:
+//   * each thread keeps its column's centre values and in-plane face sums S4 of
+//     the last planes in registers, so a 19-point Mehrstellen node (E12)
+//     reads only its 4 in-plane face and 4 in-plane diagonal neighbours from
+//     shared memory (the z-neighbours and the z±1 edge sums come from registers);
+//   * only xy planes (with an x/y halo) are staged in shared memory, through a
+//     cp.async ring that keeps D planes in flight ahead of the compute;
+//   * the red and black half-sweeps of one RB sweep (reading Z10: colour = parity
+//     of the level-global index, red = even first, each colour from a snapshot)
+//     come out of one pass: red at plane s-1 and black at plane s-2 while plane s
+//     arrives, so u and f are read from HBM once per sweep (24 B / unknown).
+// Boundary-ghost nodes (ghost blocks: c2f at resolution jumps, exterior band) are
+// frozen during a sweep (reading Z9): halo nodes in non-real blocks keep their value.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mg_internal.h"
+
+namespace mg {
+
+namespace {
+
+constexpr int PB = 16;             // block edge
+constexpr int PB3 = PB * PB * PB;
+constexpr int PMAXL = 16;          // longest pencil (blocks)
+
+__device__ __forceinline__ int reg16(int x) { return x < 0 ? -1 : (x >= PB ? 1 : 0); }
+
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Source block / z-local index of plane z of a pencil of `len` blocks (planes
+// [-H, 16 len + H)): below the pencil -> neighbour slot dz = -1 of its first block,
+// above -> dz = +1 of its last block.
+__device__ __forceinline__ void plane_src(int z, int nz, int len, int& k, int& dz, int& zl) {
+  dz = z < 0 ? -1 : (z >= nz ? 1 : 0);
+  k = z < 0 ? 0 : (z >= nz ? len - 1 : (z >> 4));
+  zl = z - PB * k - PB * dz;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+// Red-black sweep.  Plane tile of old u: x, y in [-2, 18) (halo 2), 20 x 20 doubles,
+// staged by 16-byte cp.async into an R-plane ring D planes ahead (f likewise, one
+// pair per thread).  Each thread owns a pair of columns (a, b) = (x0, x0+1), x0 even
+// in [-2, 16], on a row y in [-1, 17); at every plane one of the two is red and the
+// other black.  Which one is red at even planes depends only on the row parity, so
+// warps hold rows of one parity (warps 0-2: even y, 3-5: odd y), 3 whole rows of 10
+// pairs each (lanes 30, 31 idle): the red and black phases run without divergence,
+// and the in-row neighbours x0-1, x0+2 come from the adjacent lanes by shuffles
+// instead of strided shared-memory loads.  The step loop is unrolled by 4 so that
+// every per-column history (planes s … s-3) is a compile-time-indexed register ring.
+// Per step s:
+//   load plane s | red at plane s-1 on x, y in [-1, 17) | black at s-2 on [0, 16)^2.
+// Δ_h^M of a node = (2F + E - 24c)/(6h^2) (M=4) or (F - 6c)/h^2 (M=2), with
+//   F = S4(z) + c(z-1) + c(z+1)  (6 faces),  E = D4(z) + S4(z-1) + S4(z+1)  (12 edges),
+// S4/D4 the sums of the 4 in-plane face / diagonal neighbours.  For a red node all
+// operands are old values; for a black node the faces are red (new, after the red
+// phase) and the edges and centre black (old).
+// ---------------------------------------------------------------------------------
+template <int D>
+struct RBShape {
+  static constexpr int T = PB + 4;                 // 20: x, y in [-2, 18)
+  // row pitch 26 doubles: a warp's 3 same-parity rows (2 apart, 416 B ≡ 32 mod 128)
+  // read with 16-byte loads are bank-conflict free
+  static constexpr int TW = 26;
+  static constexpr int TP = T * TW;                // 520 doubles per plane
+  static constexpr int R = 8;                      // plane ring (power of 2)
+  static constexpr int NT = 192;                   // 6 warps x (30 pair-threads + 2 idle)
+  static constexpr int NPAIR = T * T / 2;          // 200 16-byte u pairs per plane
+  static constexpr int NLD = (NPAIR + NT - 1) / NT;  // 2
+  // [R][TP] old u | [2][TP] red-phase values | [R][NT] f pairs
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + 2 * TP + R * NT * 2);
+  static_assert(D + 3 <= R, "ring too small for the prefetch depth");
+};
+
+struct RBCtx {
+  const int* snb;
+  const uint32_t* sreal;
+  double* su;
+  double* sn;
+  double2* sf;
+  int len, nz;
+  int ld_xy[2], ld_sxy[2], ld_dst[2];
+};
+
+__device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+
+template <int ORDER, int D, int RP>
+__device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int wg, int lane, double omega,
+                                        double inv_h2, double inv_d) {
+  using S = RBShape<D>;
+  constexpr int TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NLD = S::NLD;
+  constexpr int PC = RP;  // column (0 = a = x0, 1 = b = x0+1) that is red at even planes
+  const int* snb = cx.snb;
+  const int len = cx.len, nz = cx.nz;
+  double* su = cx.su;
+  double* sn = cx.sn;
+  const int tid = threadIdx.x;
+  double2* sfme = cx.sf + tid;  // this thread's f pair, slot stride NT
+  const bool valid = lane < 30;  // lanes 30, 31 mirror lane 29 (broadcast reads), write nothing
+  const int ri = valid ? 3 * wg + lane / 10 : 3 * wg + 2;
+  const int cy = 2 * ri - RP, x0 = valid ? 2 * (lane % 10) - 2 : 16;
+  const int i0 = (cy + 2) * TW + (x0 + 2);
+  const int dxc = reg16(x0), dyc = reg16(cy);
+  const int sxy = (dxc + 1) + 3 * (dyc + 1);
+  const int fxy = (cy - PB * dyc) * PB + (x0 - PB * dxc);
+  const bool inner = valid && dxc == 0 && dyc == 0;
+
+  // ---- plane cursors: source pointers change only at block boundaries (z % 16 == 0)
+  // and at the pencil ends; between them they advance by one plane (PB^2 doubles).
+  const double* ip[NLD];
+  const double* fp = nullptr;
+  int zi = -2;
+  auto seek_issue = [&](int z) {
+    int k, dz, zl;
+    plane_src(z, nz, len, k, dz, zl);
+    const int o = zl * (PB * PB);
+#pragma unroll
+    for (int d = 0; d < NLD; ++d)
+      ip[d] = cx.ld_sxy[d] < 0 ? nullptr
+                               : L.u + (size_t)snb[k * 27 + cx.ld_sxy[d] + 9 * (dz + 1)] * PB3 + o + cx.ld_xy[d];
+    fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
+  };
+  auto issue = [&]() {
+    if (zi < nz + 2) {
+      if ((zi & 15) == 0) seek_issue(zi);
+      const int slot = (zi + 2) & (R - 1);
+      double* dst = su + slot * TP;
+#pragma unroll
+      for (int d = 0; d < NLD; ++d) {
+        if (cx.ld_sxy[d] < 0) continue;
+        cpa16(dst + cx.ld_dst[d], ip[d]);
+        ip[d] += PB * PB;
+      }
+      if (valid && zi >= -1 && zi <= nz) cpa16(sfme + slot * NT, fp);
+      fp += PB * PB;
+    }
+    cpa_commit();
+    ++zi;
+  };
+  bool live = false;  // red-phase liveness of this pair's columns at plane r
+  auto seek_live = [&](int z) {
+    int k, dz, zl;
+    plane_src(z, nz, len, k, dz, zl);
+    live = valid && ((cx.sreal[k] >> (sxy + 9 * (dz + 1))) & 1u);
+  };
+  seek_issue(-2);
+  seek_live(-1);
+#pragma unroll
+  for (int q = 0; q < D; ++q) issue();
+
+  // Per-column accumulators (column q = a, b).  With α(z) = 2c(z) + S4(z),
+  // β(z) = 2S4(z) + D4(z) - 24c(z), γ(z) = 2n(z) + S4(z) (n = value after the red
+  // phase), the Mehrstellen operator times 6h^2 is
+  //   red node at r:   α(r-1) + β(r) + α(r+1)                   (all old values)
+  //   black node at b: γ(b-1) + 2 S4n(b) + D4(b) - 24c(b) + γ(b+1)  (S4n: red, new)
+  // so each column carries only partial sums between steps.
+  double accR[2] = {0, 0}, cR[2] = {0, 0};  // red plane: α(r-1) + β(r), c(r)
+  double accB[2] = {0, 0}, cB[2] = {0, 0};  // black plane: D4(b) - 24c(b) + γ(b-1), c(b)
+  double s4r[2] = {0, 0};                   // S4 at the column's last red plane
+  double nl[2] = {0, 0};                    // value after the red phase at the last red plane
+  const double h6 = inv_h2 * (1.0 / 6.0);
+  const double wd = omega * inv_d;
+  double2 fr = make_double2(0.0, 0.0);  // f pair at the plane of the last red phase
+  double fb = 0.0;                      // f of the column black at plane s-2
+
+  for (int s0 = -2; s0 < nz + 2; s0 += 4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int s = s0 + j;
+      const int X = (j & 1) ? PC : 1 - PC;  // red at s-1 (black at s and s-2); s0 even
+      const int O = 1 - X;                  // red at s (and s-2)
+      cpa_wait<D - 1>();
+      __syncthreads();
+      issue();
+      double cq[2], s4q[2], d4q[2];
+      {
+        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+        const double2 m = *reinterpret_cast<const double2*>(U - TW);
+        const double2 cc = *reinterpret_cast<const double2*>(U);
+        const double2 p = *reinterpret_cast<const double2*>(U + TW);
+        const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);  // u(x0-1), u(x0+2)
+        cq[0] = cc.x;
+        cq[1] = cc.y;
+        s4q[0] = (l + cc.y) + (m.x + p.x);
+        s4q[1] = (cc.x + r) + (m.y + p.y);
+        if (ORDER == 4) {
+          const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
+          d4q[0] = (ml + m.y) + (pl + p.y);
+          d4q[1] = (m.x + mr) + (p.x + pr);
+        } else {
+          d4q[0] = d4q[1] = 0.0;
+        }
+      }
+      // in-row red neighbour of the black node at s-2 held by the adjacent lane
+      const double nx = X ? shfl_dn1(nl[0]) : shfl_up1(nl[1]);
+      // column X: black at plane s
+      const double alpha = ORDER == 4 ? 2.0 * cq[X] + s4q[X] : cq[X];
+      if (s >= 0) {  // red half-sweep at plane r = s-1 in [-1, nz] (column X)
+        if (((s - 1) & 15) == 0) seek_live(s - 1);
+        fb = X ? fr.y : fr.x;                 // f at plane s-2 of column X (pair read last step)
+        fr = sfme[((s + 1) & (R - 1)) * NT];  // f pair at plane s-1
+        double v = cR[X];
+        if (live) {
+          const double Lu = ORDER == 4 ? (accR[X] + alpha) * h6 : (accR[X] + alpha) * inv_h2;
+          v = cR[X] + wd * ((X ? fr.y : fr.x) - Lu);
+        }
+        if (valid) sn[(j & 1) * TP + i0 + X] = v;  // new-plane slot = parity of s
+        const double g = ORDER == 4 ? 2.0 * v + s4r[X] : v;  // γ(s-1) of column X
+        if (s >= 2 && inner) {  // black half-sweep at plane b = s-2 (column X)
+          const double* N = sn + ((j & 1) ^ 1) * TP + i0 + X;
+          const double S4n = (nl[O] + nx) + (N[-TW] + N[TW]);
+          const double Lu = ORDER == 4 ? (accB[X] + 2.0 * S4n + g) * h6 : (accB[X] + S4n + g) * inv_h2;
+          const double vb = cB[X] + wd * (fb - Lu);
+          double* op = L.u_out + (size_t)snb[((s - 2) >> 4) * 27 + 13] * PB3 + ((s - 2) & 15) * (PB * PB) + fxy;
+          *reinterpret_cast<double2*>(op) = X ? make_double2(nl[O], vb) : make_double2(vb, nl[O]);
+        }
+        accB[X] = (ORDER == 4 ? d4q[X] - 24.0 * cq[X] : -6.0 * cq[X]) + g;
+        nl[X] = v;
+      }
+      cB[X] = cq[X];
+      accR[X] = alpha;  // α(s): first term of the red node at s+1
+      // column O: red at plane s
+      accR[O] += ORDER == 4 ? 2.0 * s4q[O] + d4q[O] - 24.0 * cq[O] : s4q[O] - 6.0 * cq[O];
+      cR[O] = cq[O];
+      s4r[O] = s4q[O];
+    }
+  }
+  cpa_wait<0>();
+}
+
+template <int ORDER, int D>
+__global__ void __maxnreg__(96)
+    k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
+  using S = RBShape<D>;
+  constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int snb[PMAXL * 27];
+  __shared__ uint32_t sreal[PMAXL];
+  const int tid = threadIdx.x;
+  RBCtx cx;
+  cx.len = __ldg(L.pen_len + blockIdx.x);
+  cx.nz = PB * cx.len;
+  cx.snb = snb;
+  cx.sreal = sreal;
+  cx.su = sm;
+  cx.sn = sm + R * TP;
+  cx.sf = reinterpret_cast<double2*>(sm + R * TP + 2 * TP);
+  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  for (int i = tid; i < cx.len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  if (tid < cx.len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
+#pragma unroll
+  for (int d = 0; d < NLD; ++d) {
+    const int j = tid + d * NT;
+    const int py = j / (T / 2), px = 2 * (j % (T / 2));
+    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
+    cx.ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
+    cx.ld_sxy[d] = j < NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
+    cx.ld_dst[d] = py * TW + px;
+  }
+  __syncthreads();  // snb / sreal
+  // warp-uniform row parity: warps 0-2 even rows, 3-5 odd rows
+  const int w = tid >> 5, lane = tid & 31;
+  if (w < 3) rb_body<ORDER, D, 0>(L, cx, w, lane, omega, inv_h2, inv_d);
+  else rb_body<ORDER, D, 1>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
+}
+
+// ---------------------------------------------------------------------------------
+// Residual r = f - Δ_h^M u (Alg. 1) on every node of the pencil's blocks.
+// Plane tile of u: x, y in [-2, 18) (halo 1 used; pairs keep 16-byte alignment);
+// f: the block's own 16 x 16 plane.  One thread per interior column (256).
+// ---------------------------------------------------------------------------------
+template <int D>
+struct ResShape {
+  static constexpr int T = PB + 4, TP = T * T;  // 20, 400
+  static constexpr int FP = PB * PB;            // 256
+  static constexpr int R = D + 2;
+  static constexpr int NT = PB * PB;            // 256
+  static constexpr int NUP = TP / 2, NFP = FP / 2;  // 200 + 128 pairs
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * (TP + FP));
+};
+
+template <int ORDER, int D>
+__global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, double inv_h2) {
+  using S = ResShape<D>;
+  constexpr int T = S::T, TP = S::TP, FP = S::FP, R = S::R, NT = S::NT;
+  extern __shared__ __align__(16) double sm[];
+  double* su = sm;           // [R][TP]
+  double* sf = sm + R * TP;  // [R][FP]
+  __shared__ int snb[PMAXL * 27];
+  const int tid = threadIdx.x;
+  const int len = __ldg(L.pen_len + blockIdx.x);
+  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  const int nz = PB * len;
+
+  int ld_xy[2], ld_sxy[2], ld_dst[2];
+  bool ld_on[2], ld_f[2];
+#pragma unroll
+  for (int d = 0; d < 2; ++d) {
+    const int j = tid + d * NT;
+    ld_on[d] = j < S::NUP + S::NFP;
+    ld_f[d] = j >= S::NUP;
+    if (ld_f[d]) {
+      const int jj = j - S::NUP;
+      ld_xy[d] = 2 * jj;
+      ld_sxy[d] = 4;  // own block (dx = dy = 0)
+      ld_dst[d] = R * TP + 2 * jj;
+    } else {
+      const int py = j / (T / 2), px = 2 * (j % (T / 2));
+      const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
+      ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
+      ld_sxy[d] = (dx + 1) + 3 * (dy + 1);
+      ld_dst[d] = py * T + px;
+    }
+  }
+  __syncthreads();
+
+  auto issue = [&](int z) {
+    if (z < nz + 1) {
+      int k, dz, zl;
+      plane_src(z, nz, len, k, dz, zl);
+      const int slot = (z + 1) % R;
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        if (!ld_on[d] || (ld_f[d] && dz != 0)) continue;
+        const int blk = snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)];
+        const double* src = (ld_f[d] ? L.f : L.u) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
+        cpa16(sm + ld_dst[d] + slot * (ld_f[d] ? FP : TP), src);
+      }
+    }
+    cpa_commit();
+  };
+
+  const int cx = tid % PB, cy = tid / PB;
+  const int ci = (cy + 2) * T + (cx + 2);
+#pragma unroll
+  for (int q = 0; q < D; ++q) issue(-1 + q);
+
+  double c0 = 0, c1 = 0, c2 = 0, a0 = 0, a1 = 0, a2 = 0;
+  const double h6 = inv_h2 * (1.0 / 6.0);
+  for (int s = -1; s < nz + 1; ++s) {
+    cpa_wait<D - 1>();
+    __syncthreads();
+    issue(s + D);
+    c2 = c1; c1 = c0;
+    a2 = a1; a1 = a0;
+    {
+      const double* U = su + ((s + 1) % R) * TP + ci;
+      c0 = U[0];
+      a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
+    }
+    if (s >= 1) {
+      const int r = s - 1;
+      const int sl = (r + 1) % R;
+      const double f = sf[sl * FP + tid];
+      double Lu;
+      if (ORDER == 2) {
+        Lu = ((a1 + (c2 + c0)) - 6.0 * c1) * inv_h2;
+      } else {
+        const double* U = su + sl * TP + ci;
+        const double Dg = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
+        const double F = a1 + (c2 + c0);
+        const double E = Dg + (a2 + a0);
+        Lu = (2.0 * F + E - 24.0 * c1) * h6;
+      }
+      L.r[(size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid] = f - Lu;
+    }
+  }
+  cpa_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------
+constexpr int RB_D = 5;
+constexpr int RES_D = 3;
+
+void prepare_pencil_kernels() {
+  // the whole unified L1 as shared memory: several pencil CTAs per SM
+  auto setup = [](const void* k, size_t smem) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  };
+  setup((const void*)k_rb_pencil<2, RB_D>, RBShape<RB_D>::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D>, RBShape<RB_D>::SMEM);
+  setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D>, ResShape<RES_D>::SMEM);
+}
+
+bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s) {
+  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
+  if (order == 2)
+    k_rb_pencil<2, RB_D><<<L.npen, RBShape<RB_D>::NT, RBShape<RB_D>::SMEM, s>>>(L, omega, inv_h2, inv_d);
+  else
+    k_rb_pencil<4, RB_D><<<L.npen, RBShape<RB_D>::NT, RBShape<RB_D>::SMEM, s>>>(L, omega, inv_h2, inv_d);
+  note_launch();
+  return true;
+}
+
+bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s) {
+  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  if (order == 2) k_res_pencil<2, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
+  else k_res_pencil<4, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
+  note_launch();
+  return true;
+}
+
+}  // namespace mg
