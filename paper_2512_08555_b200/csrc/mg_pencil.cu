@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "mg_internal.h"
 
@@ -75,20 +76,22 @@ __device__ __forceinline__ void plane_src(int z, int nz, int len, int& k, int& d
 // operands are old values; for a black node the faces are red (new, after the red
 // phase) and the edges and centre black (old).
 // ---------------------------------------------------------------------------------
-template <int D>
+template <int D, int RR>
 struct RBShape {
   static constexpr int T = PB + 4;                 // 20: x, y in [-2, 18)
   // row pitch 26 doubles: a warp's 3 same-parity rows (2 apart, 416 B ≡ 32 mod 128)
   // read with 16-byte loads are bank-conflict free
   static constexpr int TW = 26;
   static constexpr int TP = T * TW;                // 520 doubles per plane
-  static constexpr int R = 8;                      // plane ring (power of 2)
+  static constexpr int R = RR;                     // plane ring (power of 2)
   static constexpr int NT = 192;                   // 6 warps x (30 pair-threads + 2 idle)
   static constexpr int NPAIR = T * T / 2;          // 200 16-byte u pairs per plane
   static constexpr int NLD = (NPAIR + NT - 1) / NT;  // 2
-  // [R][TP] old u | [2][TP] red-phase values | [R][NT] f pairs
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + 2 * TP + R * NT * 2);
-  static_assert(D + 3 <= R, "ring too small for the prefetch depth");
+  // red-phase values, one per pair: [2 planes][18 rows][pitch 13] (conflict-free)
+  static constexpr int SNW = 13, SNP = 18 * SNW;
+  // [R][TP] old u | [2][SNP] red-phase values | [R][NT] f pairs
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + 2 * SNP + R * NT * 2);
+  static_assert((R & (R - 1)) == 0 && D + 2 <= R, "ring too small for the prefetch depth");
 };
 
 struct RBCtx {
@@ -104,11 +107,11 @@ struct RBCtx {
 __device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-template <int ORDER, int D, int RP>
+template <int ORDER, int D, int RR, int RP>
 __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int wg, int lane, double omega,
                                         double inv_h2, double inv_d) {
-  using S = RBShape<D>;
-  constexpr int TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NLD = S::NLD;
+  using S = RBShape<D, RR>;
+  constexpr int TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NLD = S::NLD, SNW = S::SNW, SNP = S::SNP;
   constexpr int PC = RP;  // column (0 = a = x0, 1 = b = x0+1) that is red at even planes
   const int* snb = cx.snb;
   const int len = cx.len, nz = cx.nz;
@@ -118,8 +121,10 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   double2* sfme = cx.sf + tid;  // this thread's f pair, slot stride NT
   const bool valid = lane < 30;  // lanes 30, 31 mirror lane 29 (broadcast reads), write nothing
   const int ri = valid ? 3 * wg + lane / 10 : 3 * wg + 2;
-  const int cy = 2 * ri - RP, x0 = valid ? 2 * (lane % 10) - 2 : 16;
+  const int pi = valid ? lane % 10 : 9;
+  const int cy = 2 * ri - RP, x0 = 2 * pi - 2;
   const int i0 = (cy + 2) * TW + (x0 + 2);
+  double* snme = sn + (cy + 1) * SNW + pi;  // this pair's red value (row cy) in the compact planes
   const int dxc = reg16(x0), dyc = reg16(cy);
   const int sxy = (dxc + 1) + 3 * (dyc + 1);
   const int fxy = (cy - PB * dyc) * PB + (x0 - PB * dxc);
@@ -224,11 +229,11 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
           const double Lu = ORDER == 4 ? (accR[X] + alpha) * h6 : (accR[X] + alpha) * inv_h2;
           v = cR[X] + wd * ((X ? fr.y : fr.x) - Lu);
         }
-        if (valid) sn[(j & 1) * TP + i0 + X] = v;  // new-plane slot = parity of s
+        if (valid) snme[(j & 1) * SNP] = v;  // new-plane slot = parity of s
         const double g = ORDER == 4 ? 2.0 * v + s4r[X] : v;  // γ(s-1) of column X
         if (s >= 2 && inner) {  // black half-sweep at plane b = s-2 (column X)
-          const double* N = sn + ((j & 1) ^ 1) * TP + i0 + X;
-          const double S4n = (nl[O] + nx) + (N[-TW] + N[TW]);
+          const double* N = snme + ((j & 1) ^ 1) * SNP;  // rows cy±1 hold the red node at x of X
+          const double S4n = (nl[O] + nx) + (N[-SNW] + N[SNW]);
           const double Lu = ORDER == 4 ? (accB[X] + 2.0 * S4n + g) * h6 : (accB[X] + S4n + g) * inv_h2;
           const double vb = cB[X] + wd * (fb - Lu);
           double* op = L.u_out + (size_t)snb[((s - 2) >> 4) * 27 + 13] * PB3 + ((s - 2) & 15) * (PB * PB) + fxy;
@@ -248,10 +253,10 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   cpa_wait<0>();
 }
 
-template <int ORDER, int D>
-__global__ void __maxnreg__(96)
+template <int ORDER, int D, int RR, int NREG>
+__global__ void __maxnreg__(NREG)
     k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
-  using S = RBShape<D>;
+  using S = RBShape<D, RR>;
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
   extern __shared__ __align__(16) double sm[];
   __shared__ int snb[PMAXL * 27];
@@ -264,7 +269,7 @@ __global__ void __maxnreg__(96)
   cx.sreal = sreal;
   cx.su = sm;
   cx.sn = sm + R * TP;
-  cx.sf = reinterpret_cast<double2*>(sm + R * TP + 2 * TP);
+  cx.sf = reinterpret_cast<double2*>(sm + R * TP + 2 * S::SNP);
   const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
   for (int i = tid; i < cx.len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
   if (tid < cx.len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
@@ -280,8 +285,8 @@ __global__ void __maxnreg__(96)
   __syncthreads();  // snb / sreal
   // warp-uniform row parity: warps 0-2 even rows, 3-5 odd rows
   const int w = tid >> 5, lane = tid & 31;
-  if (w < 3) rb_body<ORDER, D, 0>(L, cx, w, lane, omega, inv_h2, inv_d);
-  else rb_body<ORDER, D, 1>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
+  if (w < 3) rb_body<ORDER, D, RR, 0>(L, cx, w, lane, omega, inv_h2, inv_d);
+  else rb_body<ORDER, D, RR, 1>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
 }
 
 // ---------------------------------------------------------------------------------
@@ -390,8 +395,30 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
 }
 
 // ---------------------------------------------------------------------------------
-constexpr int RB_D = 5;
 constexpr int RES_D = 3;
+
+// RB sweep variants (prefetch depth D, ring R, register cap): MG_RB_VAR selects one
+// for tuning; the default is the fastest measured on B200.
+struct RBVar {
+  void (*k2)(LevelView, double, double, double);
+  void (*k4)(LevelView, double, double, double);
+  size_t smem;
+};
+template <int D, int RR, int NREG>
+static RBVar rb_var() {
+  return {k_rb_pencil<2, D, RR, NREG>, k_rb_pencil<4, D, RR, NREG>, RBShape<D, RR>::SMEM};
+}
+static const RBVar& rb_pick() {
+  // cfg2 256^3 finest sweep on B200 (tools/time_ops.py): <2,4,80> 108.7 us (4 CTAs/SM),
+  // <2,4,96> 116.5, <5,8,96> 120.9, <2,4,72> 124.6 (spills), <3,8,80> 129.4 (smem: 3 CTAs/SM)
+  static RBVar vars[] = {rb_var<2, 4, 80>(), rb_var<2, 4, 96>(), rb_var<5, 8, 96>(), rb_var<3, 8, 80>()};
+  static int sel = [] {
+    const char* e = std::getenv("MG_RB_VAR");
+    const int v = e ? std::atoi(e) : 0;
+    return (v >= 0 && v < (int)(sizeof(vars) / sizeof(vars[0]))) ? v : 0;
+  }();
+  return vars[sel];
+}
 
 void prepare_pencil_kernels() {
   // the whole unified L1 as shared memory: several pencil CTAs per SM
@@ -399,8 +426,9 @@ void prepare_pencil_kernels() {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   };
-  setup((const void*)k_rb_pencil<2, RB_D>, RBShape<RB_D>::SMEM);
-  setup((const void*)k_rb_pencil<4, RB_D>, RBShape<RB_D>::SMEM);
+  const RBVar& v = rb_pick();
+  setup((const void*)v.k2, v.smem);
+  setup((const void*)v.k4, v.smem);
   setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D>, ResShape<RES_D>::SMEM);
 }
@@ -409,10 +437,8 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
-  if (order == 2)
-    k_rb_pencil<2, RB_D><<<L.npen, RBShape<RB_D>::NT, RBShape<RB_D>::SMEM, s>>>(L, omega, inv_h2, inv_d);
-  else
-    k_rb_pencil<4, RB_D><<<L.npen, RBShape<RB_D>::NT, RBShape<RB_D>::SMEM, s>>>(L, omega, inv_h2, inv_d);
+  const RBVar& v = rb_pick();
+  (order == 2 ? v.k2 : v.k4)<<<L.npen, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
   note_launch();
   return true;
 }
