@@ -575,7 +575,7 @@ void build_ghosts(mg_handle* h) {
 // `lmax` blocks, longest first.  The z-marching kernels (mg_pencil.cu) walk one
 // pencil per CTA; halos above/below a pencil come through the neighbour tables.
 void build_pencils(mg_handle* h) {
-  int lmax = 4;
+  int lmax = 2;  // cfg2 256^3 on B200: 2 blocks per pencil beats 4 (more CTAs, shorter tail)
   if (const char* e = std::getenv("MG_PENCIL")) lmax = std::max(1, std::min(16, std::atoi(e)));
   const bool off = std::getenv("MG_NO_PENCIL") != nullptr;
   for (auto& l : h->L) {
