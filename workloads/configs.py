@@ -5,6 +5,10 @@ Recipes are stated in DESIGN.md §Inputs; seeds are fixed here.
 """
 from __future__ import annotations
 
+import hashlib
+import json
+import os
+
 import numpy as np
 
 from . import sources as S
@@ -85,10 +89,38 @@ def source_fn(cfg):
     raise KeyError(s)
 
 
+LAYOUT_VERSION = 1   # bump when the refinement recipe (layouts.py) changes
+CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cache")
+
+
+def _cache_path(cfg) -> str:
+    keys = ("source", "seed", "base_blocks", "max_level", "target_leaves", "h0", "origin", "bc", "B")
+    txt = json.dumps({k: cfg.get(k) for k in keys}, sort_keys=True, default=list) + f"v{LAYOUT_VERSION}"
+    return os.path.join(CACHE_DIR, f"{cfg['name']}_{hashlib.sha1(txt.encode()).hexdigest()[:12]}.npz")
+
+
 def leaves_for(cfg) -> np.ndarray:
+    """Leaf list of a config.  Adaptive layouts (tau bisection, minutes of pure Python
+    for cfg5) are cached under workloads/cache/ keyed by the recipe parameters; the
+    cache holds inputs only (no method arithmetic) and is regenerated when absent."""
     dom = domain(cfg)
     if cfg["max_level"] == 0:
         return uniform_leaves(dom, 0)
+    path = _cache_path(cfg)
+    if os.path.exists(path):
+        z = np.load(path)
+        cfg["tau"] = float(z["tau"])
+        return z["leaves"].astype(np.int32)
+    leaves = _adaptive_leaves(cfg, dom)
+    try:
+        os.makedirs(CACHE_DIR, exist_ok=True)
+        np.savez_compressed(path, leaves=leaves, tau=cfg["tau"])
+    except OSError:
+        pass
+    return leaves
+
+
+def _adaptive_leaves(cfg, dom) -> np.ndarray:
     fn = source_fn(cfg)
 
     def score(lev, coords):

@@ -129,29 +129,31 @@ class Tree:
 
     def balance(self, forbid):
         """26-neighbour 2:1 balance. Returns [] or the list of (leaf_level, leaf)
-        whose refinement cannot be balanced without refining a forbidden block."""
-        changed = True
+        whose refinement cannot be balanced without refining a forbidden block.
+
+        One pass from the finest level down suffices: making the level-(lev-1)
+        neighbourhood of a level-lev leaf exist only refines blocks of levels
+        <= lev-2, i.e. creates blocks of levels < lev, which are visited later."""
         bad = []
-        while changed and not bad:
-            changed = False
-            for lev in sorted(self.nodes, reverse=True):
-                if lev < 2:
+        for lev in sorted(self.nodes, reverse=True):
+            if lev < 2:
+                continue
+            for b in sorted(self.nodes[lev]):
+                if self.refined(lev, b):
                     continue
-                for b in sorted(self.nodes[lev]):
-                    if self.refined(lev, b):
+                for o in OFFS26:
+                    n = self.wrap(lev, (b[0] + o[0], b[1] + o[1], b[2] + o[2]))
+                    if n is None:
                         continue
-                    for o in OFFS26:
-                        n = self.wrap(lev, (b[0] + o[0], b[1] + o[1], b[2] + o[2]))
-                        if n is None:
-                            continue
-                        p = (n[0] // 2, n[1] // 2, n[2] // 2)
-                        if self.has(lev - 1, p):
-                            continue
-                        r = self.ensure(lev - 1, p, forbid)
-                        if r is not None:
-                            bad.append((lev, b))
-                            break
-                        changed = True
+                    p = (n[0] // 2, n[1] // 2, n[2] // 2)
+                    if self.has(lev - 1, p):
+                        continue
+                    r = self.ensure(lev - 1, p, forbid)
+                    if r is not None:
+                        bad.append((lev, b))
+                        break
+            if bad:
+                break
         return bad
 
 
