@@ -88,7 +88,7 @@ struct Level {
   std::vector<uint8_t> ghost_ext;           // per ghost block: beyond an unbounded face
   bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
   // host tables
-  std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len;
+  std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len, gbox;
   int pen_lmax = 0;
   std::vector<uint32_t> nbr_real;
   std::vector<uint8_t> covmask, c2f_ext;
@@ -98,7 +98,8 @@ struct Level {
   double *f = nullptr, *r = nullptr, *uhat = nullptr;
   int cur = 0;
   int32_t *d_nbr = nullptr, *d_parent = nullptr, *d_bmap = nullptr, *d_c2f_dst = nullptr, *d_c2f_J = nullptr,
-          *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr;
+          *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr,
+          *d_gbox = nullptr;
   uint32_t* d_nbr_real = nullptr;
   uint8_t *d_covmask = nullptr, *d_c2f_ext = nullptr;
 
@@ -570,6 +571,32 @@ void build_ghosts(mg_handle* h) {
   }
 }
 
+// Ghost boxes of levels >= 1: per ghost block, the bounding box of its needed nodes
+// (record: block, lo[3], hi[3] block-local, org[3] level-global index of node (0,0,0),
+// 2 unused).  The c2f kernel (mg_ghost.cu) fills one box per CTA.
+void build_ghost_boxes(mg_handle* h) {
+  for (size_t m = 1; m < h->L.size(); ++m) {
+    Level& l = h->L[m];
+    l.gbox.clear();
+    for (int gi = 0; gi < l.nghost; ++gi) {
+      int lo[3] = {l.B, l.B, l.B}, hi[3] = {0, 0, 0};
+      for (int loc = 0; loc < l.B3; ++loc) {
+        if (!((l.need[gi][loc >> 6] >> (loc & 63)) & 1)) continue;
+        const int q[3] = {loc % l.B, (loc / l.B) % l.B, loc / (l.B * l.B)};
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = std::min(lo[a], q[a]);
+          hi[a] = std::max(hi[a], q[a] + 1);
+        }
+      }
+      if (hi[0] <= lo[0]) continue;
+      const auto c = l.coords[l.nreal + gi];
+      const int32_t rec[12] = {l.nreal + gi, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2],
+                               c[0] * l.B, c[1] * l.B, c[2] * l.B, 0, 0};
+      l.gbox.insert(l.gbox.end(), rec, rec + 12);
+    }
+  }
+}
+
 // Pencils of B = 16 levels: maximal runs of consecutive real blocks along z (same
 // bx, by; no periodic wrap inside a run), split into near-equal chunks of at most
 // `lmax` blocks, longest first.  The z-marching kernels (mg_pencil.cu) walk one
@@ -641,6 +668,7 @@ void alloc_device(mg_handle* h) {
     l.d_inj_src = dev_upload(l.inj_src);
     l.d_pen_blk = dev_upload(l.pen_blk);
     l.d_pen_len = dev_upload(l.pen_len);
+    l.d_gbox = dev_upload(l.gbox);
   }
   // leaf map: leaf n -> (level, block)
   std::vector<int64_t> map(h->leaves.size());
@@ -746,9 +774,9 @@ void refresh(mg_handle* h, int m) {
   }
   for (int j = lo; j <= m; ++j) {
     Level& F = h->L[j];
-    if (F.c2f_dst.empty()) continue;
+    if (F.gbox.empty()) continue;
     LevelView fv = view(h, j), cv = view(h, j - 1);
-    launch_c2f(fv, cv, c2f_list(F), F.u[F.cur], cv.u, h->I, false, h->s);
+    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / 12, F.u[F.cur], cv.u, h->I, false, h->s);
   }
 }
 
@@ -944,9 +972,9 @@ void set_rhs(mg_handle* h, const double* f_dev) {
   // f ghosts: c2f of f, f := 0 beyond unbounded faces (reading Z16)
   for (int m = 1; m < nlev; ++m) {
     Level& F = h->L[m];
-    if (F.c2f_dst.empty()) continue;
+    if (F.gbox.empty()) continue;
     LevelView fv = view(h, m), cv = view(h, m - 1);
-    launch_c2f(fv, cv, c2f_list(F), F.f, h->L[m - 1].f, h->I, true, h->s);
+    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / 12, F.f, h->L[m - 1].f, h->I, true, h->s);
   }
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
@@ -969,7 +997,7 @@ void destroy(mg_handle* h) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
                     (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
                     (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src, (void*)l.d_pen_blk,
-                    (void*)l.d_pen_len})
+                    (void*)l.d_pen_len, (void*)l.d_gbox})
       if (p) cudaFree(p);
   }
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
@@ -1021,6 +1049,7 @@ int mg_create(const mg_desc* d, void* stream, mg_handle** out) {
     prepare_kernels();
     validate_and_build(h);
     build_ghosts(h);
+    build_ghost_boxes(h);
     build_pencils(h);
     alloc_device(h);
     setup_coarse(h);

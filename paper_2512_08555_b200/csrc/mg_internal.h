@@ -61,6 +61,10 @@ bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
 void prepare_pencil_kernels();
 void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
                 const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
+// separable box c2f (mg_ghost.cu): boxes = [nbox][12] int32 records (see mg_host.cpp)
+void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox,
+                    double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
+void prepare_ghost_kernels();
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);

@@ -479,6 +479,7 @@ static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res
 void prepare_kernels() {
   upload_weights();
   prepare_pencil_kernels();
+  prepare_ghost_kernels();
   prepare_b<16, 2>(); prepare_b<16, 4>();
   prepare_b<8, 2>(); prepare_b<8, 4>();
   prepare_b<4, 2>(); prepare_b<4, 4>();
