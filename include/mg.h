@@ -117,12 +117,15 @@ int mg_use_graph(mg_handle* h, int enable);
 enum { MG_INFO_NLEVELS = 0 };
 /* info[0..9] = B, n_real, n_ghost, N[3], amr_level, n_c2f, n_inject, n_leaf_blocks */
 int mg_level_info(mg_handle* h, int level, int64_t* info);
-/* host int32[n_real][3]: block coordinates of the level's real blocks (storage order) */
+/* host int32[n][3]: block coordinates of the level's real blocks (storage order);
+ * with `level | MG_ALL_BLOCKS`, real then ghost blocks (n = n_real + n_ghost) */
+enum { MG_ALL_BLOCKS = 0x10000 };
 int mg_level_blocks(mg_handle* h, int level, int32_t* coords_host);
 int mg_num_levels(mg_handle* h);
 
 enum { MG_FIELD_U = 0, MG_FIELD_F = 1, MG_FIELD_R = 2, MG_FIELD_UHAT = 3 };
-/* dir 0: export the level's real blocks [n_real][B^3] into dev; 1: import from dev */
+/* dir 0: export the level's real blocks [n_real][B^3] into dev; 1: import from dev;
+ * 2: export real then ghost blocks [n_real + n_ghost][B^3] (ghost-fill checks) */
 int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev);
 enum {
   MG_OP_REFRESH = 0,        /* ghost fill of `level` (f2c injection + c2f / band) */

@@ -538,6 +538,29 @@ void build_ghosts(mg_handle* h) {
       }
     }
   }
+  // Exterior chains (reading U1): refreshing level m recomputes the exterior ghosts of
+  // every level 1..m, and the oracle's W_{j-1} holds, at EVERY covered node, the value
+  // injected from level j (recursively from the finest level).  The per-level f2c lists
+  // above only cover the tap hull of level j's own ghosts, so close them: every level-
+  // (j-1) node that inj(j-1) reads and that level j covers must first be injected from
+  // level j.  (Coarse to fine, so additions to inj(j-1) propagate.)
+  for (int j = 2; j < nlev; ++j) {
+    if (!h->L[j].ext_chain) continue;
+    Level &F = h->L[j], &C = h->L[j - 1];
+    std::unordered_set<int32_t> have(F.inj_dst.begin(), F.inj_dst.end());
+    for (int32_t src : C.inj_src) {
+      const int blk = src / C.B3, loc = src % C.B3;
+      const int Jx = C.coords[blk][0] * C.B + loc % C.B, Jy = C.coords[blk][1] * C.B + (loc / C.B) % C.B,
+                Jz = C.coords[blk][2] * C.B + loc / (C.B * C.B);
+      int fflat;
+      if (!is_real_node(h, F, 2 * Jx, 2 * Jy, 2 * Jz, &fflat)) continue;
+      if (have.insert(src).second) {
+        F.inj_dst.push_back(src);
+        F.inj_src.push_back(fflat);
+      }
+    }
+  }
+
   // neighbour tables and block maps
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
@@ -883,6 +906,15 @@ void run_vcycles(mg_handle* h, int n) {
     for (int i = 0; i < n; ++i) vcycle_body(h);
     return;
   }
+  // the captured graph bakes in the ping-pong parity of every level's u buffers:
+  // re-capture if it changed since (debug single sweeps, set_solution)
+  int sig = 0;
+  for (size_t m = 0; m < h->L.size(); ++m) sig |= h->L[m].cur << (m % 30);
+  if (h->gexec && sig != h->graph_cur_sig) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  h->graph_cur_sig = sig;
   if (!h->gexec) {
     // capture on a private stream (the caller's may be the legacy default stream,
     // which cannot be captured), replay on the caller's stream
@@ -1205,9 +1237,12 @@ int mg_level_info(mg_handle* h, int level, int64_t* info) {
 }
 
 int mg_level_blocks(mg_handle* h, int level, int32_t* coords) {
+  const bool all = (level & MG_ALL_BLOCKS) != 0;
+  level &= ~MG_ALL_BLOCKS;
   if (!h || !coords || level < 0 || level >= (int)h->L.size()) return MG_ERR_ARG;
   Level& l = h->L[level];
-  for (int i = 0; i < l.nreal; ++i)
+  const int n = all ? l.ntot() : l.nreal;
+  for (int i = 0; i < n; ++i)
     for (int a = 0; a < 3; ++a) coords[3 * i + a] = l.coords[i][a];
   return MG_OK;
 }
@@ -1217,8 +1252,8 @@ int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev) {
   return guard(h, [&] {
     Level& l = h->L[level];
     double* p = field == MG_FIELD_U ? l.u[l.cur] : field == MG_FIELD_F ? l.f : field == MG_FIELD_R ? l.r : l.uhat;
-    const size_t n = (size_t)l.nreal * l.B3 * sizeof(double);
-    if (dir == 0) CUDA_OK(cudaMemcpyAsync(dev, p, n, cudaMemcpyDeviceToDevice, h->s));
+    const size_t n = (size_t)(dir == 2 ? l.ntot() : l.nreal) * l.B3 * sizeof(double);
+    if (dir == 0 || dir == 2) CUDA_OK(cudaMemcpyAsync(dev, p, n, cudaMemcpyDeviceToDevice, h->s));
     else CUDA_OK(cudaMemcpyAsync(p, dev, n, cudaMemcpyDeviceToDevice, h->s));
     CUDA_OK(cudaStreamSynchronize(h->s));
   });

@@ -692,8 +692,13 @@ __global__ void k_prolong(LevelView F, LevelView C) {
       double vy[2];
       for (int ty = 0; ty < ny; ++ty) {
         double vx[2];
-        for (int tx = 0; tx < nx; ++tx)
-          vx[tx] = fetch(C.u, nb, C.B, cx + tx, cy + ty, cz + tz) - fetch(C.uhat, nb, C.B, cx + tx, cy + ty, cz + tz);
+        for (int tx = 0; tx < nx; ++tx) {
+          const int X = cx + tx, Y = cy + ty, Z = cz + tz;
+          const int slot = (region(X, C.B) + 1) + 3 * (region(Y, C.B) + 1) + 9 * (region(Z, C.B) + 1);
+          // ε := 0 outside the coarse level's blocks (reading Z13-W)
+          vx[tx] = ((C.nbr_real[p] >> slot) & 1u)
+                       ? fetch(C.u, nb, C.B, X, Y, Z) - fetch(C.uhat, nb, C.B, X, Y, Z) : 0.0;
+        }
         vy[ty] = nx == 2 ? 0.5 * (vx[0] + vx[1]) : vx[0];
       }
       vz[tz] = ny == 2 ? 0.5 * (vy[0] + vy[1]) : vy[0];
@@ -720,12 +725,14 @@ __global__ void __launch_bounds__(256) k_prolong2(LevelView F, LevelView C) {
   for (int k = 0; k < B3 / 256; ++k) uf[k] = F.u[(size_t)b * B3 + tid + k * 256];
   __syncthreads();
   const int CB = C.B;
+  const uint32_t creal = C.nbr_real[p];
   for (int i = tid; i < E * E * E; i += 256) {
     const int x = ox + i % E, y = oy + (i / E) % E, z = oz + i / (E * E);
     const int dx = region(x, CB), dy = region(y, CB), dz = region(z, CB);
-    const size_t g = (size_t)snb[(dx + 1) + 3 * (dy + 1) + 9 * (dz + 1)] * C.B3 +
-                     ((z - dz * CB) * CB + (y - dy * CB)) * CB + (x - dx * CB);
-    eps[i] = __ldg(C.u + g) - __ldg(C.uhat + g);
+    const int slot = (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1);
+    const size_t g = (size_t)snb[slot] * C.B3 + ((z - dz * CB) * CB + (y - dy * CB)) * CB + (x - dx * CB);
+    // ε := 0 at coarse nodes outside the level's blocks (jump / exterior ghosts, reading Z13-W)
+    eps[i] = ((creal >> slot) & 1u) ? __ldg(C.u + g) - __ldg(C.uhat + g) : 0.0;
   }
   __syncthreads();
 #pragma unroll

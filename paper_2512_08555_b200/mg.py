@@ -21,6 +21,7 @@ MG_FIELD_U, MG_FIELD_F, MG_FIELD_R, MG_FIELD_UHAT = 0, 1, 2, 3
 OPS = dict(refresh=0, smooth=1, residual=2, restrict=3, prolong=4, inject_up=5, coarse_solve=6,
            smooth_residual=7)
 MG_OK, MG_WARN_NOT_CONVERGED = 0, 1
+MG_ALL_BLOCKS = 0x10000
 
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
@@ -193,19 +194,23 @@ class Solver:
         keys = ["B", "nreal", "nghost", "Nx", "Ny", "Nz", "amr", "n_c2f", "n_inject", "n_leaf_blocks"]
         return dict(zip(keys, list(info)))
 
-    def level_blocks(self, m):
-        n = self.level_info(m)["nreal"]
+    def level_blocks(self, m, ghosts=False):
+        info = self.level_info(m)
+        n = info["nreal"] + (info["nghost"] if ghosts else 0)
         out = np.zeros((n, 3), dtype=np.int32)
-        self._check(self.lib.mg_level_blocks(self.h, int(m), out.ctypes.data_as(C.POINTER(C.c_int32))))
+        code = int(m) | (MG_ALL_BLOCKS if ghosts else 0)
+        self._check(self.lib.mg_level_blocks(self.h, code, out.ctypes.data_as(C.POINTER(C.c_int32))))
         return out
 
-    def debug_field(self, field, m, tensor=None):
-        """Export (tensor None) or import a level field [nreal, B, B, B]."""
+    def debug_field(self, field, m, tensor=None, ghosts=False):
+        """Export (tensor None) or import a level field [nreal, B, B, B]; with
+        ghosts=True export real then ghost blocks [nreal + nghost, B, B, B]."""
         t = self.torch
         info = self.level_info(m)
         if tensor is None:
-            out = t.empty((info["nreal"], info["B"], info["B"], info["B"]), dtype=t.float64, device="cuda")
-            self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 0, _ptr(out)))
+            n = info["nreal"] + (info["nghost"] if ghosts else 0)
+            out = t.empty((n, info["B"], info["B"], info["B"]), dtype=t.float64, device="cuda")
+            self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 2 if ghosts else 0, _ptr(out)))
             return out
         self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 1, _ptr(tensor)))
 

@@ -62,6 +62,8 @@ def _cfg(name):
         return _periodic_adaptive()
     elif name == "cfg4_small":
         c = C.cfg4(base=4, max_level=1, target=60)
+    elif name == "cfg3_64":
+        c = C.cfg3(64, coarse_n=16)
     else:
         raise KeyError(name)
     dom, lv, f = C.build(c)
@@ -87,7 +89,7 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 2)])
+                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
@@ -142,7 +144,7 @@ def _prepared(name, warm=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64"])
 def test_op_smooth(name):
     p = _prepared(name)
     for m in range(1, len(p.o.levels)):
@@ -154,7 +156,7 @@ def test_op_smooth(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
 def test_op_residual(name):
     p = _prepared(name)
     for m in range(0, len(p.o.levels)):
@@ -168,7 +170,7 @@ def test_op_residual(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
 def test_op_restrict(name):
     p = _prepared(name)
     for m in range(len(p.o.levels) - 1, 0, -1):
@@ -183,7 +185,7 @@ def test_op_restrict(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
 def test_op_prolong(name):
     p = _prepared(name)
     rng = np.random.default_rng(5)
@@ -199,7 +201,7 @@ def test_op_prolong(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64"])
 def test_op_coarse_solve(name):
     p = _prepared(name)
     c = p.o.levels[0]
@@ -225,3 +227,41 @@ def test_set_rhs_fstar_parity():
     for m, L in enumerate(p.o.levels):
         e = rel_err(p.gpu_field("f", m)[L.leaf], L.f[L.leaf]) if L.leaf.any() else 0.0
         assert e < OP_TOL, (m, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64"])
+def test_op_ghost_fill(name):
+    """Boundary-ghost fill (a1: f2c injection + c2f, exterior chain U1) of every level:
+    GPU ghost-block values vs the oracle's lookup V_m(J) at every halo node (within
+    2 nodes of the level's real blocks) — the nodes the stencil kernels read."""
+    from oracle.mg_oracle import E
+    p = _prepared(name)
+    for m in range(1, len(p.o.levels)):
+        L = p.o.levels[m]
+        if L.mask_ext.all():
+            continue
+        p.g.debug_apply("refresh", m)
+        vals = p.g.debug_field(0, m, ghosts=True).cpu().numpy()
+        coords = p.g.level_blocks(m, ghosts=True)
+        nreal = p.g.level_info(m)["nreal"]
+        ref = p.o.lookup(m, p.o.uvals())
+        # halo: extended-lattice positions within Chebyshev distance 2 of a real node
+        from scipy.ndimage import maximum_filter
+        halo = maximum_filter(L.mask_ext, size=5, mode="constant") & ~L.mask_ext
+        B = p.B[m]
+        worst, n = 0.0, 0
+        scale = np.abs(L.u[L.mask]).max()
+        for g in range(nreal, len(coords)):
+            c = coords[g]
+            for lz in range(B):
+                for ly in range(B):
+                    for lx in range(B):
+                        J = (c[0] * B + lx, c[1] * B + ly, c[2] * B + lz)
+                        X = tuple(J[a] + E for a in range(3))
+                        if not all(0 <= X[a] < halo.shape[a] for a in range(3)) or not halo[X]:
+                            continue
+                        n += 1
+                        worst = max(worst, abs(vals[g, lz, ly, lx] - ref[X]) / scale)
+        assert n > 0
+        assert worst < OP_TOL, (m, worst, n)

@@ -122,3 +122,26 @@ def test_adaptive_periodic_singular_stall_and_cauchy():
     o.set_rhs(f)
     cyc, hist = o.solve(1e-9, max_cycles=25, criterion="cauchy")
     assert hist[-1] < 1e-9
+
+
+def test_cfg3_reduced_free_space_fourth_order():
+    """Config 3 recipe (UUU, Gaussian σ=0.08, reading U1) at 32^3 and 64^3: the
+    V-cycle converges and the origin value approaches the free-space closed form
+    -Q erf(r/(√2σ))/(4πr) -> -√(2/π)/(4πσ) at 4th order (P10, E12 design order)."""
+    errs = []
+    for N, cn in ((32, 8), (64, 16)):
+        cfg = C.cfg3(N, coarse_n=cn)
+        dom, lv, f = C.build(cfg)
+        o = MO.Oracle(cfg, lv)
+        o.set_rhs(f)
+        hist = []
+        for _ in range(14):
+            o.vcycle(1)
+            hist.append(o.residual_norm()[1])
+        assert hist[-1] < 1e-8 * (N / 32) and hist[-1] < hist[0] * 1e-6
+        u = o.get_solution()
+        c = N // 32
+        n = int(np.nonzero((lv == np.array([0, c, c, c])).all(axis=1))[0][0])
+        errs.append(abs(u[n, 0, 0, 0] + math.sqrt(2 / math.pi) / (4 * math.pi * 0.08)))
+    order = math.log2(errs[0] / errs[1])
+    assert 3.4 < order < 4.8, (errs, order)

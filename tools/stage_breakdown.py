@@ -1,0 +1,51 @@
+#!/usr/bin/env python
+"""Per-level, per-stage CUDA-event breakdown of a V-cycle (non-graph launches).
+
+  python tools/stage_breakdown.py [--cfg cfg2] [--cycles 5]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="cfg2")
+    ap.add_argument("--cycles", type=int, default=5)
+    a = ap.parse_args()
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    from workloads import configs as C
+    cfg = getattr(C, a.cfg)()
+    dom, leaves, f = C.build(cfg)
+    S = Solver(cfg, leaves)
+    S.set_rhs(torch.from_numpy(f).cuda())
+    S.vcycle(2)
+    S.use_graph(False)
+    S.profile(True)
+    S.vcycle(a.cycles)
+    prof = S.profile_read()
+    S.profile(False)
+    nlev = S.num_levels()
+    rows = {}
+    for st, (ms, cnt) in prof.items():
+        for m in range(nlev):
+            if cnt[m]:
+                rows.setdefault(st, {})[m] = (round(ms[m] / a.cycles * 1e3, 1), round(cnt[m] / a.cycles, 2))
+    info = [S.level_info(m) for m in range(nlev)]
+    print(json.dumps({"cfg": a.cfg, "blocks": [i["nreal"] for i in info], "ghosts": [i["nghost"] for i in info],
+                      "us_per_cycle[stage][level]=(us, launches)": rows}), flush=True)
+    S.use_graph(True)
+    ms = S.time_op("vcycle", 0, 10)
+    print(json.dumps({"cfg": a.cfg, "graph_ms_per_vcycle": ms}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
