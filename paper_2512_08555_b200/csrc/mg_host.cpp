@@ -625,10 +625,14 @@ void build_ghost_boxes(mg_handle* h) {
 // `lmax` blocks, longest first.  The z-marching kernels (mg_pencil.cu) walk one
 // pencil per CTA; halos above/below a pencil come through the neighbour tables.
 void build_pencils(mg_handle* h) {
-  int lmax = 2;  // cfg2 256^3 on B200: 2 blocks per pencil beats 4 (more CTAs, shorter tail)
-  if (const char* e = std::getenv("MG_PENCIL")) lmax = std::max(1, std::min(16, std::atoi(e)));
+  // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs.
+  // A level with fewer blocks than ~2 resident waves (148 SMs x 4 CTAs) uses 1-block
+  // pencils; larger levels 2 (cfg2 256^3 on B200: 2 beats 4 — shorter tail).
+  int lmax_env = 0;
+  if (const char* e = std::getenv("MG_PENCIL")) lmax_env = std::max(1, std::min(16, std::atoi(e)));
   const bool off = std::getenv("MG_NO_PENCIL") != nullptr;
   for (auto& l : h->L) {
+    const int lmax = lmax_env ? lmax_env : (l.nreal >= 2 * 148 * 4 ? 2 : 1);
     l.pen_blk.clear();
     l.pen_len.clear();
     l.pen_lmax = lmax;
@@ -839,9 +843,26 @@ void sweep(mg_handle* h, int m, bool with_res) {
   }
 }
 
+// Restriction of level m into m-1 (Alg. 1) starting from refreshed level-m
+// ghosts: residual + u injection + full weighting (fused in one pencil kernel on B = 16
+// levels; else residual kernel + restriction kernel), then the level-(m-1) refresh,
+// FAS right-hand side and the û snapshot.
+// The fused kernel (mg_pencil.cu) is correct but, at 2 CTAs/SM, slower on cfg2 256^3
+// (190 us) than the residual pencil + restriction kernels (90 + 62 us): opt-in only.
+bool fused_res_restrict(mg_handle* h, int m) { return std::getenv("MG_FUSED_RR") != nullptr && h->L[m].B == 16; }
+
 void restrict_level(mg_handle* h, int m) {
   Level& C = h->L[m - 1];
-  {
+  bool done = false;
+  if (fused_res_restrict(h, m)) {
+    Prof pr(h, ST_RESTRICT, m);
+    done = launch_res_restrict_pencil(view(h, m), view(h, m - 1), h->order, h->s);
+  }
+  if (!done) {
+    {
+      Prof pr(h, ST_RESIDUAL, m);
+      residual_kernel(h, m);
+    }
     Prof pr(h, ST_RESTRICT, m);
     launch_restrict(view(h, m), view(h, m - 1), h->s);
   }
@@ -873,12 +894,8 @@ void inject_up_all(mg_handle* h) {
 void vcycle_body(mg_handle* h) {
   const int top = (int)h->L.size() - 1;
   for (int m = top; m >= 1; --m) {
-    for (int k = 1; k <= h->eta1; ++k) sweep(h, m, k == h->eta1);
-    if (h->eta1 == 0) {
-      refresh(h, m);
-      Prof pr(h, ST_RESIDUAL, m);
-      residual_kernel(h, m);
-    }
+    for (int k = 1; k <= h->eta1; ++k) sweep(h, m, false);
+    refresh(h, m);
     restrict_level(h, m);
   }
   coarse_solve(h);
@@ -1273,7 +1290,6 @@ static void apply_op(mg_handle* h, int op, int level) {
     case MG_OP_RESTRICT:
       if (level < 1) throw MgError(MG_ERR_ARG, "restrict needs level >= 1");
       refresh(h, level);
-      residual_kernel(h, level);
       restrict_level(h, level);
       break;
     case MG_OP_PROLONG:

@@ -58,6 +58,8 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s);
 // z-marching pencil kernels (B = 16 levels); return false if the level is not eligible
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s);
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
+// fused fine residual + full-weighting restriction + u injection into the coarse level
+bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
 void prepare_pencil_kernels();
 void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
                 const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
