@@ -89,6 +89,7 @@ struct Level {
   bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
   // host tables
   std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len, gbox;
+  std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
   std::vector<uint32_t> nbr_real;
   std::vector<uint8_t> covmask, c2f_ext;
@@ -99,7 +100,7 @@ struct Level {
   int cur = 0;
   int32_t *d_nbr = nullptr, *d_parent = nullptr, *d_bmap = nullptr, *d_c2f_dst = nullptr, *d_c2f_J = nullptr,
           *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr,
-          *d_gbox = nullptr;
+          *d_gbox = nullptr, *d_sw_blk = nullptr, *d_sw_len = nullptr, *d_sw_z = nullptr;
   uint32_t* d_nbr_real = nullptr;
   uint8_t *d_covmask = nullptr, *d_c2f_ext = nullptr;
 
@@ -230,6 +231,11 @@ LevelView view(mg_handle* h, int m) {
   v.pen_lmax = l.pen_lmax;
   v.pen_blk = l.d_pen_blk;
   v.pen_len = l.d_pen_len;
+  v.sw_npen = (int)l.sw_len.size();
+  v.sw_pen_lmax = 1;
+  v.sw_pen_blk = l.d_sw_blk;
+  v.sw_pen_len = l.d_sw_len;
+  v.sw_pen_z = l.d_sw_z;
   return v;
 }
 
@@ -673,6 +679,20 @@ void build_pencils(mg_handle* h) {
       l.pen_len.push_back((int32_t)p.size());
       for (int t = 0; t < lmax; ++t) l.pen_blk.push_back(t < (int)p.size() ? p[t] : -1);
     }
+    // sweep pencils: a level with fewer blocks than SMs splits every block into 2
+    // z-parts of 8 planes (twice the CTAs, 12 steps each; cfg2 64^3 level: 58 -> 50 us
+    // per 4 sweeps; at 512 blocks the split is slower)
+    l.sw_blk.clear();
+    l.sw_len.clear();
+    l.sw_z.clear();
+    if (lmax == 1 && l.nreal < 148 && std::getenv("MG_NO_ZSPLIT") == nullptr) {
+      for (int32_t b : l.pen_blk)
+        for (int z0 = 0; z0 < 16; z0 += 8) {
+          l.sw_blk.push_back(b);
+          l.sw_len.push_back(1);
+          l.sw_z.push_back(z0 | (8 << 8));
+        }
+    }
   }
 }
 
@@ -696,6 +716,9 @@ void alloc_device(mg_handle* h) {
     l.d_pen_blk = dev_upload(l.pen_blk);
     l.d_pen_len = dev_upload(l.pen_len);
     l.d_gbox = dev_upload(l.gbox);
+    l.d_sw_blk = dev_upload(l.sw_blk);
+    l.d_sw_len = dev_upload(l.sw_len);
+    l.d_sw_z = dev_upload(l.sw_z);
   }
   // leaf map: leaf n -> (level, block)
   std::vector<int64_t> map(h->leaves.size());
@@ -868,7 +891,7 @@ void restrict_level(mg_handle* h, int m) {
   }
   refresh(h, m - 1);
   Prof pr(h, ST_RESTRICT, m);
-  launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
+  if (!launch_fas_pencil(view(h, m - 1), h->order, h->s)) launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
   CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
 }
 
@@ -1046,7 +1069,7 @@ void destroy(mg_handle* h) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
                     (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
                     (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src, (void*)l.d_pen_blk,
-                    (void*)l.d_pen_len, (void*)l.d_gbox})
+                    (void*)l.d_pen_len, (void*)l.d_gbox, (void*)l.d_sw_blk, (void*)l.d_sw_len, (void*)l.d_sw_z})
       if (p) cudaFree(p);
   }
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,

@@ -33,6 +33,12 @@ struct LevelView {
   int npen, pen_lmax;
   const int32_t* pen_blk;   // [npen][pen_lmax] real block indices, bottom to top (-1 padded)
   const int32_t* pen_len;   // [npen]
+  // sweep pencils (k_rb_pencil only): like the above, plus (z0 | nplanes << 8) so that
+  // small levels can split a block into several z-parts for more CTAs; sw_npen = 0: use pen_*
+  int sw_npen, sw_pen_lmax;
+  const int32_t* sw_pen_blk;
+  const int32_t* sw_pen_len;
+  const int32_t* sw_pen_z;
 };
 
 struct C2FList {           // boundary-ghost entries of one level
@@ -58,6 +64,8 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s);
 // z-marching pencil kernels (B = 16 levels); return false if the level is not eligible
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s);
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
+// FAS right-hand side f = r + Δu on the covered nodes of a coarse level (B = 16)
+bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s);
 // fused fine residual + full-weighting restriction + u injection into the coarse level
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
 void prepare_pencil_kernels();

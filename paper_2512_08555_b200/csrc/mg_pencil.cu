@@ -91,7 +91,7 @@ struct RBShape {
   static constexpr int SNW = 13, SNP = 18 * SNW;
   // [R][TP] old u | [2][SNP] red-phase values | [R][NT] f pairs
   static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + 2 * SNP + R * NT * 2);
-  static_assert((R & (R - 1)) == 0 && D + 2 <= R, "ring too small for the prefetch depth");
+  static_assert(D + 2 <= R, "ring too small for the prefetch depth");
 };
 
 struct RBCtx {
@@ -100,21 +100,25 @@ struct RBCtx {
   double* su;
   double* sn;
   double2* sf;
-  int len, nz;
+  int len, nz;       // pencil blocks, interior planes of this pencil (16 len, or a part of one block)
+  int z0, nzb;       // first interior plane relative to the first block, 16 len
+  const int* glen;   // shared copy of len
   int ld_xy[2], ld_sxy[2], ld_dst[2];
 };
 
 __device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-template <int ORDER, int D, int RR, int RP>
+template <int ORDER, int D, int RR, int RP, bool SW>
 __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int wg, int lane, double omega,
                                         double inv_h2, double inv_d) {
   using S = RBShape<D, RR>;
   constexpr int TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NLD = S::NLD, SNW = S::SNW, SNP = S::SNP;
   constexpr int PC = RP;  // column (0 = a = x0, 1 = b = x0+1) that is red at even planes
   const int* snb = cx.snb;
-  const int len = cx.len, nz = cx.nz;
+  // planes are indexed relative to the pencil's first block: interior [zlo, zhi);
+  // zlo ∈ {0, 8} keeps zlo ≡ 0 (mod 4), which the unrolled step loop relies on
+  const int zlo = SW ? cx.z0 : 0, zhi = SW ? cx.z0 + cx.nz : PB * cx.len;
   double* su = cx.su;
   double* sn = cx.sn;
   const int tid = threadIdx.x;
@@ -134,10 +138,11 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   // and at the pencil ends; between them they advance by one plane (PB^2 doubles).
   const double* ip[NLD];
   const double* fp = nullptr;
-  int zi = -2;
+  int zi = zlo - 2;
   auto seek_issue = [&](int z) {
     int k, dz, zl;
-    plane_src(z, nz, len, k, dz, zl);
+    const int len = *cx.glen;  // pencil geometry from shared memory (rare path: spare registers)
+    plane_src(z, PB * len, len, k, dz, zl);
     const int o = zl * (PB * PB);
 #pragma unroll
     for (int d = 0; d < NLD; ++d)
@@ -146,9 +151,9 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
     fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
   };
   auto issue = [&]() {
-    if (zi < nz + 2) {
+    if (zi < zhi + 2) {
       if ((zi & 15) == 0) seek_issue(zi);
-      const int slot = (zi + 2) & (R - 1);
+      const int slot = (zi + 2) % R;  // zi >= -2
       double* dst = su + slot * TP;
 #pragma unroll
       for (int d = 0; d < NLD; ++d) {
@@ -156,7 +161,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
         cpa16(dst + cx.ld_dst[d], ip[d]);
         ip[d] += PB * PB;
       }
-      if (valid && zi >= -1 && zi <= nz) cpa16(sfme + slot * NT, fp);
+      if (valid && zi >= zlo - 1 && zi <= zhi) cpa16(sfme + slot * NT, fp);
       fp += PB * PB;
     }
     cpa_commit();
@@ -165,11 +170,12 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   bool live = false;  // red-phase liveness of this pair's columns at plane r
   auto seek_live = [&](int z) {
     int k, dz, zl;
-    plane_src(z, nz, len, k, dz, zl);
+    const int len = *cx.glen;
+    plane_src(z, PB * len, len, k, dz, zl);
     live = valid && ((cx.sreal[k] >> (sxy + 9 * (dz + 1))) & 1u);
   };
-  seek_issue(-2);
-  seek_live(-1);
+  seek_issue(zlo - 2);
+  seek_live(zlo - 1);
 #pragma unroll
   for (int q = 0; q < D; ++q) issue();
 
@@ -188,7 +194,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   double2 fr = make_double2(0.0, 0.0);  // f pair at the plane of the last red phase
   double fb = 0.0;                      // f of the column black at plane s-2
 
-  for (int s0 = -2; s0 < nz + 2; s0 += 4) {
+  for (int s0 = zlo - 2; s0 < zhi + 2; s0 += 4) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int s = s0 + j;
@@ -199,7 +205,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       issue();
       double cq[2], s4q[2], d4q[2];
       {
-        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+        const double* U = su + ((s + 2) % R) * TP + i0;
         const double2 m = *reinterpret_cast<const double2*>(U - TW);
         const double2 cc = *reinterpret_cast<const double2*>(U);
         const double2 p = *reinterpret_cast<const double2*>(U + TW);
@@ -220,10 +226,10 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       const double nx = X ? shfl_dn1(nl[0]) : shfl_up1(nl[1]);
       // column X: black at plane s
       const double alpha = ORDER == 4 ? 2.0 * cq[X] + s4q[X] : cq[X];
-      if (s >= 0) {  // red half-sweep at plane r = s-1 in [-1, nz] (column X)
+      if (s >= zlo) {  // red half-sweep at plane r = s-1 in [zlo-1, zhi] (column X)
         if (((s - 1) & 15) == 0) seek_live(s - 1);
         fb = X ? fr.y : fr.x;                 // f at plane s-2 of column X (pair read last step)
-        fr = sfme[((s + 1) & (R - 1)) * NT];  // f pair at plane s-1
+        fr = sfme[((s + 1) % R) * NT];  // f pair at plane s-1
         double v = cR[X];
         if (live) {
           const double Lu = ORDER == 4 ? (accR[X] + alpha) * h6 : (accR[X] + alpha) * inv_h2;
@@ -231,7 +237,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
         }
         if (valid) snme[(j & 1) * SNP] = v;  // new-plane slot = parity of s
         const double g = ORDER == 4 ? 2.0 * v + s4r[X] : v;  // γ(s-1) of column X
-        if (s >= 2 && inner) {  // black half-sweep at plane b = s-2 (column X)
+        if (s >= zlo + 2 && inner) {  // black half-sweep at plane b = s-2 (column X)
           const double* N = snme + ((j & 1) ^ 1) * SNP;  // rows cy±1 hold the red node at x of X
           const double S4n = (nl[O] + nx) + (N[-SNW] + N[SNW]);
           const double Lu = ORDER == 4 ? (accB[X] + 2.0 * S4n + g) * h6 : (accB[X] + S4n + g) * inv_h2;
@@ -253,7 +259,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   cpa_wait<0>();
 }
 
-template <int ORDER, int D, int RR, int NREG>
+template <int ORDER, int D, int RR, int NREG, bool SW>
 __global__ void __maxnreg__(NREG)
     k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
   using S = RBShape<D, RR>;
@@ -261,16 +267,30 @@ __global__ void __maxnreg__(NREG)
   extern __shared__ __align__(16) double sm[];
   __shared__ int snb[PMAXL * 27];
   __shared__ uint32_t sreal[PMAXL];
+  __shared__ int slen;
   const int tid = threadIdx.x;
   RBCtx cx;
-  cx.len = __ldg(L.pen_len + blockIdx.x);
-  cx.nz = PB * cx.len;
+  // sweep pencils (sw_*: may split a block into z-parts on small levels) or block pencils
+  const bool sw = SW;
+  cx.len = __ldg((sw ? L.sw_pen_len : L.pen_len) + blockIdx.x);
+  cx.nzb = PB * cx.len;
+  if (sw) {
+    const int zr = __ldg(L.sw_pen_z + blockIdx.x);
+    cx.z0 = zr & 0xff;
+    cx.nz = zr >> 8;
+  } else {
+    cx.z0 = 0;
+    cx.nz = cx.nzb;
+  }
   cx.snb = snb;
   cx.sreal = sreal;
+  cx.glen = &slen;
+  if (tid == 0) slen = cx.len;
   cx.su = sm;
   cx.sn = sm + R * TP;
   cx.sf = reinterpret_cast<double2*>(sm + R * TP + 2 * S::SNP);
-  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  const int32_t* pb = sw ? L.sw_pen_blk + (size_t)blockIdx.x * L.sw_pen_lmax
+                         : L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
   for (int i = tid; i < cx.len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
   if (tid < cx.len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
 #pragma unroll
@@ -285,8 +305,8 @@ __global__ void __maxnreg__(NREG)
   __syncthreads();  // snb / sreal
   // warp-uniform row parity: warps 0-2 even rows, 3-5 odd rows
   const int w = tid >> 5, lane = tid & 31;
-  if (w < 3) rb_body<ORDER, D, RR, 0>(L, cx, w, lane, omega, inv_h2, inv_d);
-  else rb_body<ORDER, D, RR, 1>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
+  if (w < 3) rb_body<ORDER, D, RR, 0, SW>(L, cx, w, lane, omega, inv_h2, inv_d);
+  else rb_body<ORDER, D, RR, 1, SW>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
 }
 
 // ---------------------------------------------------------------------------------
@@ -304,7 +324,10 @@ struct ResShape {
   static constexpr size_t SMEM = sizeof(double) * (size_t)(R * (TP + FP));
 };
 
-template <int ORDER, int D>
+// MODE 0: r = f - Δ_h^M u (residual, Alg. 1) on every node of the pencil.
+// MODE 1: f = r + Δ_h^M u (FAS right-hand side on the coarse level, Alg. 1) on
+//         the nodes of octants covered by the finer level (covmask); others untouched.
+template <int ORDER, int D, int MODE = 0>
 __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, double inv_h2) {
   using S = ResShape<D>;
   constexpr int T = S::T, TP = S::TP, FP = S::FP, R = S::R, NT = S::NT;
@@ -316,7 +339,10 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
   const int len = __ldg(L.pen_len + blockIdx.x);
   const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
   for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  __shared__ uint8_t scov[PMAXL];
+  if (MODE == 1 && tid < len) scov[tid] = __ldg(L.covmask + __ldg(pb + tid));
   const int nz = PB * len;
+  const double* __restrict__ fin = MODE == 0 ? L.f : L.r;  // the right-hand operand staged per plane
 
   int ld_xy[2], ld_sxy[2], ld_dst[2];
   bool ld_on[2], ld_f[2];
@@ -349,7 +375,7 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
       for (int d = 0; d < 2; ++d) {
         if (!ld_on[d] || (ld_f[d] && dz != 0)) continue;
         const int blk = snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)];
-        const double* src = (ld_f[d] ? L.f : L.u) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
+        const double* src = (ld_f[d] ? fin : L.u) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
         cpa16(sm + ld_dst[d] + slot * (ld_f[d] ? FP : TP), src);
       }
     }
@@ -388,7 +414,13 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
         const double E = Dg + (a2 + a0);
         Lu = (2.0 * F + E - 24.0 * c1) * h6;
       }
-      L.r[(size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid] = f - Lu;
+      const size_t o = (size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid;
+      if (MODE == 0) {
+        L.r[o] = f - Lu;
+      } else {
+        const int oct = (cx >= PB / 2) | ((cy >= PB / 2) << 1) | (((r & 15) >= PB / 2) << 2);
+        if ((scov[r >> 4] >> oct) & 1) L.f[o] = f + Lu;
+      }
     }
   }
   cpa_wait<0>();
@@ -559,16 +591,20 @@ constexpr int RES_D = 3;
 struct RBVar {
   void (*k2)(LevelView, double, double, double);
   void (*k4)(LevelView, double, double, double);
+  void (*k2s)(LevelView, double, double, double);  // sweep pencils with z-parts
+  void (*k4s)(LevelView, double, double, double);
   size_t smem;
 };
 template <int D, int RR, int NREG>
 static RBVar rb_var() {
-  return {k_rb_pencil<2, D, RR, NREG>, k_rb_pencil<4, D, RR, NREG>, RBShape<D, RR>::SMEM};
+  return {k_rb_pencil<2, D, RR, NREG, false>, k_rb_pencil<4, D, RR, NREG, false>,
+          k_rb_pencil<2, D, RR, NREG, true>, k_rb_pencil<4, D, RR, NREG, true>, RBShape<D, RR>::SMEM};
 }
 static const RBVar& rb_pick() {
   // cfg2 256^3 finest sweep on B200 (tools/time_ops.py): <2,4,80> 108.7 us (4 CTAs/SM),
   // <2,4,96> 116.5, <5,8,96> 120.9, <2,4,72> 124.6 (spills), <3,8,80> 129.4 (smem: 3 CTAs/SM)
-  static RBVar vars[] = {rb_var<2, 4, 80>(), rb_var<2, 4, 96>(), rb_var<5, 8, 96>(), rb_var<3, 8, 80>()};
+  // <3,5,80> 115.3, <4,6,80> 112.9, <3,6,80> 116.7 us (deeper rings do not help)
+  static RBVar vars[] = {rb_var<2, 4, 80>(), rb_var<2, 4, 96>(), rb_var<5, 8, 96>()};
   static int sel = [] {
     const char* e = std::getenv("MG_RB_VAR");
     const int v = e ? std::atoi(e) : 0;
@@ -586,8 +622,12 @@ void prepare_pencil_kernels() {
   const RBVar& v = rb_pick();
   setup((const void*)v.k2, v.smem);
   setup((const void*)v.k4, v.smem);
+  setup((const void*)v.k2s, v.smem);
+  setup((const void*)v.k4s, v.smem);
   setup((const void*)k_res_restrict_pencil<2>, RRShape::SMEM);
   setup((const void*)k_res_restrict_pencil<4>, RRShape::SMEM);
+  setup((const void*)k_res_pencil<2, RES_D, 1>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D>, ResShape<RES_D>::SMEM);
 }
@@ -597,7 +637,18 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
   const RBVar& v = rb_pick();
-  (order == 2 ? v.k2 : v.k4)<<<L.npen, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
+  const int grid = L.sw_npen > 0 ? L.sw_npen : L.npen;
+  if (L.sw_npen > 0) (order == 2 ? v.k2s : v.k4s)<<<grid, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
+  else (order == 2 ? v.k2 : v.k4)<<<grid, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
+  note_launch();
+  return true;
+}
+
+bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s) {
+  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  if (order == 2) k_res_pencil<2, RES_D, 1><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
+  else k_res_pencil<4, RES_D, 1><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
   note_launch();
   return true;
 }
