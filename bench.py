@@ -89,6 +89,29 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def max_over_ranks(x, dist, device):
+    """Max of a per-rank float over all ranks (device timing rule: the slowest rank)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    `ncu --set full` capture summary (profiles/ncu_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+    except Exception:
+        return None
+    for k, v in d.get("kernels", {}).items():
+        if k.startswith(kernel_prefix):
+            return v.get("dram_bytes_per_launch")
+    return None
+
+
 def dist_setup(args):
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -128,7 +151,7 @@ def run_reference(args, ws, rank, dist):
     if rank != 0:
         return
     from oracle.mg_oracle import Oracle
-    cfg, leaves, f = build_workload(128)
+    cfg, leaves, f = build_workload(args.ref_n)
     o = Oracle(cfg, leaves)
     o.set_rhs(f)
     for _ in range(args.warmup):
@@ -143,9 +166,9 @@ def run_reference(args, ws, rank, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "cfg2 recipe (periodic, M=4 Mehrstellen, RB V(2,2), 64 seeded Fourier modes) "
-                                   "at 128^3 as a bounded CPU sample of the 256^3 workload", "leaf_unknowns": n},
+                                   f"at {args.ref_n}^3 as a bounded CPU sample of the 256^3 workload", "leaf_unknowns": n},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": "1 oracle V-cycle of the cfg2 recipe at 128^3 per step"},
+                             "sample": f"1 oracle V-cycle of the cfg2 recipe at {args.ref_n}^3 per step"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -191,11 +214,7 @@ def run_mine(args, ws, rank, local, dist):
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    ms = e0.elapsed_time(e1) / args.steps
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, dev)
     clocks = clk.summary()
     value = nleaf_unknowns * ws / (ms * 1e-3)
 
@@ -253,14 +272,16 @@ def run_mine(args, ws, rank, local, dist):
     ke = max(1, min(args.steps, 5))
     if dist:
         dist.barrier()
-    t0 = time.perf_counter()
+    torch.cuda.synchronize()
+    # CUDA events on the stream the library enqueues on (the legacy default stream):
+    # mg_run_host enqueues H2D, set_rhs, the cycles and D2H there and synchronises
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
     for _ in range(ke):
         rel_e2e = S.run_host(fh, uh, ncyc)
-    te = (time.perf_counter() - t0) / ke
-    if dist:
-        t = torch.tensor([te], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        te = float(t.item())
+    h1.record(stream)
+    torch.cuda.synchronize()
+    te = max_over_ranks(h0.elapsed_time(h1) / ke * 1e-3, dist, dev)
     e2e = {"value": nleaf_unknowns * ncyc * ws / te, "unit": UNIT, "h2d_bytes_per_step": int(f.nbytes),
            "d2h_bytes_per_step": int(f.nbytes + 8), "cycles_per_step": ncyc, "rel_residual": rel_e2e,
            "ms_per_step": te * 1e3, "what": "mg_run_host: pinned f -> device, set_rhs (f*), V-cycles to rel. "
@@ -275,7 +296,10 @@ def run_mine(args, ws, rank, local, dist):
                        "l2": "inputs larger than L2 (u,u',f,r at 256^3 = 537 MB working set)",
                        "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": ncu_traffic("k_rb_pencil") if st == "smooth" else None,
+                         "traffic_source": "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read+write "
+                                           "per launch of the finest-level sweep)",
+                         "peak_source": peak_src,
                          "kernel": f"{st} (level {lv}, {Nl} unknowns/launch)",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms,
                          "frac_of_8TBps": achieved / NORTH_STAR_PEAK_GBS},
@@ -303,6 +327,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-n", type=int, default=128, help="grid of the oracle's bounded sample (--impl reference)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
