@@ -818,6 +818,9 @@ void swap_u(Level& l) { l.cur = 1 - l.cur; }
 void refresh(mg_handle* h, int m) {
   if (m <= 0) return;
   const int lo = h->L[m].ext_chain ? 1 : m;
+  bool any = false;
+  for (int j = lo; j <= m; ++j) any = any || !h->L[j].inj_dst.empty() || !h->L[j].gbox.empty();
+  if (!any) return;  // ghost-free level (no events either: keeps the stage profile honest)
   Prof pr(h, ST_GHOST, m);
   for (int j = m; j >= lo; --j) {
     Level &F = h->L[j], &C = h->L[j - 1];

@@ -23,13 +23,17 @@ def main():
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--coarse", type=int, default=0)
     a = ap.parse_args()
     import torch
 
     from paper_2512_08555_b200 import Solver
     from paper_2512_08555_b200.mg import OPS
     from workloads import configs as C
-    cfg = getattr(C, a.cfg)(a.n) if a.cfg in ("cfg2", "cfg3") else getattr(C, a.cfg)()
+    if a.cfg == "cfg2":
+        cfg = C.cfg2(a.n, coarse_n=a.coarse or None)
+    else:
+        cfg = getattr(C, a.cfg)(a.n) if a.cfg == "cfg3" else getattr(C, a.cfg)()
     dom, leaves, f = C.build(cfg)
     S = Solver(cfg, leaves)
     S.set_rhs(torch.from_numpy(f).cuda())
@@ -48,6 +52,11 @@ def main():
     ms = S.time_op(100, 0, a.reps)
     out["vcycle_ms"] = round(ms, 4)
     out["vcycle_unknowns_per_s"] = f.size / (ms * 1e-3)
+    S.use_graph(True)
+    S.set_rhs(torch.from_numpy(f).cuda())
+    cyc, rel, ok = S.solve(cfg["tol"], 30)
+    out["cycles_to_tol"] = cyc
+    out["levels"] = S.num_levels()
     print(json.dumps(out), flush=True)
 
 
