@@ -293,10 +293,21 @@ __global__ void __maxnreg__(NREG)
                          : L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
   for (int i = tid; i < cx.len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
   if (tid < cx.len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
+  // load items: 0-159 = the 16-wide interior part of the 20 tile rows, 8 lanes per row
+  // (each group of 8 lanes fetches one aligned 128-byte line); 160-199 = the 16-byte
+  // halo pieces x in [-2, 0) and [16, 18) of every row
 #pragma unroll
   for (int d = 0; d < NLD; ++d) {
     const int j = tid + d * NT;
-    const int py = j / (T / 2), px = 2 * (j % (T / 2));
+    int py, px;
+    if (j < 8 * T) {
+      py = j / 8;
+      px = 2 + 2 * (j % 8);
+    } else {
+      const int hh = j - 8 * T;
+      py = hh / 2;
+      px = (hh & 1) ? PB + 2 : 0;
+    }
     const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
     cx.ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
     cx.ld_sxy[d] = j < NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
