@@ -50,7 +50,9 @@ __device__ __forceinline__ void taps(int J, int c0, int& first, int& n, double* 
 }  // namespace
 
 // box record (12 int32): dst block, lo[3], hi[3] (fine block-local, hi exclusive),
-// org[3] = level-global fine index of the block's node (0,0,0), 2 unused
+// org[3] = level-global fine index of the block's node (0,0,0), 2 unused.
+// Threads form a 16 x 16 (x, y) tile and loop over the third axis, so that every
+// index is an add, not a division by a runtime extent.
 template <int I>
 __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ boxes, LevelView F, LevelView C,
                                                    double* __restrict__ ff, const double* __restrict__ cf,
@@ -71,79 +73,81 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   double* Cs = sm;                   // [nc2][nc1][nc0]
   double* T1 = sm + GB_SZ_A;         // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
-  const int tid = threadIdx.x;
-  // ---- stage the coarse support (periodic wrap; nodes outside the coarse level -> 0,
-  // only reached by non-needed nodes of the box)
-  const int ncc = nc[0] * nc[1] * nc[2];
-  for (int i = tid; i < ncc; i += GB_NT) {
-    int q[3] = {i % nc[0], (i / nc[0]) % nc[1], i / (nc[0] * nc[1])};
-    double v = 0.0;
-    bool ok = true;
-    int cb[3], cl[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      int ci = c0[a] + q[a];
-      if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
-      const int b = ci >= 0 ? ci / C.B : -((-ci + C.B - 1) / C.B);
-      cl[a] = ci - b * C.B;
-      cb[a] = b - C.bmap_lo[a];
-      ok = ok && cb[a] >= 0 && cb[a] < C.bmap_n[a];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // coarse block / local index along one axis (periodic wrap); -1 outside the block map
+  auto cidx = [&](int a, int ci, int& b, int& l) {
+    if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
+    const int bb = ci >= 0 ? ci / C.B : -((-ci + C.B - 1) / C.B);
+    l = ci - bb * C.B;
+    b = bb - C.bmap_lo[a];
+    if (b < 0 || b >= C.bmap_n[a]) b = -1;
+  };
+  // ---- stage the coarse support (nodes outside the coarse level -> 0, only reached
+  // by non-needed nodes of the box)
+  if (tx < nc[0] && ty < nc[1]) {
+    int bxx, lx, byy, ly;
+    cidx(0, c0[0] + tx, bxx, lx);
+    cidx(1, c0[1] + ty, byy, ly);
+    for (int cz = 0; cz < nc[2]; ++cz) {
+      int bzz, lz;
+      cidx(2, c0[2] + cz, bzz, lz);
+      double v = 0.0;
+      if (bxx >= 0 && byy >= 0 && bzz >= 0) {
+        const int cblk = __ldg(C.bmap + ((size_t)bzz * C.bmap_n[1] + byy) * C.bmap_n[0] + bxx);
+        if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (lz * C.B + ly) * C.B + lx];
+      }
+      Cs[(cz * nc[1] + ty) * nc[0] + tx] = v;
     }
-    if (ok) {
-      const int cblk = __ldg(C.bmap + ((size_t)cb[2] * C.bmap_n[1] + cb[1]) * C.bmap_n[0] + cb[0]);
-      if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (cl[2] * C.B + cl[1]) * C.B + cl[0]];
-    }
-    Cs[i] = v;
   }
   __syncthreads();
   // ---- pass x: T1[cz][cy][fx]
-  const int n1 = nf[0] * nc[1] * nc[2];
-  for (int i = tid; i < n1; i += GB_NT) {
-    const int fx = i % nf[0], cyz = i / nf[0];
+  if (tx < nf[0] && ty < nc[1]) {
     double w[I];
     int first, n;
-    taps<I>(g0[0] + fx, c0[0], first, n, w);
-    const double* row = Cs + cyz * nc[0] + first;
-    double sx = 0.0;
-    for (int t = 0; t < n; ++t) sx += w[t] * row[t];
-    T1[i] = sx;
+    taps<I>(g0[0] + tx, c0[0], first, n, w);
+    for (int cz = 0; cz < nc[2]; ++cz) {
+      const double* row = Cs + (cz * nc[1] + ty) * nc[0] + first;
+      double sx = 0.0;
+      for (int t = 0; t < n; ++t) sx += w[t] * row[t];
+      T1[(cz * nc[1] + ty) * nf[0] + tx] = sx;
+    }
   }
   __syncthreads();
   // ---- pass y: T2[cz][fy][fx]
-  const int n2 = nf[0] * nf[1] * nc[2];
-  for (int i = tid; i < n2; i += GB_NT) {
-    const int fx = i % nf[0], fy = (i / nf[0]) % nf[1], cz = i / (nf[0] * nf[1]);
+  if (tx < nf[0] && ty < nf[1]) {
     double w[I];
     int first, n;
-    taps<I>(g0[1] + fy, c0[1], first, n, w);
-    const double* col = T1 + (cz * nc[1] + first) * nf[0] + fx;
-    double sy = 0.0;
-    for (int t = 0; t < n; ++t) sy += w[t] * col[t * nf[0]];
-    T2[i] = sy;
+    taps<I>(g0[1] + ty, c0[1], first, n, w);
+    for (int cz = 0; cz < nc[2]; ++cz) {
+      const double* col = T1 + (cz * nc[1] + first) * nf[0] + tx;
+      double sy = 0.0;
+      for (int t = 0; t < n; ++t) sy += w[t] * col[t * nf[0]];
+      T2[(cz * nf[1] + ty) * nf[0] + tx] = sy;
+    }
   }
   __syncthreads();
   // ---- pass z -> ghost block
-  const int n3 = nf[0] * nf[1] * nf[2];
-  double* dst = ff + (size_t)blk * F.B3;
-  for (int i = tid; i < n3; i += GB_NT) {
-    const int fx = i % nf[0], fy = (i / nf[0]) % nf[1], fz = i / (nf[0] * nf[1]);
-    const int J[3] = {g0[0] + fx, g0[1] + fy, g0[2] + fz};
-    double v;
-    bool ext = false;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) ext = ext || (!F.per[a] && (J[a] < 0 || J[a] >= F.N[a]));
-    if (ext_zero && ext) {
-      v = 0.0;
-    } else {
-      double w[I];
-      int first, n;
-      taps<I>(J[2], c0[2], first, n, w);
-      const double* col = T2 + (first * nf[1] + fy) * nf[0] + fx;
-      double sz = 0.0;
-      for (int t = 0; t < n; ++t) sz += w[t] * col[t * nf[0] * nf[1]];
-      v = sz;
+  if (tx < nf[0] && ty < nf[1]) {
+    double* dst = ff + (size_t)blk * F.B3 + ((lo[2]) * B + (lo[1] + ty)) * B + (lo[0] + tx);
+    const int Jx = g0[0] + tx, Jy = g0[1] + ty;
+    const bool extxy = (!F.per[0] && (Jx < 0 || Jx >= F.N[0])) || (!F.per[1] && (Jy < 0 || Jy >= F.N[1]));
+    for (int fz = 0; fz < nf[2]; ++fz) {
+      const int Jz = g0[2] + fz;
+      const bool ext = extxy || (!F.per[2] && (Jz < 0 || Jz >= F.N[2]));
+      double v;
+      if (ext_zero && ext) {
+        v = 0.0;
+      } else {
+        double w[I];
+        int first, n;
+        taps<I>(Jz, c0[2], first, n, w);
+        const double* col = T2 + (first * nf[1] + ty) * nf[0] + tx;
+        double sz = 0.0;
+        for (int t = 0; t < n; ++t) sz += w[t] * col[t * nf[0] * nf[1]];
+        v = sz;
+      }
+      dst[fz * B * B] = v;
     }
-    dst[((lo[2] + fz) * B + (lo[1] + fy)) * B + (lo[0] + fx)] = v;
   }
 }
 
