@@ -51,8 +51,27 @@ __device__ __forceinline__ void taps(int J, int c0, int& first, int& n, double* 
 
 // box record (12 int32): dst block, lo[3], hi[3] (fine block-local, hi exclusive),
 // org[3] = level-global fine index of the block's node (0,0,0), 2 unused.
-// Threads form a 16 x 16 (x, y) tile and loop over the third axis, so that every
-// index is an add, not a division by a runtime extent.
+// Every stage iterates a 3-D index box with the 256 threads laid out as a 16 x 16 tile
+// over its two largest axes and a loop over the smallest one (ghost boxes are thin
+// slabs: 2 x 16 x 16 faces, 2 x 2 x 16 edges), so that the index arithmetic is adds
+// and every thread has work.
+template <typename Fn>
+__device__ __forceinline__ void box_for(const int D[3], Fn&& fn) {
+  int L = 2;  // loop axis: the smallest extent
+  if (D[0] < D[L]) L = 0;
+  if (D[1] < D[L]) L = 1;
+  const int A = L == 0 ? 1 : 0, Bx = L == 2 ? 1 : 2;
+  const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
+  if (ta >= D[A] || tb >= D[Bx]) return;
+  int k[3];
+  k[A] = ta;
+  k[Bx] = tb;
+  for (int l = 0; l < D[L]; ++l) {
+    k[L] = l;
+    fn(k[0], k[1], k[2]);
+  }
+}
+
 template <int I>
 __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ boxes, LevelView F, LevelView C,
                                                    double* __restrict__ ff, const double* __restrict__ cf,
@@ -73,7 +92,6 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   double* Cs = sm;                   // [nc2][nc1][nc0]
   double* T1 = sm + GB_SZ_A;         // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   // coarse block / local index along one axis (periodic wrap); -1 outside the block map
   auto cidx = [&](int a, int ci, int& b, int& l) {
     if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
@@ -84,71 +102,68 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   };
   // ---- stage the coarse support (nodes outside the coarse level -> 0, only reached
   // by non-needed nodes of the box)
-  if (tx < nc[0] && ty < nc[1]) {
-    int bxx, lx, byy, ly;
-    cidx(0, c0[0] + tx, bxx, lx);
-    cidx(1, c0[1] + ty, byy, ly);
-    for (int cz = 0; cz < nc[2]; ++cz) {
-      int bzz, lz;
-      cidx(2, c0[2] + cz, bzz, lz);
-      double v = 0.0;
-      if (bxx >= 0 && byy >= 0 && bzz >= 0) {
-        const int cblk = __ldg(C.bmap + ((size_t)bzz * C.bmap_n[1] + byy) * C.bmap_n[0] + bxx);
-        if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (lz * C.B + ly) * C.B + lx];
-      }
-      Cs[(cz * nc[1] + ty) * nc[0] + tx] = v;
+  box_for(nc, [&](int qx, int qy, int qz) {
+    int b[3], l[3];
+    cidx(0, c0[0] + qx, b[0], l[0]);
+    cidx(1, c0[1] + qy, b[1], l[1]);
+    cidx(2, c0[2] + qz, b[2], l[2]);
+    double v = 0.0;
+    if (b[0] >= 0 && b[1] >= 0 && b[2] >= 0) {
+      const int cblk = __ldg(C.bmap + ((size_t)b[2] * C.bmap_n[1] + b[1]) * C.bmap_n[0] + b[0]);
+      if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (l[2] * C.B + l[1]) * C.B + l[0]];
     }
-  }
+    Cs[(qz * nc[1] + qy) * nc[0] + qx] = v;
+  });
   __syncthreads();
   // ---- pass x: T1[cz][cy][fx]
-  if (tx < nf[0] && ty < nc[1]) {
-    double w[I];
-    int first, n;
-    taps<I>(g0[0] + tx, c0[0], first, n, w);
-    for (int cz = 0; cz < nc[2]; ++cz) {
-      const double* row = Cs + (cz * nc[1] + ty) * nc[0] + first;
+  {
+    const int D[3] = {nf[0], nc[1], nc[2]};
+    box_for(D, [&](int fx, int cy, int cz) {
+      double w[I];
+      int first, n;
+      taps<I>(g0[0] + fx, c0[0], first, n, w);
+      const double* row = Cs + (cz * nc[1] + cy) * nc[0] + first;
       double sx = 0.0;
       for (int t = 0; t < n; ++t) sx += w[t] * row[t];
-      T1[(cz * nc[1] + ty) * nf[0] + tx] = sx;
-    }
+      T1[(cz * nc[1] + cy) * nf[0] + fx] = sx;
+    });
   }
   __syncthreads();
   // ---- pass y: T2[cz][fy][fx]
-  if (tx < nf[0] && ty < nf[1]) {
-    double w[I];
-    int first, n;
-    taps<I>(g0[1] + ty, c0[1], first, n, w);
-    for (int cz = 0; cz < nc[2]; ++cz) {
-      const double* col = T1 + (cz * nc[1] + first) * nf[0] + tx;
+  {
+    const int D[3] = {nf[0], nf[1], nc[2]};
+    box_for(D, [&](int fx, int fy, int cz) {
+      double w[I];
+      int first, n;
+      taps<I>(g0[1] + fy, c0[1], first, n, w);
+      const double* col = T1 + (cz * nc[1] + first) * nf[0] + fx;
       double sy = 0.0;
       for (int t = 0; t < n; ++t) sy += w[t] * col[t * nf[0]];
-      T2[(cz * nf[1] + ty) * nf[0] + tx] = sy;
-    }
+      T2[(cz * nf[1] + fy) * nf[0] + fx] = sy;
+    });
   }
   __syncthreads();
   // ---- pass z -> ghost block
-  if (tx < nf[0] && ty < nf[1]) {
-    double* dst = ff + (size_t)blk * F.B3 + ((lo[2]) * B + (lo[1] + ty)) * B + (lo[0] + tx);
-    const int Jx = g0[0] + tx, Jy = g0[1] + ty;
-    const bool extxy = (!F.per[0] && (Jx < 0 || Jx >= F.N[0])) || (!F.per[1] && (Jy < 0 || Jy >= F.N[1]));
-    for (int fz = 0; fz < nf[2]; ++fz) {
-      const int Jz = g0[2] + fz;
-      const bool ext = extxy || (!F.per[2] && (Jz < 0 || Jz >= F.N[2]));
-      double v;
-      if (ext_zero && ext) {
-        v = 0.0;
-      } else {
-        double w[I];
-        int first, n;
-        taps<I>(Jz, c0[2], first, n, w);
-        const double* col = T2 + (first * nf[1] + ty) * nf[0] + tx;
-        double sz = 0.0;
-        for (int t = 0; t < n; ++t) sz += w[t] * col[t * nf[0] * nf[1]];
-        v = sz;
-      }
-      dst[fz * B * B] = v;
+  double* dst = ff + (size_t)blk * F.B3;
+  box_for(nf, [&](int fx, int fy, int fz) {
+    const int J[3] = {g0[0] + fx, g0[1] + fy, g0[2] + fz};
+    bool ext = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) ext = ext || (!F.per[a] && (J[a] < 0 || J[a] >= F.N[a]));
+    double v;
+    if (ext_zero && ext) {
+      v = 0.0;
+    } else {
+      double w[I];
+      int first, n;
+      taps<I>(J[2], c0[2], first, n, w);
+      const double* col = T2 + (first * nf[1] + fy) * nf[0] + fx;
+      double sz = 0.0;
+      for (int t = 0; t < n; ++t) sz += w[t] * col[t * nf[0] * nf[1]];
+      v = sz;
     }
-  }
+    dst[((lo[2] + fz) * B + (lo[1] + fy)) * B + (lo[0] + fx)] = v;
+  });
 }
 
 size_t c2f_box_smem() { return sizeof(double) * (size_t)(GB_SZ_A + GB_SZ_B); }
