@@ -93,11 +93,15 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   double* T1 = sm + GB_SZ_A;         // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
   // coarse block / local index along one axis (periodic wrap); -1 outside the block map
+  // (no runtime-extent divisions: B is a power of two, periodic wraps are conditional adds)
+  const int bsh = __ffs(C.B) - 1, bmask = C.B - 1;
   auto cidx = [&](int a, int ci, int& b, int& l) {
-    if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
-    const int bb = ci >= 0 ? ci / C.B : -((-ci + C.B - 1) / C.B);
-    l = ci - bb * C.B;
-    b = bb - C.bmap_lo[a];
+    if (C.per[a]) {
+      while (ci < 0) ci += C.N[a];
+      while (ci >= C.N[a]) ci -= C.N[a];
+    }
+    l = ci & bmask;
+    b = (ci >> bsh) - C.bmap_lo[a];  // arithmetic shift: floor(ci / B)
     if (b < 0 || b >= C.bmap_n[a]) b = -1;
   };
   // ---- stage the coarse support (nodes outside the coarse level -> 0, only reached
