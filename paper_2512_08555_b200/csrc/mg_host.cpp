@@ -874,9 +874,10 @@ void sweep(mg_handle* h, int m, bool with_res) {
 // ghosts: residual + u injection + full weighting (fused in one pencil kernel on B = 16
 // levels; else residual kernel + restriction kernel), then the level-(m-1) refresh,
 // FAS right-hand side and the û snapshot.
-// The fused kernel (mg_pencil.cu) is correct but, at 2 CTAs/SM, slower on cfg2 256^3
-// (190 us) than the residual pencil + restriction kernels (90 + 62 us): opt-in only.
-bool fused_res_restrict(mg_handle* h, int m) { return std::getenv("MG_FUSED_RR") != nullptr && h->L[m].B == 16; }
+// Fused residual + restriction (k_rr2_pencil) on B = 16 levels: the fine residual is
+// never written to HBM (cfg2 256^3: 127 us instead of 90 + 62 us); MG_NO_FUSED_RR=1
+// restores the two-kernel path.
+bool fused_res_restrict(mg_handle* h, int m) { return std::getenv("MG_NO_FUSED_RR") == nullptr && h->L[m].B == 16; }
 
 void restrict_level(mg_handle* h, int m) {
   Level& C = h->L[m - 1];

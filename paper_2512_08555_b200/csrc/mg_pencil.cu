@@ -585,11 +585,190 @@ __global__ void __launch_bounds__(RRShape::NT, 2) k_res_restrict_pencil(LevelVie
   cpa_wait<0>();
 }
 
+// Fused residual + restriction, column-pair version: the residual of the pencil and
+// its halo ring is computed as in the RB sweep (pairs of columns, shuffles for the
+// in-row neighbours, Mehrstellen partial sums per column: r(z) = f(z) - h6 [α(z-1) +
+// β(z) + α(z+1)]) and kept in a 2-plane shared ring; 2 extra warps form the
+// full-weighting sums of each plane and the coarse values (u injection at even planes).
+// Step s: load plane s | r at plane s-1 | xy weights of r(s-2) | coarse r at s-3.
+struct RR2Shape {
+  static constexpr int T = PB + 4, TW = 26, TP = T * TW;  // u tile as in the RB sweep
+  static constexpr int D = 2, R = 4;
+  static constexpr int NR = 192;                           // 6 warps of 30 pair threads
+  static constexpr int NT = NR + 64;                       // + 2 warps for the coarse nodes
+  static constexpr int NPAIR = T * T / 2;                  // 200 u pairs per plane
+  static constexpr int NLD = (NPAIR + NT - 1) / NT;        // 1
+  static constexpr int RRW = 20, RRP = 18 * RRW;           // r planes: rows [-1, 17), x in [-2, 18)
+  // [R][TP] u | [R][NR] f pairs | [2][RRP] r
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + R * NR * 2 + 2 * RRP);
+};
+
+template <int ORDER>
+__global__ void __maxnreg__(80)
+    k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
+  using S = RR2Shape;
+  constexpr int T = S::T, TW = S::TW, TP = S::TP, D = S::D, R = S::R, NR = S::NR, NT = S::NT;
+  constexpr int RRW = S::RRW, RRP = S::RRP;
+  extern __shared__ __align__(16) double sm[];
+  double* su = sm;
+  double2* sf = reinterpret_cast<double2*>(sm + R * TP);  // [R][NR]
+  double* sr = sm + R * TP + R * NR * 2;                   // [2][RRP]
+  __shared__ int snb[PMAXL * 27];
+  __shared__ uint32_t sreal[PMAXL];
+  __shared__ int spar[PMAXL * 4];
+  const int tid = threadIdx.x;
+  const int len = __ldg(L.pen_len + blockIdx.x);
+  const int nz = PB * len;
+  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  if (tid < len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
+  if (tid < 4 * len) spar[tid] = __ldg(L.parent + 4 * (size_t)__ldg(pb + tid / 4) + tid % 4);
+  // u load items (interior 128-byte lines first, then halo pieces), one per thread
+  int ld_xy, ld_sxy, ld_dst;
+  {
+    const int j = tid;
+    int py, px;
+    if (j < 8 * T) {
+      py = j / 8;
+      px = 2 + 2 * (j % 8);
+    } else {
+      const int hh = j - 8 * T;
+      py = hh / 2;
+      px = (hh & 1) ? PB + 2 : 0;
+    }
+    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
+    ld_xy = (y - PB * dy) * PB + (x - PB * dx);
+    ld_sxy = j < S::NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
+    ld_dst = py * TW + px;
+  }
+  // residual pair threads (warps 0-5): rows y = 3 w + lane / 10 - 1 in [-1, 17), x0 even
+  const int w = tid >> 5, lane = tid & 31;
+  const bool rthr = w < 6;
+  const bool valid = rthr && lane < 30;
+  const int ry = rthr ? 3 * w + (valid ? lane / 10 : 2) - 1 : 0;
+  const int pi = valid ? lane % 10 : 9;
+  const int x0 = 2 * pi - 2;
+  const int i0 = (ry + 2) * TW + (x0 + 2);
+  const int dxc = reg16(x0), dyc = reg16(ry);
+  const int sxy = (dxc + 1) + 3 * (dyc + 1);
+  const int fxy = (ry - PB * dyc) * PB + (x0 - PB * dxc);
+  double2* sfme = sf + (rthr ? tid : 0);
+  // coarse threads (warps 6-7): (qx, qy) of the octant
+  const bool cthr = tid >= NR;
+  const int qx = (tid - NR) & 7, qy = ((tid - NR) >> 3) & 7;
+  __syncthreads();
+
+  const double* ip = nullptr;
+  const double* fp = nullptr;
+  int zi = -2;
+  auto seek_issue = [&](int z) {
+    int k, dz, zl;
+    plane_src(z, nz, len, k, dz, zl);
+    const int o = zl * (PB * PB);
+    ip = ld_sxy < 0 ? nullptr : L.u + (size_t)snb[k * 27 + ld_sxy + 9 * (dz + 1)] * PB3 + o + ld_xy;
+    fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
+  };
+  auto issue = [&]() {
+    if (zi < nz + 2) {
+      if ((zi & 15) == 0) seek_issue(zi);
+      const int slot = (zi + 2) & (R - 1);
+      if (ld_sxy >= 0) cpa16(su + slot * TP + ld_dst, ip);
+      ip += PB * PB;
+      if (valid && zi >= -1 && zi <= nz) cpa16(sfme + slot * NR, fp);
+      fp += PB * PB;
+    }
+    cpa_commit();
+    ++zi;
+  };
+  bool live = false;
+  auto seek_live = [&](int z) {
+    int k, dz, zl;
+    plane_src(z, nz, len, k, dz, zl);
+    live = valid && ((sreal[k] >> (sxy + 9 * (dz + 1))) & 1u);
+  };
+  seek_issue(-2);
+  seek_live(-1);
+#pragma unroll
+  for (int q = 0; q < D; ++q) issue();
+
+  double aA[2] = {0, 0}, aP[2] = {0, 0};  // per column: α(s-1); α(s-2) + β(s-1)
+  double t0 = 0, t1 = 0, t2 = 0;          // coarse threads: T at planes s-2, s-3, s-4
+  const double h6 = ORDER == 4 ? inv_h2 * (1.0 / 6.0) : inv_h2;
+  for (int s = -2; s <= nz + 2; ++s) {
+    cpa_wait<D - 1>();
+    __syncthreads();
+    issue();
+    if (rthr) {
+      // plane s (shuffles: every lane of warps 0-5 takes part)
+      const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+      const double2 m = *reinterpret_cast<const double2*>(U - TW);
+      const double2 cc = *reinterpret_cast<const double2*>(U);
+      const double2 p = *reinterpret_cast<const double2*>(U + TW);
+      const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
+      double cq[2] = {cc.x, cc.y};
+      double s4q[2] = {(l + cc.y) + (m.x + p.x), (cc.x + r) + (m.y + p.y)};
+      double d4q[2] = {0, 0};
+      if (ORDER == 4) {
+        const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
+        d4q[0] = (ml + m.y) + (pl + p.y);
+        d4q[1] = (m.x + mr) + (p.x + pr);
+      }
+      if (s >= 0 && s <= nz + 1) {  // residual at plane s-1 in [-1, nz]
+        if (((s - 1) & 15) == 0) seek_live(s - 1);
+        const double2 fq = sfme[((s + 1) & (R - 1)) * NR];
+        double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
+        if (live) {
+          const double al0 = ORDER == 4 ? 2.0 * cq[0] + s4q[0] : cq[0];
+          const double al1 = ORDER == 4 ? 2.0 * cq[1] + s4q[1] : cq[1];
+          rr.x = fq.x - (aP[0] + al0) * h6;
+          rr.y = fq.y - (aP[1] + al1) * h6;
+        }
+        if (valid) *reinterpret_cast<double2*>(sr + ((s - 1) & 1) * RRP + (ry + 1) * RRW + (x0 + 2)) = rr;
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double al = ORDER == 4 ? 2.0 * cq[q] + s4q[q] : cq[q];
+        const double be = ORDER == 4 ? 2.0 * s4q[q] + d4q[q] - 24.0 * cq[q] : s4q[q] - 6.0 * cq[q];
+        aP[q] = aA[q] + be;  // α(s-1) + β(s): the node at s, completed at step s+1
+        aA[q] = al;
+      }
+    } else if (cthr) {
+      // coarse u = fine u(2i) at even interior planes (E7)
+      if (s >= 0 && s < nz && (s & 1) == 0) {
+        const int k = s >> 4, qz = (s & 15) >> 1;
+        const int* pr = spar + 4 * k;
+        C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] =
+            su[((s + 2) & (R - 1)) * TP + (2 * qy + 2) * TW + (2 * qx + 2)];
+      }
+      // full weighting of the residual plane s-2 (written last step): x, then y, then z
+      if (s - 2 >= -1 && s - 2 <= nz) {
+        const double* rp = sr + ((s - 2) & 1) * RRP + (2 * qy + 1) * RRW + (2 * qx + 2);
+        double sy = 0.0;
+#pragma unroll
+        for (int dy = -1; dy <= 1; ++dy) {
+          const double* row = rp + dy * RRW;
+          const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
+          sy += (dy == 0 ? 0.5 : 0.25) * sx;
+        }
+        t2 = t1; t1 = t0; t0 = sy;
+        const int zc = s - 3;
+        if (zc >= 0 && zc < nz && (zc & 1) == 0) {
+          const double sz = (0.25 * t2 + 0.5 * t1) + 0.25 * t0;
+          const int k = zc >> 4, qz = (zc & 15) >> 1;
+          const int* pr = spar + 4 * k;
+          C.r[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] = sz;
+        }
+      }
+    }
+  }
+  cpa_wait<0>();
+}
+
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (fine.B != PB || fine.npen <= 0 || fine.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (fine.h * fine.h);
-  if (order == 2) k_res_restrict_pencil<2><<<fine.npen, RRShape::NT, RRShape::SMEM, s>>>(fine, coarse, inv_h2);
-  else k_res_restrict_pencil<4><<<fine.npen, RRShape::NT, RRShape::SMEM, s>>>(fine, coarse, inv_h2);
+  if (order == 2) k_rr2_pencil<2><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else k_rr2_pencil<4><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
   note_launch();
   return true;
 }
@@ -635,8 +814,8 @@ void prepare_pencil_kernels() {
   setup((const void*)v.k4, v.smem);
   setup((const void*)v.k2s, v.smem);
   setup((const void*)v.k4s, v.smem);
-  setup((const void*)k_res_restrict_pencil<2>, RRShape::SMEM);
-  setup((const void*)k_res_restrict_pencil<4>, RRShape::SMEM);
+  setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
+  setup((const void*)k_rr2_pencil<4>, RR2Shape::SMEM);
   setup((const void*)k_res_pencil<2, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
