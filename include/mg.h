@@ -125,7 +125,7 @@ int mg_num_levels(mg_handle* h);
 
 enum { MG_FIELD_U = 0, MG_FIELD_F = 1, MG_FIELD_R = 2, MG_FIELD_UHAT = 3 };
 /* dir 0: export the level's real blocks [n_real][B^3] into dev; 1: import from dev;
- * 2: export real then ghost blocks [n_real + n_ghost][B^3] (ghost-fill checks) */
+ * 2 / 3: export / import real then ghost blocks [n_real + n_ghost][B^3] (ghost checks) */
 int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev);
 enum {
   MG_OP_REFRESH = 0,        /* ghost fill of `level` (f2c injection + c2f / band) */

@@ -367,6 +367,10 @@ class Oracle:
         Lc = self.Lu(m - 1)
         C.f = np.where(C.cov, C.r + Lc, C.f)
         C.uhat = np.where(C.mask, C.u, 0.0)
+        # "the û snapshot includes the band": the exterior values of
+        # level m-1 (c2f chain / coarse-solve band) at this moment (Z13-W)
+        if self._exterior_ext(C).any():
+            C.uhat_ext = self.lookup(m - 1, self.uvals())
 
     def prolong(self, m):
         """u_m += I ε_{m-1}, ε = u - û on level-(m-1) nodes (correction sign: reading
@@ -375,6 +379,12 @@ class Oracle:
         L, C = self.levels[m], self.levels[m - 1]
         eps = np.where(C.mask, C.u - C.uhat, 0.0)
         X = self._pad(eps, fill=0.0)
+        # exterior band (U1): ε = current exterior value - its snapshot at restriction;
+        # jump ghosts keep ε := 0 (Z13-W)
+        ext = self._exterior_ext(C)
+        if ext.any() and hasattr(C, "uhat_ext"):
+            cur = self.lookup(m - 1, self.uvals())
+            X = np.where(ext, cur - C.uhat_ext, X)
         for ax in range(3):
             Xm = np.moveaxis(X, ax, 0)
             nce = Xm.shape[0]

@@ -91,7 +91,7 @@ struct Level {
   std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len, gbox;
   std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
-  std::vector<uint32_t> nbr_real;
+  std::vector<uint32_t> nbr_real, nbr_ext;
   std::vector<uint8_t> covmask, c2f_ext;
   int bmap_lo[3] = {0, 0, 0}, bmap_n[3] = {1, 1, 1};
   // device
@@ -102,6 +102,7 @@ struct Level {
           *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr,
           *d_gbox = nullptr, *d_sw_blk = nullptr, *d_sw_len = nullptr, *d_sw_z = nullptr;
   uint32_t* d_nbr_real = nullptr;
+  uint32_t* d_nbr_ext = nullptr;
   uint8_t *d_covmask = nullptr, *d_c2f_ext = nullptr;
 
   int ntot() const { return nreal + nghost; }
@@ -225,6 +226,7 @@ LevelView view(mg_handle* h, int m) {
   v.uhat = l.uhat;
   v.nbr = l.d_nbr;
   v.nbr_real = l.d_nbr_real;
+  v.nbr_ext = l.d_nbr_ext;
   v.covmask = l.d_covmask;
   v.parent = l.d_parent;
   v.bmap = l.d_bmap;
@@ -573,6 +575,7 @@ void build_ghosts(mg_handle* h) {
     Level& l = h->L[m];
     l.nbr.assign(27 * (size_t)l.nreal, -1);
     l.nbr_real.assign(l.nreal, 0);
+    l.nbr_ext.assign(l.nreal, 0);
     for (int i = 0; i < l.nreal; ++i) {
       const auto c = l.coords[i];
       for (int o = 0; o < 27; ++o) {
@@ -585,6 +588,7 @@ void build_ghosts(mg_handle* h) {
         if (idx < 0) throw MgError(MG_ERR_LAYOUT_GHOST, "missing neighbour block");
         l.nbr[27 * (size_t)i + o] = idx;
         if (idx < l.nreal) l.nbr_real[i] |= 1u << o;
+        else if (l.ghost_ext[idx - l.nreal]) l.nbr_ext[i] |= 1u << o;
       }
     }
     int lo[3], hi[3];
@@ -706,6 +710,7 @@ void alloc_device(mg_handle* h) {
     }
     l.d_nbr = dev_upload(l.nbr);
     l.d_nbr_real = dev_upload(l.nbr_real);
+    l.d_nbr_ext = dev_upload(l.nbr_ext);
     l.d_covmask = dev_upload(l.covmask);
     l.d_parent = dev_upload(l.parent);
     l.d_bmap = dev_upload(l.bmap);
@@ -900,6 +905,14 @@ void restrict_level(mg_handle* h, int m) {
   CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
 }
 
+// u_m += P(u - û)_{m-1} (Alg. 1).  Under U1 the exterior band of level m-1
+// enters ε (current exterior value minus its snapshot, Z13-W): refresh it first.
+void prolong_level(mg_handle* h, int m) {
+  if (m - 1 >= 1 && h->L[m - 1].ext_chain) refresh(h, m - 1);
+  Prof pr(h, ST_PROLONG, m);
+  launch_prolong(view(h, m), view(h, m - 1), h->s);
+}
+
 void coarse_solve(mg_handle* h) {
   Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
@@ -928,10 +941,7 @@ void vcycle_body(mg_handle* h) {
   }
   coarse_solve(h);
   for (int m = 1; m <= top; ++m) {
-    {
-      Prof pr(h, ST_PROLONG, m);
-      launch_prolong(view(h, m), view(h, m - 1), h->s);
-    }
+    prolong_level(h, m);
     for (int k = 0; k < h->eta2; ++k) sweep(h, m, false);
   }
   // Inject-up (a8) is deferred to the next consumer of coarse covered values that is
@@ -1080,7 +1090,7 @@ void destroy(mg_handle* h) {
   for (auto e : h->evpool) cudaEventDestroy(e);
   for (auto& l : h->L) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
-                    (void*)l.d_nbr_real, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
+                    (void*)l.d_nbr_real, (void*)l.d_nbr_ext, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
                     (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src, (void*)l.d_pen_blk,
                     (void*)l.d_pen_len, (void*)l.d_gbox, (void*)l.d_sw_blk, (void*)l.d_sw_len, (void*)l.d_sw_z})
       if (p) cudaFree(p);
@@ -1305,7 +1315,7 @@ int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev) {
   return guard(h, [&] {
     Level& l = h->L[level];
     double* p = field == MG_FIELD_U ? l.u[l.cur] : field == MG_FIELD_F ? l.f : field == MG_FIELD_R ? l.r : l.uhat;
-    const size_t n = (size_t)(dir == 2 ? l.ntot() : l.nreal) * l.B3 * sizeof(double);
+    const size_t n = (size_t)(dir >= 2 ? l.ntot() : l.nreal) * l.B3 * sizeof(double);
     if (dir == 0 || dir == 2) CUDA_OK(cudaMemcpyAsync(dev, p, n, cudaMemcpyDeviceToDevice, h->s));
     else CUDA_OK(cudaMemcpyAsync(p, dev, n, cudaMemcpyDeviceToDevice, h->s));
     CUDA_OK(cudaStreamSynchronize(h->s));
@@ -1330,7 +1340,7 @@ static void apply_op(mg_handle* h, int op, int level) {
       break;
     case MG_OP_PROLONG:
       if (level < 1) throw MgError(MG_ERR_ARG, "prolong needs level >= 1");
-      launch_prolong(view(h, level), view(h, level - 1), h->s);
+      prolong_level(h, level);
       break;
     case MG_OP_INJECT_UP: inject_up_all(h); break;
     case MG_OP_COARSE_SOLVE: coarse_solve(h); break;

@@ -23,6 +23,7 @@ struct LevelView {
   double* uhat;
   const int32_t* nbr;       // [nreal][27], slot (dx+1)+3(dy+1)+9(dz+1) -> block index
   const uint32_t* nbr_real; // [nreal] bit s set iff slot s is a real block
+  const uint32_t* nbr_ext;  // [nreal] bit s set iff slot s is a ghost block beyond an unbounded face
   const uint8_t* covmask;   // [nreal] octant o covered by the finer level (bit o)
   const int32_t* parent;    // [nreal][4] (parent block in level-1, ox, oy, oz); m >= 1
   const int32_t* bmap;      // dense block-coordinate map (real+ghost) of this level

@@ -696,7 +696,7 @@ __global__ void k_prolong(LevelView F, LevelView C) {
           const int X = cx + tx, Y = cy + ty, Z = cz + tz;
           const int slot = (region(X, C.B) + 1) + 3 * (region(Y, C.B) + 1) + 9 * (region(Z, C.B) + 1);
           // ε := 0 outside the coarse level's blocks (reading Z13-W)
-          vx[tx] = ((C.nbr_real[p] >> slot) & 1u)
+          vx[tx] = (((C.nbr_real[p] | C.nbr_ext[p]) >> slot) & 1u)
                        ? fetch(C.u, nb, C.B, X, Y, Z) - fetch(C.uhat, nb, C.B, X, Y, Z) : 0.0;
         }
         vy[ty] = nx == 2 ? 0.5 * (vx[0] + vx[1]) : vx[0];
@@ -725,7 +725,8 @@ __global__ void __launch_bounds__(256) k_prolong2(LevelView F, LevelView C) {
   for (int k = 0; k < B3 / 256; ++k) uf[k] = F.u[(size_t)b * B3 + tid + k * 256];
   __syncthreads();
   const int CB = C.B;
-  const uint32_t creal = C.nbr_real[p];
+  // ε is taken on real coarse nodes and on the exterior band (U1); 0 at jump ghosts (Z13-W)
+  const uint32_t creal = C.nbr_real[p] | C.nbr_ext[p];
   for (int i = tid; i < E * E * E; i += 256) {
     const int x = ox + i % E, y = oy + (i / E) % E, z = oz + i / (E * E);
     const int dx = region(x, CB), dy = region(y, CB), dz = region(z, CB);

@@ -212,7 +212,7 @@ class Solver:
             out = t.empty((n, info["B"], info["B"], info["B"]), dtype=t.float64, device="cuda")
             self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 2 if ghosts else 0, _ptr(out)))
             return out
-        self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 1, _ptr(tensor)))
+        self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 3 if ghosts else 1, _ptr(tensor)))
 
     def debug_apply(self, op, m):
         self._check(self.lib.mg_debug_apply(self.h, OPS[op] if isinstance(op, str) else int(op), int(m)))

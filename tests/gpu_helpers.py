@@ -66,3 +66,27 @@ class Pair:
 
     def solution(self):
         return self.g.get_solution().cpu().numpy()
+
+    def push_exterior(self, field, m, ext_arr):
+        """Write the oracle's extended-array values (pad E) at the exterior ghost-block
+        nodes of GPU level m (U1 band snapshots), keeping everything else."""
+        from oracle.mg_oracle import E
+        from paper_2512_08555_b200 import MG_FIELD_F, MG_FIELD_R, MG_FIELD_U, MG_FIELD_UHAT
+        code = dict(u=MG_FIELD_U, f=MG_FIELD_F, r=MG_FIELD_R, uhat=MG_FIELD_UHAT)[field]
+        allb = self.g.debug_field(code, m, ghosts=True).cpu().numpy()
+        coords = self.g.level_blocks(m, ghosts=True)
+        nreal = self.g.level_info(m)["nreal"]
+        B = self.B[m]
+        N = self.o.levels[m].N
+        per = self.o.per
+        for g in range(nreal, len(coords)):
+            c = coords[g]
+            if all(per[a] or 0 <= c[a] * B < N[a] for a in range(3)):
+                continue                      # a jump ghost block, not exterior
+            for lz in range(B):
+                for ly in range(B):
+                    for lx in range(B):
+                        X = (c[0] * B + lx + E, c[1] * B + ly + E, c[2] * B + lz + E)
+                        if all(0 <= X[a] < ext_arr.shape[a] for a in range(3)) and np.isfinite(ext_arr[X]):
+                            allb[g, lz, ly, lx] = ext_arr[X]
+        self.g.debug_field(code, m, self.torch.from_numpy(allb).cuda(), ghosts=True)

@@ -192,6 +192,9 @@ def test_op_prolong(name):
     for L in p.o.levels:
         L.uhat = np.where(L.mask, L.u + 1e-2 * rng.standard_normal(L.u.shape), 0.0)
     p.push_state()
+    for m, L in enumerate(p.o.levels):   # U1: the band snapshot enters ε (Z13-W)
+        if hasattr(L, "uhat_ext"):
+            p.push_exterior("uhat", m, L.uhat_ext)
     for m in range(1, len(p.o.levels)):
         p.o.prolong(m)
         p.g.debug_apply("prolong", m)
