@@ -417,27 +417,46 @@ class Oracle:
             return
         shape = [N[ax] if self.per[ax] else LGF.pad_size(N[ax], GE) for ax in range(3)]
         self.coarse_shape = shape
+        th = [2 * np.pi * np.fft.fftfreq(s) for s in shape]
+        TH = np.meshgrid(*th, indexing="ij")
         if len(self.unb) == 3:
             self.coarse_kind = "UUU"
             R = LGF.box_radius(max(shape))
             G = LGF.box_lgf(3, self.order, R)
             T = LGF.wrapped_table(G, R, shape)
             self.coarse_mult = np.fft.fftn(T).real * c.h * c.h
-        elif len(self.unb) == 2 and self.per[0]:
-            self.coarse_kind = "PUU"
-            R = LGF.box_radius(max(shape[1:]))
-            G2 = LGF.box_lgf(2, self.order, R)
-            T2 = LGF.wrapped_table(G2, R, shape[1:])
-            K = np.empty(shape)
-            th = [2 * np.pi * np.fft.fftfreq(s) for s in shape]
-            TH = np.meshgrid(*th, indexing="ij")
-            sig = symbol(self.order, TH, c.h)
-            sig[0] = 1.0
-            K[...] = 1.0 / sig
-            K[0] = np.fft.fft2(T2).real * c.h * c.h      # E14: k_per = 0 -> 2D LGF
-            self.coarse_mult = K
+            return
+        # mixed periodic / unbounded (E14, generalised; reading Z22): along the
+        # periodic axes the transform is exact, along the unbounded ones zero-padded.  The
+        # Fourier modes with zero periodic wavenumber reduce the operator to the unbounded
+        # axes alone (their δ² eigenvalues vanish in the symbol): there the multiplier is
+        # the transform of that lower-dimensional LGF (2D box LGF, or the 1D LGF |n|/2);
+        # every other mode is regular and takes 1/σ_M on the padded lattice.
+        sig = symbol(self.order, TH, c.h)
+        zero_per = np.ones(tuple(shape), dtype=bool)
+        for ax in range(3):
+            if self.per[ax]:
+                sl = [None, None, None]
+                sl[ax] = slice(None)
+                zero_per &= (np.arange(shape[ax]) == 0).reshape([-1 if a == ax else 1 for a in range(3)])
+        K = 1.0 / np.where(zero_per, 1.0, sig)
+        ush = [shape[ax] for ax in self.unb]
+        if len(self.unb) == 2:
+            self.coarse_kind = "P" + "U" * 2
+            R = LGF.box_radius(max(ush))
+            G = LGF.box_lgf(2, self.order, R)
+            Tl = LGF.wrapped_table(G, R, ush)
+            Kl = np.fft.fft2(Tl).real * c.h * c.h
         else:
-            raise NotImplementedError("boundary combination not supported by the oracle")
+            self.coarse_kind = "PPU"
+            P = ush[0]
+            n = np.arange(P)
+            n = np.where(n <= P // 2, n, n - P)
+            Tl = np.abs(n) / 2.0      # 1D LGF: δ²(|n|/2) = δ[n], G[0] = 0
+            Kl = np.fft.fft(Tl).real * c.h * c.h
+        shp = [shape[ax] if not self.per[ax] else 1 for ax in range(3)]
+        K = np.where(zero_per, Kl.reshape(shp), K)
+        self.coarse_mult = K
 
     def coarse_solve(self):
         """u_0 <- S_0 f_0 (Alg. 1).  PPP: F^-1[F f / σ_M], zero mode -> 0

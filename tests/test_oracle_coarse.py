@@ -53,11 +53,15 @@ def _single_level(bc, n=32, order=4):
     return MO.Oracle(d, Lay.uniform_leaves(C.domain(d)))
 
 
-@pytest.mark.parametrize("bc", [(0, 0, 0), (0, 1, 1), (1, 1, 1)])
+ALL_BC = [(0, 0, 0), (0, 1, 1), (1, 0, 1), (1, 1, 0), (0, 0, 1), (0, 1, 0), (1, 0, 0), (1, 1, 1)]
+
+
+@pytest.mark.parametrize("bc", ALL_BC)
 @pytest.mark.parametrize("order", [2, 4])
 def test_direct_solve_discrete_exactness(bc, order):
-    """Δ_h^M (S_0 f) = f on every domain node and on the exterior band (GE layers):
-    the coarse kernel is the exact inverse of the multigrid operator."""
+    """Δ_h^M (S_0 f) = f on every domain node and on the exterior band (GE layers), for
+    every mix of periodic / unbounded axes: the coarse kernel is the exact inverse of
+    the multigrid operator on the zero-padded lattice."""
     o = _single_level(bc, order=order)
     c = o.levels[0]
     rng = np.random.default_rng(7)
@@ -68,16 +72,55 @@ def test_direct_solve_discrete_exactness(bc, order):
     o.coarse_solve()
     X = o.lookup(0, o.uvals())
     Lu = MO.apply_L(X, c.h, order)
-    Fe = np.zeros_like(X)
-    Fe[MO.E:MO.E + 32, MO.E:MO.E + 32, MO.E:MO.E + 32] = f
-    if bc[0] == 0:
-        Fe = o._pad(f, fill=0.0)
+    Fe = o._pad(f, fill=0.0)          # periodic images / zero beyond unbounded faces
     lo, hi = MO.E - (MO.GE - 1), MO.E + 32 + (MO.GE - 1)
     sl = tuple(slice(MO.E, MO.E + 32) if bc[a] == 0 else slice(lo, hi) for a in range(3))
     err = np.abs(Lu[sl] - Fe[sl]).max() / np.abs(f).max()
     assert err < 1e-12, err
     if bc == (0, 0, 0):
         assert abs(c.u.mean()) < 1e-14 * np.abs(c.u).max()     # zero average
+
+
+def test_one_dimensional_lgf_closed_form():
+    """The 1D lattice Green's function used for one unbounded axis: δ²(|n|/2) = δ[n]."""
+    n = np.arange(-20, 21)
+    G = np.abs(n) / 2.0
+    d2 = G[:-2] - 2 * G[1:-1] + G[2:]
+    assert np.array_equal(d2, (n[1:-1] == 0).astype(float))
+
+
+@pytest.mark.parametrize("bc", [(0, 0, 1), (1, 0, 1)])
+def test_product_manufactured_mixed_fourth_order(bc):
+    """Manufactured products in the spirit of E25-E28 for other periodic /
+    unbounded mixes: u = Π_d g_d(x_d) with g = u_per on periodic axes and u_unb (compact,
+    so the free-space solution) on unbounded ones; 4th-order convergence of S_0."""
+    errs = []
+    for n in (32, 64):
+        d = dict(origin=(0.0, 0.0, 0.0), h0=1 / n, base_blocks=(n // 16,) * 3, B=16, bc=bc,
+                 order=4, smoother=1, omega=1.0, eta1=1, eta2=1, coarse_n=0)
+        dom = C.domain(d)
+        lv = Lay.uniform_leaves(dom)
+        g = [S.u_per if b == 0 else S.u_unb for b in bc]
+        d2g = [S.d2u_per if b == 0 else S.d2u_unb for b in bc]
+
+        def fn(x, y, z):
+            X = (x, y, z)
+            tot = 0.0
+            for k in range(3):
+                term = 1.0
+                for a in range(3):
+                    term = term * (d2g[a](X[a]) if a == k else g[a](X[a]))
+                tot = tot + term
+            return tot
+
+        f = S.sample_on_leaves(dom, lv, fn)
+        ue = S.sample_on_leaves(dom, lv, lambda x, y, z: g[0](x) * g[1](y) * g[2](z))
+        o = MO.Oracle(d, lv)
+        o.set_rhs(f)
+        o.vcycle(1)
+        errs.append(np.abs(o.get_solution() - ue).max())
+    rate = math.log2(errs[0] / errs[1])
+    assert rate > 3.6, (errs, rate)
 
 
 def test_free_space_gaussian_fourth_order():
