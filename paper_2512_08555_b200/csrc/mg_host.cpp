@@ -759,10 +759,10 @@ void setup_coarse(mg_handle* h) {
     h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * c.N[a] + 2 * GE - 1);
     nunb += !h->per[a];
   }
-  if (nunb == 0) h->coarse_kind = 0;
-  else if (nunb == 3) h->coarse_kind = 1;
-  else if (nunb == 2 && h->per[0]) h->coarse_kind = 2;
-  else throw MgError(MG_ERR_BC, "boundary combination not supported yet (PPP, UUU, x-periodic PUU)");
+  // 0: all periodic (spectral, zero mode -> 0); 1: all unbounded (3D LGF table);
+  // 2: any other mix (generalised E14: lower-dimensional LGF on zero periodic
+  //    wavenumbers, 1/σ elsewhere; reading Z22)
+  h->coarse_kind = nunb == 0 ? 0 : (nunb == 3 ? 1 : 2);
   const int Px = h->P[0], Py = h->P[1], Pz = h->P[2];
   const int64_t nd = (int64_t)Px * Py * Pz, nc = (int64_t)(Px / 2 + 1) * Py * Pz;
   CUDA_OK(cudaMalloc(&h->d_dense, nd * sizeof(double)));
@@ -788,27 +788,52 @@ void setup_coarse(mg_handle* h) {
     CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
     launch_real_part_scale(h->d_spec, h->d_mult, nc, sc, h->s);
   } else if (h->coarse_kind == 2) {
-    const int R = std::max(Py, Pz) / 2 + 8;
-    std::vector<double> G = box_lgf(2, h->order, R);
-    const int n = 2 * R + 1;
-    std::vector<cufftDoubleComplex> T((size_t)Py * Pz);
-    for (int z = 0; z < Pz; ++z)
-      for (int y = 0; y < Py; ++y) {
-        const int ny = y <= Py / 2 ? y : y - Py, nz = z <= Pz / 2 ? z : z - Pz;
-        T[(size_t)z * Py + y] = make_cuDoubleComplex(G[(size_t)(nz + R) * n + (ny + R)], 0.0);
+    int ua = -1, ub = -1;  // the unbounded axes (ub = -1: only one)
+    for (int a = 0; a < 3; ++a)
+      if (!h->per[a]) (ua < 0 ? ua : ub) = a;
+    double* dLow = nullptr;  // transform of the lower-dimensional LGF, x h^2 / (Px Py Pz)
+    if (ub >= 0) {
+      const int Pa = h->P[ua], Pb = h->P[ub];
+      const int R = std::max(Pa, Pb) / 2 + 8;
+      std::vector<double> G = box_lgf(2, h->order, R);
+      const int n = 2 * R + 1;
+      std::vector<cufftDoubleComplex> T((size_t)Pa * Pb);
+      for (int j = 0; j < Pb; ++j)
+        for (int i = 0; i < Pa; ++i) {
+          const int ni = i <= Pa / 2 ? i : i - Pa, nj = j <= Pb / 2 ? j : j - Pb;
+          // G index (first, second) = (axis ua, axis ub), matching the oracle's box layout
+          T[(size_t)j * Pa + i] = make_cuDoubleComplex(G[(size_t)(ni + R) * n + (nj + R)], 0.0);
+        }
+      cufftDoubleComplex* dT = nullptr;
+      CUDA_OK(cudaMalloc(&dT, T.size() * sizeof(cufftDoubleComplex)));
+      CUDA_OK(cudaMemcpy(dT, T.data(), T.size() * sizeof(cufftDoubleComplex), cudaMemcpyHostToDevice));
+      cufftHandle p2;
+      CUFFT_OK(cufftPlan2d(&p2, Pb, Pa, CUFFT_Z2Z));
+      CUFFT_OK(cufftSetStream(p2, h->s));
+      CUFFT_OK(cufftExecZ2Z(p2, dT, dT, CUFFT_FORWARD));
+      CUDA_OK(cudaMalloc(&dLow, T.size() * sizeof(double)));
+      launch_real_part_scale(dT, dLow, (int64_t)T.size(), sc, h->s);
+      CUDA_OK(cudaStreamSynchronize(h->s));
+      cufftDestroy(p2);
+      cudaFree(dT);
+    } else {
+      // one unbounded axis: the 1D LGF |n|/2 (δ²(|n|/2) = δ), transformed by a direct DFT
+      const int P = h->P[ua];
+      std::vector<double> T1(P);
+      for (int k = 0; k < P; ++k) {
+        double acc = 0.0;
+        for (int i = 0; i < P; ++i) {
+          const int ni = i <= P / 2 ? i : i - P;
+          acc += 0.5 * std::abs(ni) * std::cos(2.0 * M_PI * (double)((int64_t)k * i % P) / P);
+        }
+        T1[k] = acc * sc;
       }
-    cufftDoubleComplex* dT = nullptr;
-    CUDA_OK(cudaMalloc(&dT, T.size() * sizeof(cufftDoubleComplex)));
-    CUDA_OK(cudaMemcpy(dT, T.data(), T.size() * sizeof(cufftDoubleComplex), cudaMemcpyHostToDevice));
-    cufftHandle p2;
-    CUFFT_OK(cufftPlan2d(&p2, Pz, Py, CUFFT_Z2Z));
-    CUFFT_OK(cufftSetStream(p2, h->s));
-    CUFFT_OK(cufftExecZ2Z(p2, dT, dT, CUFFT_FORWARD));
-    CUDA_OK(cudaMalloc(&h->d_mult, T.size() * sizeof(double)));
-    launch_real_part_scale(dT, h->d_mult, (int64_t)T.size(), sc, h->s);
+      dLow = dev_upload(T1);
+    }
+    CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
+    launch_build_mult(h->d_mult, h->P, h->per, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, h->s);
     CUDA_OK(cudaStreamSynchronize(h->s));
-    cufftDestroy(p2);
-    cudaFree(dT);
+    cudaFree(dLow);
   }
   CUDA_OK(cudaStreamSynchronize(h->s));
 }
@@ -919,9 +944,7 @@ void coarse_solve(mg_handle* h) {
   launch_coarse_gather(c, h->d_dense, h->P, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
   if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
-  else if (h->coarse_kind == 1)
-    launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
-  else launch_coarse_mul_puu(h->d_spec, h->P, h->order, h->L[0].h, h->d_mult, h->s);
+  else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
   CUFFT_OK(cufftExecZ2D(h->plan_b, (cufftDoubleComplex*)h->d_spec, h->d_dense));
   launch_coarse_scatter(c, h->d_dense, h->P, c2f_list(h->L[0]), h->s);
 }

@@ -92,6 +92,9 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
                            cudaStream_t s);
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s);
 void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s);
+// full multiplier table of a mixed periodic / unbounded coarse solve (R2C layout)
+void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
+                       double h2, double scale, cudaStream_t s);
 void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s);
 void launch_scale(double* p, int64_t n, double a, cudaStream_t s);
 void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s);

@@ -998,6 +998,41 @@ void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const 
   { k_mul_puu<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h, tab2); ++g_nlaunch; }
 }
 
+// Multiplier of a mixed periodic / unbounded coarse solve on the R2C spectrum (x halved):
+// modes whose periodic wavenumbers are all zero take the transform of the LGF of the
+// operator restricted to the unbounded axes (`low`, already x h^2 / (Px Py Pz)); all
+// others h^2 / σ_M(k) / (Px Py Pz) (generalised E14, reading Z22).
+__global__ void k_build_mult(double* __restrict__ mult, int Px, int Py, int Pz, int perx, int pery, int perz,
+                             int ua, int ub, const double* __restrict__ low, int order, double h2, double scale) {
+  const int Hx = Px / 2 + 1;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Hx * Py * Pz;
+  if (i >= n) return;
+  const int k[3] = {(int)(i % Hx), (int)((i / Hx) % Py), (int)(i / ((int64_t)Hx * Py))};
+  const int P[3] = {Px, Py, Pz}, per[3] = {perx, pery, perz};
+  bool zero_per = true;
+  for (int a = 0; a < 3; ++a)
+    if (per[a] && k[a] != 0) zero_per = false;
+  double m;
+  if (zero_per) {
+    m = ub >= 0 ? low[(int64_t)k[ub] * P[ua] + k[ua]] : low[k[ua]];
+  } else {
+    const double tw = 6.283185307179586476925286766559;
+    const double sx = 2.0 * cos(tw * k[0] / Px) - 2.0, sy = 2.0 * cos(tw * k[1] / Py) - 2.0,
+                 sz = 2.0 * cos(tw * k[2] / Pz) - 2.0;
+    m = h2 / symbol_h2(order, sx, sy, sz) * scale;
+  }
+  mult[i] = m;
+}
+
+void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
+                       double h2, double scale, cudaStream_t s) {
+  const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
+  k_build_mult<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mult, P[0], P[1], P[2], per[0], per[1], per[2], ua, ub,
+                                                             low, order, h2, scale);
+  ++g_nlaunch;
+}
+
 __global__ void k_scale(double* p, int64_t n, double a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] *= a;

@@ -35,6 +35,22 @@ def _puu_adaptive(depth=1):
     return d, lv, f
 
 
+def _mixed_adaptive(bc):
+    """2-level layout for any periodic / unbounded mix: base 4^3 blocks (h0 = 1/64), the
+    blocks away from every unbounded face refined once around a Gaussian charge."""
+    d = dict(origin=(0.0, 0.0, 0.0), h0=1 / 64, base_blocks=(4, 4, 4), B=16, bc=bc, order=4,
+             smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(d)
+    t = Lay.Tree(dom)
+    for b in sorted(t.nodes[0]):
+        if all(bc[a] == 0 or 1 <= b[a] <= 2 for a in range(3)) and all(1 <= b[a] <= 2 for a in range(3)):
+            t.refine(0, b)
+    lv = t.leaves()
+    Lay.check_layout(dom, lv)
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_charge(x, y, z, sigma=0.07, c=(0.45, 0.5, 0.55)))
+    return d, lv, f
+
+
 def _periodic_adaptive():
     dom = Lay.Domain((0.0, 0.0, 0.0), 1 / 32, (2, 2, 2), 16, (0, 0, 0))
     lv = Lay.corner_nested_leaves(dom, 1)
@@ -64,6 +80,9 @@ def _cfg(name):
         c = C.cfg4(base=4, max_level=1, target=60)
     elif name == "cfg3_64":
         c = C.cfg3(64, coarse_n=16)
+    elif name in ("ppu", "upu", "upp", "pup"):
+        bc = tuple(0 if ch == "p" else 1 for ch in name)
+        return _mixed_adaptive(bc)
     else:
         raise KeyError(name)
     dom, lv, f = C.build(c)
@@ -89,7 +108,8 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3)])
+                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("ppu", 2), ("upu", 2),
+                                         ("upp", 2)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
@@ -204,7 +224,7 @@ def test_op_prolong(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup"])
 def test_op_coarse_solve(name):
     p = _prepared(name)
     c = p.o.levels[0]
