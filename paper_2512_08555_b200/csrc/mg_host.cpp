@@ -133,12 +133,12 @@ struct mg_handle {
   bool canonical = true;  // coarse covered nodes hold the injected fine values (a8)
   double fstar_norm = 0.0;
   // coarse solve
-  int coarse_kind = 0;  // 0 PPP, 1 UUU, 2 PUU
+  int coarse_kind = 0;  // 0 all periodic, 1 all unbounded, 2 any mix (see setup_coarse)
   int P[3] = {0, 0, 0};
   cufftHandle plan_f = 0, plan_b = 0;
   double* d_dense = nullptr;
   void* d_spec = nullptr;
-  double* d_mult = nullptr;  // UUU: full table; PUU: 2D table
+  double* d_mult = nullptr;  // kinds 1, 2: full multiplier table on the R2C spectrum
   // per-stage CUDA-event profiling (non-graph launches only)
   bool prof_on = false;
   struct Ev { cudaEvent_t a, b; int st, lv; };
