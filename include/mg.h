@@ -57,7 +57,7 @@ enum {
   MG_ERR_LAYOUT_2TO1 = -3,       /* 26-neighbour 2:1 constraint violated */
   MG_ERR_UNBOUNDED_REFINED = -4, /* refined block touches an unbounded face */
   MG_ERR_BC = -5,                /* unpaired periodic faces or EVEN/ODD requested */
-  MG_ERR_ORDER = -6,             /* order not in {2,4} */
+  MG_ERR_ORDER = -6,             /* order not in {2,4,6} */
   MG_ERR_STATE = -7,             /* e.g. mg_vcycle before mg_set_rhs */
   MG_ERR_CUDA = -8,              /* CUDA / cuFFT failure or no device */
   MG_ERR_OOM = -9,               /* device allocation failed */
@@ -71,7 +71,9 @@ typedef struct mg_desc {
   int32_t base_blocks[3];    /* level-0 blocks per axis */
   int32_t block_size;        /* B: nodes per block edge; 16 (also 8) */
   int32_t bc[6];             /* per face, MG_BC_* */
-  int32_t order;             /* M = 2 (cross stencil E8) or 4 (Mehrstellen E12) */
+  int32_t order;             /* M = 2 (cross stencil E8), 4 (Mehrstellen E12) or 6 (27-point Mehrstellen
+                                E13 with its radius-2 right-hand side, reading Z24; not with
+                                allow_unbounded_refined: the I = 8 c2f chain leaves the band) */
   int32_t coarse_n;          /* nodes along x of the coarsest MG level (uniform sub-base
                                 coarsening N0/2^j, reading Z5); 0 = AMR level 0 is coarsest */
   int32_t smoother;          /* MG_SMOOTHER_* */

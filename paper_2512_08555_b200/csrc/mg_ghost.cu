@@ -22,9 +22,12 @@ namespace mg {
 namespace {
 
 constexpr int GB_NT = 256;
-constexpr int GB_MAXC = 16 / 2 + 5;                 // coarse extent per axis of a 16-wide box (I <= 6)
-constexpr int GB_SZ_A = 16 * 16 * GB_MAXC;          // >= MAXC^3 (coarse box) and 16*16*MAXC (pass-y output)
-constexpr int GB_SZ_B = 16 * GB_MAXC * GB_MAXC;     // pass-x output
+// coarse extent per axis of a 16-wide box: 7 + I (13 for I = 6, 15 for I = 8)
+template <int I> struct GB {
+  static constexpr int MAXC = 7 + I;
+  static constexpr int SZ_A = 16 * 16 * MAXC;        // >= MAXC^3 (coarse box) and 16*16*MAXC (pass-y output)
+  static constexpr int SZ_B = 16 * MAXC * MAXC;      // pass-x output
+};
 
 __device__ __forceinline__ int fdiv2(int a) { return a >> 1; }  // floor(a / 2) (arithmetic shift)
 
@@ -40,6 +43,9 @@ __device__ __forceinline__ void taps(int J, int c0, int& first, int& n, double* 
     first = fdiv2(J - 1) - I / 2 + 1 - c0;
     if (I == 4) {
       w[0] = -1.0 / 16; w[1] = 9.0 / 16; w[2] = 9.0 / 16; w[3] = -1.0 / 16;
+    } else if (I == 8) {
+      w[0] = -5.0 / 2048; w[1] = 49.0 / 2048; w[2] = -245.0 / 2048; w[3] = 1225.0 / 2048;
+      w[4] = 1225.0 / 2048; w[5] = -245.0 / 2048; w[6] = 49.0 / 2048; w[7] = -5.0 / 2048;
     } else {
       w[0] = 3.0 / 256; w[1] = -25.0 / 256; w[2] = 150.0 / 256;
       w[3] = 150.0 / 256; w[4] = -25.0 / 256; w[5] = 3.0 / 256;
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
     nc[a] = fdiv2(g0[a] + nf[a] - 1) + I / 2 - c0[a] + 1;
   }
   double* Cs = sm;                   // [nc2][nc1][nc0]
-  double* T1 = sm + GB_SZ_A;         // [nc2][nc1][nf0]
+  double* T1 = sm + GB<I>::SZ_A;     // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
   // coarse block / local index along one axis (periodic wrap); -1 outside the block map
   // (no runtime-extent divisions: B is a power of two, periodic wraps are conditional adds)
@@ -170,20 +176,24 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   });
 }
 
-size_t c2f_box_smem() { return sizeof(double) * (size_t)(GB_SZ_A + GB_SZ_B); }
+template <int I>
+size_t c2f_box_smem() { return sizeof(double) * (size_t)(GB<I>::SZ_A + GB<I>::SZ_B); }
 
 void prepare_ghost_kernels() {
-  cudaFuncSetAttribute(k_c2f_box<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem());
-  cudaFuncSetAttribute(k_c2f_box<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem());
+  cudaFuncSetAttribute(k_c2f_box<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem<4>());
+  cudaFuncSetAttribute(k_c2f_box<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem<6>());
+  cudaFuncSetAttribute(k_c2f_box<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem<8>());
 }
 
 void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox,
                     double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
   if (nbox <= 0) return;
   if (I == 4)
-    k_c2f_box<4><<<nbox, GB_NT, c2f_box_smem(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+    k_c2f_box<4><<<nbox, GB_NT, c2f_box_smem<4>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+  else if (I == 6)
+    k_c2f_box<6><<<nbox, GB_NT, c2f_box_smem<6>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
   else
-    k_c2f_box<6><<<nbox, GB_NT, c2f_box_smem(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+    k_c2f_box<8><<<nbox, GB_NT, c2f_box_smem<8>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
   note_launch();
 }
 

@@ -266,7 +266,7 @@ void validate_and_build(mg_handle* h) {
   const mg_desc& d = h->d;
   const int B = d.block_size;
   if (!(B == 16 || B == 8)) throw MgError(MG_ERR_ARG, "block_size must be 8 or 16");
-  if (d.order != 2 && d.order != 4) throw MgError(MG_ERR_ORDER, "order must be 2 or 4");
+  if (d.order != 2 && d.order != 4 && d.order != 6) throw MgError(MG_ERR_ORDER, "order must be 2, 4 or 6");
   if (d.smoother != MG_SMOOTHER_JACOBI && d.smoother != MG_SMOOTHER_RBGS) throw MgError(MG_ERR_ARG, "bad smoother");
   if (d.n_leaf <= 0 || !d.leaves) throw MgError(MG_ERR_ARG, "no leaves");
   if (d.eta1 < 0 || d.eta2 < 0 || !(d.h0 > 0)) throw MgError(MG_ERR_ARG, "bad eta/h0");
@@ -451,7 +451,8 @@ bool is_real_node(const mg_handle* h, const Level& l, int Jx, int Jy, int Jz, in
 
 void build_ghosts(mg_handle* h) {
   const int nlev = (int)h->L.size();
-  const int g = h->smoother == MG_SMOOTHER_RBGS ? 2 : 1;  // halo read by one sweep
+  // halo read by one sweep (RB: 2), and by the radius-2 right-hand side of M = 6
+  const int g = (h->smoother == MG_SMOOTHER_RBGS || h->order == 6) ? 2 : 1;
   for (int m = nlev - 1; m >= 0; --m) {
     Level& l = h->L[m];
     // halo ghosts: nodes within Chebyshev distance g of a real block, not in one

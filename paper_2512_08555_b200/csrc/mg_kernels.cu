@@ -62,7 +62,11 @@ __device__ __forceinline__ double lap_tile(const double* t, int i, double inv_h2
   const double E = (((t[i - 1 - SY] + t[i + 1 - SY]) + (t[i - 1 + SY] + t[i + 1 + SY])) +
                     ((t[i - 1 - SZ] + t[i + 1 - SZ]) + (t[i - 1 + SZ] + t[i + 1 + SZ]))) +
                    ((t[i - SY - SZ] + t[i + SY - SZ]) + (t[i - SY + SZ] + t[i + SY + SZ]));
-  return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+  if (ORDER == 4) return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+  // M = 6 (E13, fig:stencils: centre -128, faces 14, edges 3, corners 1, / 30h^2)
+  const double K = ((t[i - 1 - SY - SZ] + t[i + 1 - SY - SZ]) + (t[i - 1 + SY - SZ] + t[i + 1 + SY - SZ])) +
+                   ((t[i - 1 - SY + SZ] + t[i + 1 - SY + SZ]) + (t[i - 1 + SY + SZ] + t[i + 1 + SY + SZ]));
+  return ((14.0 * F + 3.0 * E + K) - 128.0 * c) * (inv_h2 * (1.0 / 30.0));
 }
 
 template <int ORDER>
@@ -75,7 +79,10 @@ __device__ __forceinline__ double lap_fetch(const double* __restrict__ u, const 
   const double E = (((g(-1, -1, 0) + g(1, -1, 0)) + (g(-1, 1, 0) + g(1, 1, 0))) +
                     ((g(-1, 0, -1) + g(1, 0, -1)) + (g(-1, 0, 1) + g(1, 0, 1)))) +
                    ((g(0, -1, -1) + g(0, 1, -1)) + (g(0, -1, 1) + g(0, 1, 1)));
-  return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+  if (ORDER == 4) return (2.0 * F + E - 24.0 * c) * (inv_h2 * (1.0 / 6.0));
+  const double K = ((g(-1, -1, -1) + g(1, -1, -1)) + (g(-1, 1, -1) + g(1, 1, -1))) +
+                   ((g(-1, -1, 1) + g(1, -1, 1)) + (g(-1, 1, 1) + g(1, 1, 1)));
+  return ((14.0 * F + 3.0 * E + K) - 128.0 * c) * (inv_h2 * (1.0 / 30.0));
 }
 
 // ---------------------------------------------------------------------------------
@@ -404,7 +411,7 @@ static void smooth_inst_v1(const LevelView& L, double omega, double inv_h2, doub
 template <int B, int ORDER, int MODE, bool RES>
 static void smooth_inst(const LevelView& L, double omega, double inv_h2, double inv_d, cudaStream_t s,
                         bool prepare_only = false) {
-  if constexpr (B == 16) {
+  if constexpr (B == 16 && ORDER != 6) {
     constexpr int NT = 256;
     constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
     constexpr int H = NS + (RES ? 1 : 0);
@@ -466,7 +473,7 @@ static void smooth_dispatch_b(const LevelView& L, int mode, double omega, bool r
 template <int ORDER>
 static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res, cudaStream_t s) {
   const double inv_h2 = 1.0 / (L.h * L.h);
-  const double d = (ORDER == 2 ? -6.0 : -4.0) * inv_h2;  // centre coefficient of Δ_h^M
+  const double d = (ORDER == 2 ? -6.0 : (ORDER == 4 ? -4.0 : -128.0 / 30.0)) * inv_h2;  // centre of Δ_h^M
   const double inv_d = 1.0 / d;
   switch (L.B) {
     case 16: smooth_dispatch_b<16, ORDER>(L, mode, omega, res, inv_h2, inv_d, s); break;
@@ -480,19 +487,21 @@ void prepare_kernels() {
   upload_weights();
   prepare_pencil_kernels();
   prepare_ghost_kernels();
-  prepare_b<16, 2>(); prepare_b<16, 4>();
-  prepare_b<8, 2>(); prepare_b<8, 4>();
-  prepare_b<4, 2>(); prepare_b<4, 4>();
+  prepare_b<16, 2>(); prepare_b<16, 4>(); prepare_b<16, 6>();
+  prepare_b<8, 2>(); prepare_b<8, 4>(); prepare_b<8, 6>();
+  prepare_b<4, 2>(); prepare_b<4, 4>(); prepare_b<4, 6>();
 }
 
 void launch_smooth(const LevelView& L, int order, int mode, double omega, bool with_residual, cudaStream_t s) {
   if (order == 2) smooth_dispatch<2>(L, mode, omega, with_residual, s);
-  else smooth_dispatch<4>(L, mode, omega, with_residual, s);
+  else if (order == 4) smooth_dispatch<4>(L, mode, omega, with_residual, s);
+  else smooth_dispatch<6>(L, mode, omega, with_residual, s);
 }
 
 void launch_residual(const LevelView& L, int order, cudaStream_t s) {
   if (order == 2) smooth_dispatch<2>(L, -1, 0.0, true, s);
-  else smooth_dispatch<4>(L, -1, 0.0, true, s);
+  else if (order == 4) smooth_dispatch<4>(L, -1, 0.0, true, s);
+  else smooth_dispatch<6>(L, -1, 0.0, true, s);
 }
 
 // ---------------------------------------------------------------------------------
@@ -674,7 +683,8 @@ __global__ void k_fas_rhs(LevelView F, LevelView C) {
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (!fine.nreal) return;
   if (order == 2) { k_fas_rhs<2><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
-  else { k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else if (order == 4) { k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_fas_rhs<6><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // Prolongation of the correction (Alg. 1): u_f += trilinear(u_c - û_c).
@@ -818,22 +828,39 @@ __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
 void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s) {
   if (!L.nreal) return;
   if (order == 2) { k_norm<2><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
-  else { k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else if (order == 4) { k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else { k_norm<6><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
 }
 
 // R_h^M f on all real nodes into tmp (M=4: f + (1/12)Σδ²f, right side of E12), then
 // f <- tmp on leaf nodes only (reading Z16).
+template <int ORDER>
 __global__ void k_rhs_apply(LevelView L, double* tmp) {
   const int b = blockIdx.x;
   const int B = L.B;
   const int32_t* nb = L.nbr + (size_t)b * 27;
   for (int i = threadIdx.x; i < L.B3; i += blockDim.x) {
     const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    auto g = [&](int a, int bb, int cc) { return fetch(L.f, nb, B, x + a, y + bb, z + cc); };
     const double c = L.f[(size_t)b * L.B3 + i];
-    const double dx = (fetch(L.f, nb, B, x - 1, y, z) - 2.0 * c) + fetch(L.f, nb, B, x + 1, y, z);
-    const double dy = (fetch(L.f, nb, B, x, y - 1, z) - 2.0 * c) + fetch(L.f, nb, B, x, y + 1, z);
-    const double dz = (fetch(L.f, nb, B, x, y, z - 1) - 2.0 * c) + fetch(L.f, nb, B, x, y, z + 1);
-    tmp[(size_t)b * L.B3 + i] = c + ((dx + dy) + dz) / 12.0;
+    // δ² along each axis (dimensionless), at (x,y,z) and, for M = 6, at its neighbours
+    auto d2x = [&](int yo, int zo) { return (g(-1, yo, zo) - 2.0 * g(0, yo, zo)) + g(1, yo, zo); };
+    auto d2y = [&](int xo, int zo) { return (g(xo, -1, zo) - 2.0 * g(xo, 0, zo)) + g(xo, 1, zo); };
+    auto d2z = [&](int xo, int yo) { return (g(xo, yo, -1) - 2.0 * g(xo, yo, 0)) + g(xo, yo, 1); };
+    const double dx = d2x(0, 0), dy = d2y(0, 0), dz = d2z(0, 0);
+    if (ORDER == 4) {
+      tmp[(size_t)b * L.B3 + i] = c + ((dx + dy) + dz) / 12.0;
+    } else {
+      // R_h^6 f = f + (1/12) Σ δ² f + (1/90) Σ_{d<e} δ²_d δ²_e f - (1/240) Σ δ⁴ f (E13, Z24)
+      const double dxy = (d2x(-1, 0) - 2.0 * dx) + d2x(1, 0);
+      const double dyz = (d2y(0, -1) - 2.0 * dy) + d2y(0, 1);
+      const double dzx = (d2z(-1, 0) - 2.0 * dz) + d2z(1, 0);
+      const double dxx = ((g(-2, 0, 0) - 4.0 * g(-1, 0, 0)) + 6.0 * c) + (g(2, 0, 0) - 4.0 * g(1, 0, 0));
+      const double dyy = ((g(0, -2, 0) - 4.0 * g(0, -1, 0)) + 6.0 * c) + (g(0, 2, 0) - 4.0 * g(0, 1, 0));
+      const double dzz = ((g(0, 0, -2) - 4.0 * g(0, 0, -1)) + 6.0 * c) + (g(0, 0, 2) - 4.0 * g(0, 0, 1));
+      tmp[(size_t)b * L.B3 + i] = ((c + ((dx + dy) + dz) / 12.0) + ((dxy + dyz) + dzx) / 90.0) -
+                                  ((dxx + dyy) + dzz) / 240.0;
+    }
   }
 }
 
@@ -850,7 +877,8 @@ __global__ void k_rhs_commit(LevelView L, const double* tmp) {
 
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s) {
   if (!L.nreal || order == 2) return;
-  { k_rhs_apply<<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  if (order == 4) { k_rhs_apply<4><<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  else { k_rhs_apply<6><<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
   { k_rhs_commit<<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
 }
 
@@ -938,6 +966,7 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
 __device__ __forceinline__ double symbol_h2(int order, double sx, double sy, double sz) {
   double s = sx + sy + sz;
   if (order >= 4) s += (sx * sy + sy * sz + sz * sx) * (1.0 / 6.0);
+  if (order == 6) s += sx * sy * sz * (1.0 / 30.0);
   return s;
 }
 

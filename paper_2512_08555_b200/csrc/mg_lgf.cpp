@@ -21,12 +21,15 @@ static double op_symbol(const double* lam, int dim, int order) {
       for (int b = a + 1; b < dim; ++b) p += lam[a] * lam[b];
     s += p / 6.0;
   }
+  if (order == 6 && dim == 3) s += lam[0] * lam[1] * lam[2] / 30.0;  // E13 (reading Z24)
   return s;
 }
 
 // stencil weight of ℒ (dimensionless) at offset with `nz` non-zero components
 static double op_weight(int dim, int order, int nz) {
   if (order == 2) return nz == 0 ? -2.0 * dim : (nz == 1 ? 1.0 : 0.0);
+  if (dim == 3 && order == 6)  // fig:stencils M=6: {-128, 14, 3, 1} / 30
+    return nz == 0 ? -128.0 / 30.0 : (nz == 1 ? 14.0 / 30.0 : (nz == 2 ? 3.0 / 30.0 : 1.0 / 30.0));
   if (dim == 3) return nz == 0 ? -4.0 : (nz == 1 ? 1.0 / 3.0 : (nz == 2 ? 1.0 / 6.0 : 0.0));
   return nz == 0 ? -10.0 / 3.0 : (nz == 1 ? 2.0 / 3.0 : 1.0 / 6.0);   // 2D Mehrstellen
 }

@@ -765,6 +765,7 @@ __global__ void __maxnreg__(80)
 }
 
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
+  if (order == 6) return false;
   if (fine.B != PB || fine.npen <= 0 || fine.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (fine.h * fine.h);
   if (order == 2) k_rr2_pencil<2><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
@@ -823,6 +824,7 @@ void prepare_pencil_kernels() {
 }
 
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s) {
+  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
@@ -835,6 +837,7 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
 }
 
 bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s) {
+  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (L.h * L.h);
   if (order == 2) k_res_pencil<2, RES_D, 1><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
@@ -844,6 +847,7 @@ bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s) {
 }
 
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s) {
+  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (L.h * L.h);
   if (order == 2) k_res_pencil<2, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);

@@ -80,6 +80,13 @@ def _cfg(name):
         c = C.cfg4(base=4, max_level=1, target=60)
     elif name == "cfg3_64":
         c = C.cfg3(64, coarse_n=16)
+    elif name == "cfg2_64_m6":           # 6th-order Mehrstellen (E13)
+        c = C.cfg2(64)
+        c["order"] = 6
+    elif name == "puu1_m6":
+        d, lv, f = _puu_adaptive(1)
+        d["order"] = 6
+        return d, lv, f
     elif name in ("ppu", "upu", "upp", "pup"):
         bc = tuple(0 if ch == "p" else 1 for ch in name)
         return _mixed_adaptive(bc)
@@ -109,7 +116,7 @@ def test_abi_exports_every_declared_symbol():
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
                                          ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("ppu", 2), ("upu", 2),
-                                         ("upp", 2)])
+                                         ("upp", 2), ("cfg2_64_m6", 3), ("puu1_m6", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
@@ -164,7 +171,7 @@ def _prepared(name, warm=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6"])
 def test_op_smooth(name):
     p = _prepared(name)
     for m in range(1, len(p.o.levels)):
@@ -176,7 +183,7 @@ def test_op_smooth(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
 def test_op_residual(name):
     p = _prepared(name)
     for m in range(0, len(p.o.levels)):
@@ -190,7 +197,7 @@ def test_op_residual(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
 def test_op_restrict(name):
     p = _prepared(name)
     for m in range(len(p.o.levels) - 1, 0, -1):
@@ -205,7 +212,7 @@ def test_op_restrict(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
 def test_op_prolong(name):
     p = _prepared(name)
     rng = np.random.default_rng(5)
@@ -224,7 +231,7 @@ def test_op_prolong(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup", "puu1_m6"])
 def test_op_coarse_solve(name):
     p = _prepared(name)
     c = p.o.levels[0]
@@ -244,8 +251,9 @@ def test_op_coarse_solve(name):
 
 
 @pytest.mark.gpu
-def test_set_rhs_fstar_parity():
-    cfg, lv, f = _cfg("puu2")
+@pytest.mark.parametrize("name", ["puu2", "puu1_m6"])
+def test_set_rhs_fstar_parity(name):
+    cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
     for m, L in enumerate(p.o.levels):
         e = rel_err(p.gpu_field("f", m)[L.leaf], L.f[L.leaf]) if L.leaf.any() else 0.0
@@ -253,7 +261,7 @@ def test_set_rhs_fstar_parity():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64"])
+@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6"])
 def test_op_ghost_fill(name):
     """Boundary-ghost fill (a1: f2c injection + c2f, exterior chain U1) of every level:
     GPU ghost-block values vs the oracle's lookup V_m(J) at every halo node (within
