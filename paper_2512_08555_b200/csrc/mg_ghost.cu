@@ -6,8 +6,8 @@
 // midpoint weights on coarse (J_d-1)/2 - I/2 + 1 … (J_d-1)/2 + I/2, I = M + 2.
 //
 // The per-node form costs I^3 = 216 scattered coarse reads for an odd-odd-odd node.
-// Here one CTA handles one ghost box (the bounding box of the needed nodes of one
-// ghost block): it stages the coarse support of the box in shared memory once and
+// Here one CTA handles one ghost box (a box of needed nodes of one ghost block; the
+// host splits every block's needed nodes into disjoint thin boxes): it stages the coarse support of the box in shared memory once and
 // applies the rule separably, x then y then z — the same nesting and summation
 // order as the per-node definition (Σ_z w_z Σ_y w_y Σ_x w_x W), so results are
 // identical to it, with ~3I multiply-adds per node.
@@ -31,59 +31,71 @@ template <int I> struct GB {
 
 __device__ __forceinline__ int fdiv2(int a) { return a >> 1; }  // floor(a / 2) (arithmetic shift)
 
+// 1D rule at fine index J: coarse start relative to the box origin c0; odd -> the
+// I-point midpoint weights, even -> injection (weight 1)
 template <int I>
-__device__ __forceinline__ void taps(int J, int c0, int& first, int& n, double* w) {
-  // 1D rule at fine index J; first = coarse start relative to the box origin c0
-  if ((J & 1) == 0) {
-    n = 1;
-    first = fdiv2(J) - c0;
-    w[0] = 1.0;
+__device__ __forceinline__ bool taps(int J, int c0, int& first) {
+  const bool odd = J & 1;
+  first = odd ? fdiv2(J - 1) - I / 2 + 1 - c0 : fdiv2(J) - c0;
+  return odd;
+}
+
+template <int I>
+__device__ __forceinline__ double wt(int t) {
+  if (I == 4) {
+    constexpr double w[4] = {-1.0 / 16, 9.0 / 16, 9.0 / 16, -1.0 / 16};
+    return w[t];
+  } else if (I == 8) {
+    constexpr double w[8] = {-5.0 / 2048, 49.0 / 2048, -245.0 / 2048, 1225.0 / 2048,
+                             1225.0 / 2048, -245.0 / 2048, 49.0 / 2048, -5.0 / 2048};
+    return w[t];
   } else {
-    n = I;
-    first = fdiv2(J - 1) - I / 2 + 1 - c0;
-    if (I == 4) {
-      w[0] = -1.0 / 16; w[1] = 9.0 / 16; w[2] = 9.0 / 16; w[3] = -1.0 / 16;
-    } else if (I == 8) {
-      w[0] = -5.0 / 2048; w[1] = 49.0 / 2048; w[2] = -245.0 / 2048; w[3] = 1225.0 / 2048;
-      w[4] = 1225.0 / 2048; w[5] = -245.0 / 2048; w[6] = 49.0 / 2048; w[7] = -5.0 / 2048;
-    } else {
-      w[0] = 3.0 / 256; w[1] = -25.0 / 256; w[2] = 150.0 / 256;
-      w[3] = 150.0 / 256; w[4] = -25.0 / 256; w[5] = 3.0 / 256;
-    }
+    constexpr double w[6] = {3.0 / 256, -25.0 / 256, 150.0 / 256, 150.0 / 256, -25.0 / 256, 3.0 / 256};
+    return w[t];
   }
+}
+
+// Σ_t w_t p[t * stride] in tap order (the per-node definition's summation order);
+// an even node is the single coarse value
+template <int I>
+__device__ __forceinline__ double apply_taps(const double* p, int stride, bool odd) {
+  if (!odd) return p[0];
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < I; ++t) s += wt<I>(t) * p[t * stride];
+  return s;
 }
 
 }  // namespace
 
-// box record (12 int32): dst block, lo[3], hi[3] (fine block-local, hi exclusive),
-// org[3] = level-global fine index of the block's node (0,0,0), 2 unused.
+// box record: GBOX_REC int32 (mg_internal.h).
 // Every stage iterates a 3-D index box with the 256 threads laid out as a 16 x 16 tile
 // over its two largest axes and a loop over the smallest one (ghost boxes are thin
 // slabs: 2 x 16 x 16 faces, 2 x 2 x 16 edges), so that the index arithmetic is adds
 // and every thread has work.
 template <typename Fn>
 __device__ __forceinline__ void box_for(const int D[3], Fn&& fn) {
-  int L = 2;  // loop axis: the smallest extent
-  if (D[0] < D[L]) L = 0;
-  if (D[1] < D[L]) L = 1;
-  const int A = L == 0 ? 1 : 0, Bx = L == 2 ? 1 : 2;
   const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
-  if (ta >= D[A] || tb >= D[Bx]) return;
-  int k[3];
-  k[A] = ta;
-  k[Bx] = tb;
-  for (int l = 0; l < D[L]; ++l) {
-    k[L] = l;
-    fn(k[0], k[1], k[2]);
+  if (D[0] <= D[1] && D[0] <= D[2]) {         // loop over x
+    if (ta >= D[1] || tb >= D[2]) return;
+    for (int l = 0; l < D[0]; ++l) fn(l, ta, tb);
+  } else if (D[1] <= D[2]) {                  // loop over y
+    if (ta >= D[0] || tb >= D[2]) return;
+    for (int l = 0; l < D[1]; ++l) fn(ta, l, tb);
+  } else {                                    // loop over z
+    if (ta >= D[0] || tb >= D[1]) return;
+    for (int l = 0; l < D[2]; ++l) fn(ta, tb, l);
   }
 }
 
 template <int I>
 __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ boxes, LevelView F, LevelView C,
                                                    double* __restrict__ ff, const double* __restrict__ cf,
-                                                   bool ext_zero) {
+                                                   bool ext_zero, int t1_off) {
   extern __shared__ double sm[];
-  const int32_t* bx = boxes + 12 * blockIdx.x;
+  __shared__ int s_l[3][GB<I>::MAXC];          // coarse block-local index per axis and tap
+  __shared__ unsigned char s_s[3][GB<I>::MAXC]; // which of the (<= 3) coarse blocks per axis
+  const int32_t* bx = boxes + GBOX_REC * blockIdx.x;
   const int blk = bx[0];
   const int lo[3] = {bx[1], bx[2], bx[3]}, hi[3] = {bx[4], bx[5], bx[6]};
   const int B = F.B;
@@ -96,32 +108,40 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
     nc[a] = fdiv2(g0[a] + nf[a] - 1) + I / 2 - c0[a] + 1;
   }
   double* Cs = sm;                   // [nc2][nc1][nc0]
-  double* T1 = sm + GB<I>::SZ_A;     // [nc2][nc1][nf0]
+  double* T1 = sm + t1_off;           // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
-  // coarse block / local index along one axis (periodic wrap); -1 outside the block map
-  // (no runtime-extent divisions: B is a power of two, periodic wraps are conditional adds)
-  const int bsh = __ffs(C.B) - 1, bmask = C.B - 1;
-  auto cidx = [&](int a, int ci, int& b, int& l) {
-    if (C.per[a]) {
-      while (ci < 0) ci += C.N[a];
-      while (ci >= C.N[a]) ci -= C.N[a];
+  // ---- coarse addressing, once per box: a box's coarse support spans <= 15 taps per
+  // axis, i.e. at most 2 coarse blocks per axis (3 when the coarse level has B/2
+  // blocks); the record carries the coarse block index of every slot combination
+  {
+    const int bsh = __ffs(C.B) - 1, bmask = C.B - 1;
+    const int q = threadIdx.x;
+    if (q < GB<I>::MAXC) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (q >= nc[a]) continue;
+        int ci = c0[a] + q, cf0 = c0[a];
+        if (C.per[a]) {
+          while (ci < 0) ci += C.N[a];
+          while (ci >= C.N[a]) ci -= C.N[a];
+          while (cf0 < 0) cf0 += C.N[a];
+          while (cf0 >= C.N[a]) cf0 -= C.N[a];
+        }
+        int slot = (ci >> bsh) - (cf0 >> bsh);     // 0, 1, 2 along the taps (arithmetic shifts)
+        if (slot < 0) slot += C.N[a] >> bsh;       // periodic wrap
+        s_l[a][q] = ci & bmask;
+        s_s[a][q] = (unsigned char)slot;
+      }
     }
-    l = ci & bmask;
-    b = (ci >> bsh) - C.bmap_lo[a];  // arithmetic shift: floor(ci / B)
-    if (b < 0 || b >= C.bmap_n[a]) b = -1;
-  };
+    __syncthreads();
+  }
   // ---- stage the coarse support (nodes outside the coarse level -> 0, only reached
   // by non-needed nodes of the box)
+  const int CB = C.B;
   box_for(nc, [&](int qx, int qy, int qz) {
-    int b[3], l[3];
-    cidx(0, c0[0] + qx, b[0], l[0]);
-    cidx(1, c0[1] + qy, b[1], l[1]);
-    cidx(2, c0[2] + qz, b[2], l[2]);
+    const int cblk = __ldg(bx + 12 + s_s[0][qx] + 3 * s_s[1][qy] + 9 * s_s[2][qz]);
     double v = 0.0;
-    if (b[0] >= 0 && b[1] >= 0 && b[2] >= 0) {
-      const int cblk = __ldg(C.bmap + ((size_t)b[2] * C.bmap_n[1] + b[1]) * C.bmap_n[0] + b[0]);
-      if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (l[2] * C.B + l[1]) * C.B + l[0]];
-    }
+    if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (s_l[2][qz] * CB + s_l[1][qy]) * CB + s_l[0][qx]];
     Cs[(qz * nc[1] + qy) * nc[0] + qx] = v;
   });
   __syncthreads();
@@ -129,13 +149,9 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   {
     const int D[3] = {nf[0], nc[1], nc[2]};
     box_for(D, [&](int fx, int cy, int cz) {
-      double w[I];
-      int first, n;
-      taps<I>(g0[0] + fx, c0[0], first, n, w);
-      const double* row = Cs + (cz * nc[1] + cy) * nc[0] + first;
-      double sx = 0.0;
-      for (int t = 0; t < n; ++t) sx += w[t] * row[t];
-      T1[(cz * nc[1] + cy) * nf[0] + fx] = sx;
+      int first;
+      const bool odd = taps<I>(g0[0] + fx, c0[0], first);
+      T1[(cz * nc[1] + cy) * nf[0] + fx] = apply_taps<I>(Cs + (cz * nc[1] + cy) * nc[0] + first, 1, odd);
     });
   }
   __syncthreads();
@@ -143,13 +159,9 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   {
     const int D[3] = {nf[0], nf[1], nc[2]};
     box_for(D, [&](int fx, int fy, int cz) {
-      double w[I];
-      int first, n;
-      taps<I>(g0[1] + fy, c0[1], first, n, w);
-      const double* col = T1 + (cz * nc[1] + first) * nf[0] + fx;
-      double sy = 0.0;
-      for (int t = 0; t < n; ++t) sy += w[t] * col[t * nf[0]];
-      T2[(cz * nf[1] + fy) * nf[0] + fx] = sy;
+      int first;
+      const bool odd = taps<I>(g0[1] + fy, c0[1], first);
+      T2[(cz * nf[1] + fy) * nf[0] + fx] = apply_taps<I>(T1 + (cz * nc[1] + first) * nf[0] + fx, nf[0], odd);
     });
   }
   __syncthreads();
@@ -164,13 +176,9 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
     if (ext_zero && ext) {
       v = 0.0;
     } else {
-      double w[I];
-      int first, n;
-      taps<I>(J[2], c0[2], first, n, w);
-      const double* col = T2 + (first * nf[1] + fy) * nf[0] + fx;
-      double sz = 0.0;
-      for (int t = 0; t < n; ++t) sz += w[t] * col[t * nf[0] * nf[1]];
-      v = sz;
+      int first;
+      const bool odd = taps<I>(J[2], c0[2], first);
+      v = apply_taps<I>(T2 + (first * nf[1] + fy) * nf[0] + fx, nf[0] * nf[1], odd);
     }
     dst[((lo[2] + fz) * B + (lo[1] + fy)) * B + (lo[0] + fx)] = v;
   });
@@ -185,15 +193,20 @@ void prepare_ghost_kernels() {
   cudaFuncSetAttribute(k_c2f_box<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c2f_box_smem<8>());
 }
 
-void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox,
-                    double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
+size_t c2f_box_smem_max(int I) {
+  return I == 4 ? c2f_box_smem<4>() : I == 6 ? c2f_box_smem<6>() : c2f_box_smem<8>();
+}
+
+void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, int szA,
+                    int szB, double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
   if (nbox <= 0) return;
+  const size_t smem = sizeof(double) * (size_t)(szA + szB);
   if (I == 4)
-    k_c2f_box<4><<<nbox, GB_NT, c2f_box_smem<4>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+    k_c2f_box<4><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else if (I == 6)
-    k_c2f_box<6><<<nbox, GB_NT, c2f_box_smem<6>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+    k_c2f_box<6><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else
-    k_c2f_box<8><<<nbox, GB_NT, c2f_box_smem<8>(), s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero);
+    k_c2f_box<8><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   note_launch();
 }
 

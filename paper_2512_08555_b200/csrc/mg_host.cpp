@@ -89,6 +89,7 @@ struct Level {
   bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
   // host tables
   std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len, gbox;
+  int gbox_szA = 0, gbox_szB = 0;  // c2f box kernel shared memory (doubles), max over the level's boxes
   std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
   std::vector<uint32_t> nbr_real, nbr_ext;
@@ -606,29 +607,129 @@ void build_ghosts(mg_handle* h) {
   }
 }
 
-// Ghost boxes of levels >= 1: per ghost block, the bounding box of its needed nodes
-// (record: block, lo[3], hi[3] block-local, org[3] level-global index of node (0,0,0),
-// 2 unused).  The c2f kernel (mg_ghost.cu) fills one box per CTA.
+// Ghost boxes of the c2f kernel (mg_ghost.cu): the needed nodes of every ghost block
+// are split into disjoint boxes.  Per axis, the cut points are the planes where the
+// need mask changes anywhere; the mask is constant on every cell of that grid, and the
+// needed cells are merged greedily (x, then y, then z).  For the usual need mask — a
+// union of g-thick halo slabs, one per real neighbour — the boxes are at most g thick
+// along some axis, which bounds the kernel's shared memory (~22 KB for I = 6 instead of
+// ~48 KB for a 16^3 bounding box, i.e. more resident CTAs) and skips the unneeded
+// interior of L-shaped unions.  (MG_GBOX_BBOX=1: one bounding box per ghost block.)
 void build_ghost_boxes(mg_handle* h) {
+  const int I = h->I;
+  const bool bbox = std::getenv("MG_GBOX_BBOX") != nullptr;
   for (size_t m = 1; m < h->L.size(); ++m) {
     Level& l = h->L[m];
+    const Level& C = h->L[m - 1];
     l.gbox.clear();
+    l.gbox_szA = l.gbox_szB = 0;
+    const int B = l.B;
     for (int gi = 0; gi < l.nghost; ++gi) {
-      int lo[3] = {l.B, l.B, l.B}, hi[3] = {0, 0, 0};
-      for (int loc = 0; loc < l.B3; ++loc) {
-        if (!((l.need[gi][loc >> 6] >> (loc & 63)) & 1)) continue;
-        const int q[3] = {loc % l.B, (loc / l.B) % l.B, loc / (l.B * l.B)};
+      std::vector<uint8_t> nd(l.B3);
+      for (int loc = 0; loc < l.B3; ++loc) nd[loc] = (l.need[gi][loc >> 6] >> (loc & 63)) & 1;
+      auto at = [&](int x, int y, int z) -> uint8_t& { return nd[(z * B + y) * B + x]; };
+      auto emit = [&](const int lo[3], const int hi[3]) {
+        const auto c = l.coords[l.nreal + gi];
+        int32_t rec[GBOX_REC] = {l.nreal + gi, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2],
+                                 c[0] * B, c[1] * B, c[2] * B, 0, 0};
+        int nf[3], nc[3], sb[3][3];
         for (int a = 0; a < 3; ++a) {
-          lo[a] = std::min(lo[a], q[a]);
-          hi[a] = std::max(hi[a], q[a] + 1);
+          const int g0 = rec[7 + a] + lo[a];
+          nf[a] = hi[a] - lo[a];
+          const int c0 = fdiv(g0, 2) - I / 2 + 1;
+          nc[a] = fdiv(g0 + nf[a] - 1, 2) - fdiv(g0, 2) + I;
+          // coarse block coordinate of each slot (consecutive blocks met along the taps,
+          // periodic wrap included; -1 outside the coarse block map)
+          for (int k = 0; k < 3; ++k) sb[a][k] = -1;
+          int first = 0;
+          for (int q = 0; q < nc[a]; ++q) {
+            int ci = c0 + q;
+            if (h->per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
+            const int cb = fdiv(ci, C.B);
+            if (q == 0) first = cb;
+            int slot = cb - first;
+            if (slot < 0) slot += C.N[a] / C.B;
+            if (slot > 2) throw MgError(MG_ERR_LAYOUT_GHOST, "ghost box coarse support spans > 3 blocks");
+            const int b = cb - C.bmap_lo[a];
+            sb[a][slot] = (b < 0 || b >= C.bmap_n[a]) ? -1 : b;
+          }
         }
+        for (int k = 0; k < 27; ++k) {
+          const int b0 = sb[0][k % 3], b1 = sb[1][(k / 3) % 3], b2 = sb[2][k / 9];
+          rec[12 + k] = (b0 < 0 || b1 < 0 || b2 < 0)
+                            ? -1
+                            : C.bmap[((size_t)b2 * C.bmap_n[1] + b1) * C.bmap_n[0] + b0];
+        }
+        l.gbox.insert(l.gbox.end(), rec, rec + GBOX_REC);
+        // region A = max(coarse stage, pass-y output), region B = pass-x output
+        l.gbox_szA = std::max(l.gbox_szA, std::max(nc[0] * nc[1] * nc[2], nf[0] * nf[1] * nc[2]));
+        l.gbox_szB = std::max(l.gbox_szB, nf[0] * nc[1] * nc[2]);
+      };
+      if (bbox) {
+        int lo[3] = {B, B, B}, hi[3] = {0, 0, 0};
+        for (int z = 0; z < B; ++z)
+          for (int y = 0; y < B; ++y)
+            for (int x = 0; x < B; ++x)
+              if (at(x, y, z)) {
+                const int q[3] = {x, y, z};
+                for (int a = 0; a < 3; ++a) {
+                  lo[a] = std::min(lo[a], q[a]);
+                  hi[a] = std::max(hi[a], q[a] + 1);
+                }
+              }
+        if (hi[0] > lo[0]) emit(lo, hi);
+        continue;
       }
-      if (hi[0] <= lo[0]) continue;
-      const auto c = l.coords[l.nreal + gi];
-      const int32_t rec[12] = {l.nreal + gi, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2],
-                               c[0] * l.B, c[1] * l.B, c[2] * l.B, 0, 0};
-      l.gbox.insert(l.gbox.end(), rec, rec + 12);
+      // cut points per axis
+      std::vector<int> cut[3];
+      for (int a = 0; a < 3; ++a) {
+        cut[a].push_back(0);
+        for (int k = 1; k < B; ++k) {
+          bool diff = false;
+          for (int i = 0; i < B && !diff; ++i)
+            for (int j = 0; j < B && !diff; ++j) {
+              const int p[3][3] = {{k, i, j}, {i, k, j}, {i, j, k}};
+              const int q[3][3] = {{k - 1, i, j}, {i, k - 1, j}, {i, j, k - 1}};
+              diff = at(p[a][0], p[a][1], p[a][2]) != at(q[a][0], q[a][1], q[a][2]);
+            }
+          if (diff) cut[a].push_back(k);
+        }
+        cut[a].push_back(B);
+      }
+      const int n0 = (int)cut[0].size() - 1, n1 = (int)cut[1].size() - 1, n2 = (int)cut[2].size() - 1;
+      std::vector<uint8_t> cell(n0 * n1 * n2);  // 1 = needed and not yet in a box
+      for (int z = 0; z < n2; ++z)
+        for (int y = 0; y < n1; ++y)
+          for (int x = 0; x < n0; ++x) cell[(z * n1 + y) * n0 + x] = at(cut[0][x], cut[1][y], cut[2][z]);
+      auto fr = [&](int x, int y, int z) -> uint8_t& { return cell[(z * n1 + y) * n0 + x]; };
+      for (int z = 0; z < n2; ++z)
+        for (int y = 0; y < n1; ++y)
+          for (int x = 0; x < n0; ++x) {
+            if (!fr(x, y, z)) continue;
+            int x1 = x, y1 = y, z1 = z;
+            while (x1 + 1 < n0 && fr(x1 + 1, y, z)) ++x1;
+            for (bool ok = true; ok && y1 + 1 < n1;) {
+              for (int xx = x; xx <= x1; ++xx) ok = ok && fr(xx, y1 + 1, z);
+              if (ok) ++y1;
+            }
+            for (bool ok = true; ok && z1 + 1 < n2;) {
+              for (int yy = y; yy <= y1; ++yy)
+                for (int xx = x; xx <= x1; ++xx) ok = ok && fr(xx, yy, z1 + 1);
+              if (ok) ++z1;
+            }
+            for (int zz = z; zz <= z1; ++zz)
+              for (int yy = y; yy <= y1; ++yy)
+                for (int xx = x; xx <= x1; ++xx) fr(xx, yy, zz) = 0;
+            const int lo[3] = {cut[0][x], cut[1][y], cut[2][z]};
+            const int hi[3] = {cut[0][x1 + 1], cut[1][y1 + 1], cut[2][z1 + 1]};
+            emit(lo, hi);
+          }
     }
+    if (std::getenv("MG_GBOX_STATS"))
+      std::fprintf(stderr, "gbox level %zu: %d ghost blocks, %zu boxes, smem %d+%d doubles\n", m, l.nghost,
+                   l.gbox.size() / GBOX_REC, l.gbox_szA, l.gbox_szB);
+    if (sizeof(double) * (size_t)(l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
+      throw MgError(MG_ERR_LAYOUT_GHOST, "ghost box exceeds the c2f kernel's shared memory");
   }
 }
 
@@ -861,7 +962,8 @@ void refresh(mg_handle* h, int m) {
     Level& F = h->L[j];
     if (F.gbox.empty()) continue;
     LevelView fv = view(h, j), cv = view(h, j - 1);
-    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / 12, F.u[F.cur], cv.u, h->I, false, h->s);
+    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.u[F.cur], cv.u, h->I, false,
+                   h->s);
   }
 }
 
@@ -1052,7 +1154,8 @@ double residual_abs(mg_handle* h) {
   for (int m = 0; m < (int)h->L.size(); ++m) {
     refresh(h, m);
     Prof pr(h, ST_NORM, m);
-    launch_norm(view(h, m), h->order, true, h->d_norm, h->s);
+    const LevelView v = view(h, m);
+    if (!launch_norm_pencil(v, h->order, h->d_norm, h->s)) launch_norm(v, h->order, true, h->d_norm, h->s);
   }
   return read_norm(h);
 }
@@ -1093,7 +1196,8 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     Level& F = h->L[m];
     if (F.gbox.empty()) continue;
     LevelView fv = view(h, m), cv = view(h, m - 1);
-    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / 12, F.f, h->L[m - 1].f, h->I, true, h->s);
+    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
+                   h->s);
   }
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];

@@ -64,6 +64,7 @@ void launch_smooth(const LevelView& L, int order, int mode, double omega, bool w
 void launch_residual(const LevelView& L, int order, cudaStream_t s);
 // z-marching pencil kernels (B = 16 levels); return false if the level is not eligible
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s);
+bool launch_norm_pencil(const LevelView& L, int order, unsigned long long* out, cudaStream_t s);
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
 // FAS right-hand side f = r + Δu on the covered nodes of a coarse level (B = 16)
 bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s);
@@ -73,8 +74,14 @@ void prepare_pencil_kernels();
 void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
                 const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 // separable box c2f (mg_ghost.cu): boxes = [nbox][12] int32 records (see mg_host.cpp)
-void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox,
-                    double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
+// c2f ghost-box record (int32): dst block, lo[3], hi[3] (fine block-local, hi exclusive),
+// org[3] (level-global fine index of the block's node (0,0,0)), 2 unused, then the
+// coarse block index of each of the 3 x 3 x 3 block slots the box's taps meet
+// (slot sx + 3 sy + 9 sz; -1 = none), 1 unused
+constexpr int GBOX_REC = 40;
+size_t c2f_box_smem_max(int I);
+void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, int szA,
+                    int szB, double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void prepare_ghost_kernels();
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s);

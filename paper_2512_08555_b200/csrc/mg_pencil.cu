@@ -338,8 +338,12 @@ struct ResShape {
 // MODE 0: r = f - Δ_h^M u (residual, Alg. 1) on every node of the pencil.
 // MODE 1: f = r + Δ_h^M u (FAS right-hand side on the coarse level, Alg. 1) on
 //         the nodes of octants covered by the finer level (covmask); others untouched.
+// MODE 2: max |f - Δ_h^M u| over the nodes of uncovered octants (the composite residual
+//         norm of the stopping test) as the bit pattern of a non-negative double
+//         (NaN -> quiet-NaN pattern, above +Inf), atomicMax-ed into *out; nothing written.
 template <int ORDER, int D, int MODE = 0>
-__global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, double inv_h2) {
+__global__ void __launch_bounds__(ResShape<D>::NT, 4)
+    k_res_pencil(LevelView L, double inv_h2, unsigned long long* out = nullptr) {
   using S = ResShape<D>;
   constexpr int T = S::T, TP = S::TP, FP = S::FP, R = S::R, NT = S::NT;
   extern __shared__ __align__(16) double sm[];
@@ -351,9 +355,10 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
   const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
   for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
   __shared__ uint8_t scov[PMAXL];
-  if (MODE == 1 && tid < len) scov[tid] = __ldg(L.covmask + __ldg(pb + tid));
+  if (MODE != 0 && tid < len) scov[tid] = __ldg(L.covmask + __ldg(pb + tid));
   const int nz = PB * len;
-  const double* __restrict__ fin = MODE == 0 ? L.f : L.r;  // the right-hand operand staged per plane
+  const double* __restrict__ fin = MODE == 1 ? L.r : L.f;  // the right-hand operand staged per plane
+  unsigned long long nmax = 0ull;                            // MODE 2
 
   int ld_xy[2], ld_sxy[2], ld_dst[2];
   bool ld_on[2], ld_f[2];
@@ -430,11 +435,34 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4) k_res_pencil(LevelView L, 
         L.r[o] = f - Lu;
       } else {
         const int oct = (cx >= PB / 2) | ((cy >= PB / 2) << 1) | (((r & 15) >= PB / 2) << 2);
-        if ((scov[r >> 4] >> oct) & 1) L.f[o] = f + Lu;
+        const bool cov = (scov[r >> 4] >> oct) & 1;
+        if (MODE == 1) {
+          if (cov) L.f[o] = f + Lu;
+        } else if (!cov) {
+          const double v = fabs(f - Lu);
+          unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+          if (v != v) bits = 0x7ff8000000000000ull;
+          nmax = bits > nmax ? bits : nmax;
+        }
       }
     }
   }
   cpa_wait<0>();
+  if (MODE == 2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, nmax, o);
+      nmax = t > nmax ? t : nmax;
+    }
+    __shared__ unsigned long long sred[NT / 32];
+    if ((tid & 31) == 0) sred[tid >> 5] = nmax;
+    __syncthreads();
+    if (tid == 0) {
+      unsigned long long m = 0ull;
+      for (int w = 0; w < NT / 32; ++w) m = sred[w] > m ? sred[w] : m;
+      atomicMax(out, m);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------
@@ -818,6 +846,8 @@ void prepare_pencil_kernels() {
   setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
   setup((const void*)k_rr2_pencil<4>, RR2Shape::SMEM);
   setup((const void*)k_res_pencil<2, RES_D, 1>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<2, RES_D, 2>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D, 2>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D>, ResShape<RES_D>::SMEM);
@@ -852,6 +882,16 @@ bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s) {
   const double inv_h2 = 1.0 / (L.h * L.h);
   if (order == 2) k_res_pencil<2, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
   else k_res_pencil<4, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
+  note_launch();
+  return true;
+}
+
+bool launch_norm_pencil(const LevelView& L, int order, unsigned long long* out, cudaStream_t s) {
+  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
+  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  if (order == 2) k_res_pencil<2, RES_D, 2><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, out);
+  else k_res_pencil<4, RES_D, 2><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, out);
   note_launch();
   return true;
 }
