@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 
 #include "mg_internal.h"
@@ -138,7 +139,6 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   // and at the pencil ends; between them they advance by one plane (PB^2 doubles).
   const double* ip[NLD];
   const double* fp = nullptr;
-  int zi = zlo - 2;
   auto seek_issue = [&](int z) {
     int k, dz, zl;
     const int len = *cx.glen;  // pencil geometry from shared memory (rare path: spare registers)
@@ -150,10 +150,13 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
                                : L.u + (size_t)snb[k * 27 + cx.ld_sxy[d] + 9 * (dz + 1)] * PB3 + o + cx.ld_xy[d];
     fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
   };
-  auto issue = [&]() {
-    if (zi < zhi + 2) {
-      if ((zi & 15) == 0) seek_issue(zi);
-      const int slot = (zi + 2) % R;  // zi >= -2
+  // stage plane z (called for z = zlo-2, zlo-1, … in order) into ring slot (z+2) & (R-1).
+  // In the step loop z = 4 (zq + t) + j + D - 2 with j, D compile-time, so the slot and
+  // the block-boundary test fold to constants (zlo ≡ 0 mod 4).
+  auto issue = [&](int z, auto checked) {
+    if (!decltype(checked)::value || z < zhi + 2) {
+      if ((z & 15) == 0) seek_issue(z);
+      const int slot = (z + 2) & (R - 1);
       double* dst = su + slot * TP;
 #pragma unroll
       for (int d = 0; d < NLD; ++d) {
@@ -161,11 +164,10 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
         cpa16(dst + cx.ld_dst[d], ip[d]);
         ip[d] += PB * PB;
       }
-      if (valid && zi >= zlo - 1 && zi <= zhi) cpa16(sfme + slot * NT, fp);
+      if (valid && (!decltype(checked)::value || (z >= zlo - 1 && z <= zhi))) cpa16(sfme + slot * NT, fp);
       fp += PB * PB;
     }
     cpa_commit();
-    ++zi;
   };
   bool live = false;  // red-phase liveness of this pair's columns at plane r
   auto seek_live = [&](int z) {
@@ -177,7 +179,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   seek_issue(zlo - 2);
   seek_live(zlo - 1);
 #pragma unroll
-  for (int q = 0; q < D; ++q) issue();
+  for (int q = 0; q < D; ++q) issue(zlo - 2 + q, std::true_type{});
 
   // Per-column accumulators (column q = a, b).  With α(z) = 2c(z) + S4(z),
   // β(z) = 2S4(z) + D4(z) - 24c(z), γ(z) = 2n(z) + S4(z) (n = value after the red
@@ -194,18 +196,27 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   double2 fr = make_double2(0.0, 0.0);  // f pair at the plane of the last red phase
   double fb = 0.0;                      // f of the column black at plane s-2
 
-  for (int s0 = zlo - 2; s0 < zhi + 2; s0 += 4) {
+  // output offset of this pair at the black plane b = s-2 (advanced by one plane per
+  // step, re-seeked at block starts)
+  int ooff = snb[(zlo >> 4) * 27 + 13] * PB3 + ((zlo & 15) - 4) * (PB * PB) + fxy;
+  // One group = 4 steps s = base-2 … base+1 (base a multiple of 4, so ring slots and
+  // block-boundary tests are compile-time).  The first group holds the pipeline start:
+  // red from its third step on, no black; later groups run both.  Only the last group
+  // stages planes past the pencil end (bounds-checked issue); elsewhere the staging
+  // pointers advance unconditionally.
+  auto group = [&](const int base, auto mode) {
+    constexpr bool FIRST = decltype(mode)::value == 0, LAST = decltype(mode)::value == 2;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int s = s0 + j;
-      const int X = (j & 1) ? PC : 1 - PC;  // red at s-1 (black at s and s-2); s0 even
+      const int s = base - 2 + j;
+      const int X = (j & 1) ? PC : 1 - PC;  // red at s-1 (black at s and s-2); base even
       const int O = 1 - X;                  // red at s (and s-2)
       cpa_wait<D - 1>();
       __syncthreads();
-      issue();
+      issue(s + D, std::integral_constant<bool, LAST>{});
       double cq[2], s4q[2], d4q[2];
       {
-        const double* U = su + ((s + 2) % R) * TP + i0;
+        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
         const double2 m = *reinterpret_cast<const double2*>(U - TW);
         const double2 cc = *reinterpret_cast<const double2*>(U);
         const double2 p = *reinterpret_cast<const double2*>(U + TW);
@@ -226,10 +237,10 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       const double nx = X ? shfl_dn1(nl[0]) : shfl_up1(nl[1]);
       // column X: black at plane s
       const double alpha = ORDER == 4 ? 2.0 * cq[X] + s4q[X] : cq[X];
-      if (s >= zlo) {  // red half-sweep at plane r = s-1 in [zlo-1, zhi] (column X)
+      if (!FIRST || j >= 2) {  // red half-sweep at plane r = s-1 in [zlo-1, zhi] (column X)
         if (((s - 1) & 15) == 0) seek_live(s - 1);
         fb = X ? fr.y : fr.x;                 // f at plane s-2 of column X (pair read last step)
-        fr = sfme[((s + 1) % R) * NT];  // f pair at plane s-1
+        fr = sfme[((s + 1) & (R - 1)) * NT];  // f pair at plane s-1
         double v = cR[X];
         if (live) {
           const double Lu = ORDER == 4 ? (accR[X] + alpha) * h6 : (accR[X] + alpha) * inv_h2;
@@ -237,17 +248,22 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
         }
         if (valid) snme[(j & 1) * SNP] = v;  // new-plane slot = parity of s
         const double g = ORDER == 4 ? 2.0 * v + s4r[X] : v;  // γ(s-1) of column X
-        if (s >= zlo + 2 && inner) {  // black half-sweep at plane b = s-2 (column X)
-          const double* N = snme + ((j & 1) ^ 1) * SNP;  // rows cy±1 hold the red node at x of X
-          const double S4n = (nl[O] + nx) + (N[-SNW] + N[SNW]);
-          const double Lu = ORDER == 4 ? (accB[X] + 2.0 * S4n + g) * h6 : (accB[X] + S4n + g) * inv_h2;
-          const double vb = cB[X] + wd * (fb - Lu);
-          double* op = L.u_out + (size_t)snb[((s - 2) >> 4) * 27 + 13] * PB3 + ((s - 2) & 15) * (PB * PB) + fxy;
-          *reinterpret_cast<double2*>(op) = X ? make_double2(nl[O], vb) : make_double2(vb, nl[O]);
+        if (!FIRST) {
+          const int b = s - 2;
+          if ((b & 15) == 0) ooff = snb[(b >> 4) * 27 + 13] * PB3 + fxy;
+          if (inner) {  // black half-sweep at plane b (column X)
+            const double* N = snme + ((j & 1) ^ 1) * SNP;  // rows cy±1 hold the red node at x of X
+            const double S4n = (nl[O] + nx) + (N[-SNW] + N[SNW]);
+            const double Lu = ORDER == 4 ? (accB[X] + 2.0 * S4n + g) * h6 : (accB[X] + S4n + g) * inv_h2;
+            const double vb = cB[X] + wd * (fb - Lu);
+            *reinterpret_cast<double2*>(L.u_out + (size_t)ooff) =
+                X ? make_double2(nl[O], vb) : make_double2(vb, nl[O]);
+          }
         }
         accB[X] = (ORDER == 4 ? d4q[X] - 24.0 * cq[X] : -6.0 * cq[X]) + g;
         nl[X] = v;
       }
+      ooff += PB * PB;
       cB[X] = cq[X];
       accR[X] = alpha;  // α(s): first term of the red node at s+1
       // column O: red at plane s
@@ -255,7 +271,11 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       cR[O] = cq[O];
       s4r[O] = s4q[O];
     }
-  }
+  };
+  const int zq = zlo >> 2, nt = (zhi - zlo + 4) >> 2;
+  group(4 * zq, std::integral_constant<int, 0>{});
+  for (int t = 1; t < nt - 1; ++t) group(4 * (zq + t), std::integral_constant<int, 1>{});
+  group(4 * (zq + nt - 1), std::integral_constant<int, 2>{});
   cpa_wait<0>();
 }
 
