@@ -708,7 +708,6 @@ __global__ void __maxnreg__(80)
 
   const double* ip = nullptr;
   const double* fp = nullptr;
-  int zi = -2;
   auto seek_issue = [&](int z) {
     int k, dz, zl;
     plane_src(z, nz, len, k, dz, zl);
@@ -716,17 +715,17 @@ __global__ void __maxnreg__(80)
     ip = ld_sxy < 0 ? nullptr : L.u + (size_t)snb[k * 27 + ld_sxy + 9 * (dz + 1)] * PB3 + o + ld_xy;
     fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
   };
-  auto issue = [&]() {
-    if (zi < nz + 2) {
-      if ((zi & 15) == 0) seek_issue(zi);
-      const int slot = (zi + 2) & (R - 1);
+  // stage plane z (called for z = -2, -1, … in order) into ring slot (z+2) & (R-1)
+  auto issue = [&](int z, auto checked) {
+    if (!decltype(checked)::value || z < nz + 2) {
+      if ((z & 15) == 0) seek_issue(z);
+      const int slot = (z + 2) & (R - 1);
       if (ld_sxy >= 0) cpa16(su + slot * TP + ld_dst, ip);
       ip += PB * PB;
-      if (valid && zi >= -1 && zi <= nz) cpa16(sfme + slot * NR, fp);
+      if (valid && (!decltype(checked)::value || (z >= -1 && z <= nz))) cpa16(sfme + slot * NR, fp);
       fp += PB * PB;
     }
     cpa_commit();
-    ++zi;
   };
   bool live = false;
   auto seek_live = [&](int z) {
@@ -737,78 +736,91 @@ __global__ void __maxnreg__(80)
   seek_issue(-2);
   seek_live(-1);
 #pragma unroll
-  for (int q = 0; q < D; ++q) issue();
+  for (int q = 0; q < D; ++q) issue(-2 + q, std::true_type{});
 
   double aA[2] = {0, 0}, aP[2] = {0, 0};  // per column: α(s-1); α(s-2) + β(s-1)
   double t0 = 0, t1 = 0, t2 = 0;          // coarse threads: T at planes s-2, s-3, s-4
   const double h6 = ORDER == 4 ? inv_h2 * (1.0 / 6.0) : inv_h2;
-  for (int s = -2; s <= nz + 2; ++s) {
-    cpa_wait<D - 1>();
-    __syncthreads();
-    issue();
-    if (rthr) {
-      // plane s (shuffles: every lane of warps 0-5 takes part)
-      const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
-      const double2 m = *reinterpret_cast<const double2*>(U - TW);
-      const double2 cc = *reinterpret_cast<const double2*>(U);
-      const double2 p = *reinterpret_cast<const double2*>(U + TW);
-      const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
-      double cq[2] = {cc.x, cc.y};
-      double s4q[2] = {(l + cc.y) + (m.x + p.x), (cc.x + r) + (m.y + p.y)};
-      double d4q[2] = {0, 0};
-      if (ORDER == 4) {
-        const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
-        d4q[0] = (ml + m.y) + (pl + p.y);
-        d4q[1] = (m.x + mr) + (p.x + pr);
-      }
-      if (s >= 0 && s <= nz + 1) {  // residual at plane s-1 in [-1, nz]
-        if (((s - 1) & 15) == 0) seek_live(s - 1);
-        const double2 fq = sfme[((s + 1) & (R - 1)) * NR];
-        double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
-        if (live) {
-          const double al0 = ORDER == 4 ? 2.0 * cq[0] + s4q[0] : cq[0];
-          const double al1 = ORDER == 4 ? 2.0 * cq[1] + s4q[1] : cq[1];
-          rr.x = fq.x - (aP[0] + al0) * h6;
-          rr.y = fq.y - (aP[1] + al1) * h6;
-        }
-        if (valid) *reinterpret_cast<double2*>(sr + ((s - 1) & 1) * RRP + (ry + 1) * RRW + (x0 + 2)) = rr;
-      }
+  // Steps s = -2 … nz+1 (the last coarse node, fine plane nz-2, needs residual planes
+  // up to nz-1) in groups of 4, s = base-2+j with base a multiple of 4: ring slots,
+  // plane parities and block-boundary tests are compile-time; only the first and last
+  // groups test the pencil ends.
+  auto group = [&](const int base, auto mode) {
+    constexpr bool EDGE = decltype(mode)::value != 1, LAST = decltype(mode)::value == 2;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const double al = ORDER == 4 ? 2.0 * cq[q] + s4q[q] : cq[q];
-        const double be = ORDER == 4 ? 2.0 * s4q[q] + d4q[q] - 24.0 * cq[q] : s4q[q] - 6.0 * cq[q];
-        aP[q] = aA[q] + be;  // α(s-1) + β(s): the node at s, completed at step s+1
-        aA[q] = al;
-      }
-    } else if (cthr) {
-      // coarse u = fine u(2i) at even interior planes (E7)
-      if (s >= 0 && s < nz && (s & 1) == 0) {
-        const int k = s >> 4, qz = (s & 15) >> 1;
-        const int* pr = spar + 4 * k;
-        C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] =
-            su[((s + 2) & (R - 1)) * TP + (2 * qy + 2) * TW + (2 * qx + 2)];
-      }
-      // full weighting of the residual plane s-2 (written last step): x, then y, then z
-      if (s - 2 >= -1 && s - 2 <= nz) {
-        const double* rp = sr + ((s - 2) & 1) * RRP + (2 * qy + 1) * RRW + (2 * qx + 2);
-        double sy = 0.0;
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) {
-          const double* row = rp + dy * RRW;
-          const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
-          sy += (dy == 0 ? 0.5 : 0.25) * sx;
+    for (int j = 0; j < 4; ++j) {
+      const int s = base - 2 + j;
+      cpa_wait<D - 1>();
+      __syncthreads();
+      issue(s + D, std::integral_constant<bool, LAST>{});
+      if (rthr) {
+        // plane s (shuffles: every lane of warps 0-5 takes part)
+        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+        const double2 m = *reinterpret_cast<const double2*>(U - TW);
+        const double2 cc = *reinterpret_cast<const double2*>(U);
+        const double2 p = *reinterpret_cast<const double2*>(U + TW);
+        const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
+        double cq[2] = {cc.x, cc.y};
+        double s4q[2] = {(l + cc.y) + (m.x + p.x), (cc.x + r) + (m.y + p.y)};
+        double d4q[2] = {0, 0};
+        if (ORDER == 4) {
+          const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
+          d4q[0] = (ml + m.y) + (pl + p.y);
+          d4q[1] = (m.x + mr) + (p.x + pr);
         }
-        t2 = t1; t1 = t0; t0 = sy;
-        const int zc = s - 3;
-        if (zc >= 0 && zc < nz && (zc & 1) == 0) {
-          const double sz = (0.25 * t2 + 0.5 * t1) + 0.25 * t0;
-          const int k = zc >> 4, qz = (zc & 15) >> 1;
+        if (!EDGE || s >= 0) {  // residual at plane s-1 in [-1, nz]
+          if (((s - 1) & 15) == 0) seek_live(s - 1);
+          const double2 fq = sfme[((s + 1) & (R - 1)) * NR];
+          double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
+          if (live) {
+            const double al0 = ORDER == 4 ? 2.0 * cq[0] + s4q[0] : cq[0];
+            const double al1 = ORDER == 4 ? 2.0 * cq[1] + s4q[1] : cq[1];
+            rr.x = fq.x - (aP[0] + al0) * h6;
+            rr.y = fq.y - (aP[1] + al1) * h6;
+          }
+          if (valid) *reinterpret_cast<double2*>(sr + ((s - 1) & 1) * RRP + (ry + 1) * RRW + (x0 + 2)) = rr;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double al = ORDER == 4 ? 2.0 * cq[q] + s4q[q] : cq[q];
+          const double be = ORDER == 4 ? 2.0 * s4q[q] + d4q[q] - 24.0 * cq[q] : s4q[q] - 6.0 * cq[q];
+          aP[q] = aA[q] + be;  // α(s-1) + β(s): the node at s, completed at step s+1
+          aA[q] = al;
+        }
+      } else if (cthr) {
+        // coarse u = fine u(2i) at even interior planes (E7)
+        if ((j & 1) == 0 && (!EDGE || (s >= 0 && s < nz))) {
+          const int k = s >> 4, qz = (s & 15) >> 1;
           const int* pr = spar + 4 * k;
-          C.r[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] = sz;
+          C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] =
+              su[((s + 2) & (R - 1)) * TP + (2 * qy + 2) * TW + (2 * qx + 2)];
+        }
+        // full weighting of the residual plane s-2 (written last step): x, then y, then z
+        if (!EDGE || s >= 1) {
+          const double* rp = sr + ((s - 2) & 1) * RRP + (2 * qy + 1) * RRW + (2 * qx + 2);
+          double sy = 0.0;
+#pragma unroll
+          for (int dy = -1; dy <= 1; ++dy) {
+            const double* row = rp + dy * RRW;
+            const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
+            sy += (dy == 0 ? 0.5 : 0.25) * sx;
+          }
+          t2 = t1; t1 = t0; t0 = sy;
+          const int zc = s - 3;  // even when j is odd
+          if ((j & 1) == 1 && zc >= 0 && zc < nz) {
+            const double sz = (0.25 * t2 + 0.5 * t1) + 0.25 * t0;
+            const int k = zc >> 4, qz = (zc & 15) >> 1;
+            const int* pr = spar + 4 * k;
+            C.r[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] = sz;
+          }
         }
       }
     }
-  }
+  };
+  const int nt = (nz + 4) >> 2;
+  group(0, std::integral_constant<int, 0>{});
+  for (int t = 1; t < nt - 1; ++t) group(4 * t, std::integral_constant<int, 1>{});
+  group(4 * (nt - 1), std::integral_constant<int, 2>{});
   cpa_wait<0>();
 }
 
