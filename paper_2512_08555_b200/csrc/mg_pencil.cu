@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
 #pragma unroll
   for (int q = 0; q < D; ++q) issue(-1 + q);
 
-  double c0 = 0, c1 = 0, c2 = 0, a0 = 0, a1 = 0, a2 = 0;
+  double c0 = 0, c1 = 0, c2 = 0, a0 = 0, a1 = 0, a2 = 0, d0 = 0, d1 = 0, d2 = 0;
   const double h6 = inv_h2 * (1.0 / 6.0);
   for (int s = -1; s < nz + 1; ++s) {
     cpa_wait<D - 1>();
@@ -431,10 +431,12 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
     issue(s + D);
     c2 = c1; c1 = c0;
     a2 = a1; a1 = a0;
+    d2 = d1; d1 = d0;
     {
       const double* U = su + ((s + 1) % R) * TP + ci;
       c0 = U[0];
       a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
+      if (ORDER == 6) d0 = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
     }
     if (s >= 1) {
       const int r = s - 1;
@@ -443,12 +445,18 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
       double Lu;
       if (ORDER == 2) {
         Lu = ((a1 + (c2 + c0)) - 6.0 * c1) * inv_h2;
-      } else {
+      } else if (ORDER == 4) {
         const double* U = su + sl * TP + ci;
         const double Dg = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
         const double F = a1 + (c2 + c0);
         const double E = Dg + (a2 + a0);
         Lu = (2.0 * F + E - 24.0 * c1) * h6;
+      } else {
+        // M = 6 (E13, fig:stencils): (14 faces + 3 edges + corners - 128 c) / (30 h^2)
+        const double F = a1 + (c2 + c0);
+        const double E = d1 + (a2 + a0);
+        const double K = d2 + d0;
+        Lu = ((14.0 * F + 3.0 * E) + K - 128.0 * c1) * (inv_h2 * (1.0 / 30.0));
       }
       const size_t o = (size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid;
       if (MODE == 0) {
@@ -740,7 +748,15 @@ __global__ void __maxnreg__(80)
 
   double aA[2] = {0, 0}, aP[2] = {0, 0};  // per column: α(s-1); α(s-2) + β(s-1)
   double t0 = 0, t1 = 0, t2 = 0;          // coarse threads: T at planes s-2, s-3, s-4
-  const double h6 = ORDER == 4 ? inv_h2 * (1.0 / 6.0) : inv_h2;
+  const double h6 = ORDER == 4 ? inv_h2 * (1.0 / 6.0) : ORDER == 6 ? inv_h2 * (1.0 / 30.0) : inv_h2;
+  // per column: α = 2c + S4, β = 2S4 + D4 - 24c (M = 4, times 6h^2); α = 14c + 3S4 + D4,
+  // β = 14S4 + 3D4 - 128c (M = 6, times 30h^2; the corners enter through D4 in α)
+  auto alpha_of = [&](double c, double s4, double d4) {
+    return ORDER == 4 ? 2.0 * c + s4 : ORDER == 6 ? (14.0 * c + 3.0 * s4) + d4 : c;
+  };
+  auto beta_of = [&](double c, double s4, double d4) {
+    return ORDER == 4 ? 2.0 * s4 + d4 - 24.0 * c : ORDER == 6 ? (14.0 * s4 + 3.0 * d4) - 128.0 * c : s4 - 6.0 * c;
+  };
   // Steps s = -2 … nz+1 (the last coarse node, fine plane nz-2, needs residual planes
   // up to nz-1) in groups of 4, s = base-2+j with base a multiple of 4: ring slots,
   // plane parities and block-boundary tests are compile-time; only the first and last
@@ -763,7 +779,7 @@ __global__ void __maxnreg__(80)
         double cq[2] = {cc.x, cc.y};
         double s4q[2] = {(l + cc.y) + (m.x + p.x), (cc.x + r) + (m.y + p.y)};
         double d4q[2] = {0, 0};
-        if (ORDER == 4) {
+        if (ORDER >= 4) {
           const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
           d4q[0] = (ml + m.y) + (pl + p.y);
           d4q[1] = (m.x + mr) + (p.x + pr);
@@ -773,19 +789,15 @@ __global__ void __maxnreg__(80)
           const double2 fq = sfme[((s + 1) & (R - 1)) * NR];
           double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
           if (live) {
-            const double al0 = ORDER == 4 ? 2.0 * cq[0] + s4q[0] : cq[0];
-            const double al1 = ORDER == 4 ? 2.0 * cq[1] + s4q[1] : cq[1];
-            rr.x = fq.x - (aP[0] + al0) * h6;
-            rr.y = fq.y - (aP[1] + al1) * h6;
+            rr.x = fq.x - (aP[0] + alpha_of(cq[0], s4q[0], d4q[0])) * h6;
+            rr.y = fq.y - (aP[1] + alpha_of(cq[1], s4q[1], d4q[1])) * h6;
           }
           if (valid) *reinterpret_cast<double2*>(sr + ((s - 1) & 1) * RRP + (ry + 1) * RRW + (x0 + 2)) = rr;
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const double al = ORDER == 4 ? 2.0 * cq[q] + s4q[q] : cq[q];
-          const double be = ORDER == 4 ? 2.0 * s4q[q] + d4q[q] - 24.0 * cq[q] : s4q[q] - 6.0 * cq[q];
-          aP[q] = aA[q] + be;  // α(s-1) + β(s): the node at s, completed at step s+1
-          aA[q] = al;
+          aP[q] = aA[q] + beta_of(cq[q], s4q[q], d4q[q]);  // α(s-1) + β(s): the node at s, completed at step s+1
+          aA[q] = alpha_of(cq[q], s4q[q], d4q[q]);
         }
       } else if (cthr) {
         // coarse u = fine u(2i) at even interior planes (E7)
@@ -825,11 +837,11 @@ __global__ void __maxnreg__(80)
 }
 
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
-  if (order == 6) return false;
   if (fine.B != PB || fine.npen <= 0 || fine.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (fine.h * fine.h);
   if (order == 2) k_rr2_pencil<2><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
-  else k_rr2_pencil<4><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else if (order == 4) k_rr2_pencil<4><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else k_rr2_pencil<6><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
   note_launch();
   return true;
 }
@@ -877,12 +889,30 @@ void prepare_pencil_kernels() {
   setup((const void*)v.k4s, v.smem);
   setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
   setup((const void*)k_rr2_pencil<4>, RR2Shape::SMEM);
+  setup((const void*)k_rr2_pencil<6>, RR2Shape::SMEM);
+  setup((const void*)k_res_pencil<2, RES_D, 0>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<2, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<2, RES_D, 2>, ResShape<RES_D>::SMEM);
-  setup((const void*)k_res_pencil<4, RES_D, 2>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D, 0>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<4, RES_D, 1>, ResShape<RES_D>::SMEM);
-  setup((const void*)k_res_pencil<2, RES_D>, ResShape<RES_D>::SMEM);
-  setup((const void*)k_res_pencil<4, RES_D>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D, 2>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<6, RES_D, 0>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<6, RES_D, 1>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<6, RES_D, 2>, ResShape<RES_D>::SMEM);
+}
+
+// residual-type pencil launch (MODE 0 residual, 1 FAS right-hand side, 2 norm)
+template <int MODE>
+static bool res_pencil_launch(const LevelView& L, int order, unsigned long long* out, cudaStream_t s) {
+  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  constexpr int NT = ResShape<RES_D>::NT;
+  constexpr size_t SM = ResShape<RES_D>::SMEM;
+  if (order == 2) k_res_pencil<2, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
+  else if (order == 4) k_res_pencil<4, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
+  else k_res_pencil<6, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
+  note_launch();
+  return true;
 }
 
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s) {
@@ -899,33 +929,13 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
 }
 
 bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s) {
-  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
-  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
-  const double inv_h2 = 1.0 / (L.h * L.h);
-  if (order == 2) k_res_pencil<2, RES_D, 1><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
-  else k_res_pencil<4, RES_D, 1><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
-  note_launch();
-  return true;
+  return res_pencil_launch<1>(L, order, nullptr, s);
 }
 
-bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s) {
-  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
-  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
-  const double inv_h2 = 1.0 / (L.h * L.h);
-  if (order == 2) k_res_pencil<2, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
-  else k_res_pencil<4, RES_D><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2);
-  note_launch();
-  return true;
-}
+bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s) { return res_pencil_launch<0>(L, order, nullptr, s); }
 
 bool launch_norm_pencil(const LevelView& L, int order, unsigned long long* out, cudaStream_t s) {
-  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
-  if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
-  const double inv_h2 = 1.0 / (L.h * L.h);
-  if (order == 2) k_res_pencil<2, RES_D, 2><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, out);
-  else k_res_pencil<4, RES_D, 2><<<L.npen, ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, out);
-  note_launch();
-  return true;
+  return res_pencil_launch<2>(L, order, out, s);
 }
 
 }  // namespace mg

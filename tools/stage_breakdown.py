@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Per-level, per-stage CUDA-event breakdown of a V-cycle (non-graph launches).
 
-  python tools/stage_breakdown.py [--cfg cfg2] [--cycles 5]
+  python tools/stage_breakdown.py [--cfg cfg2|cfg2_m6|…] [--cycles 5]
 """
 from __future__ import annotations
 
@@ -23,7 +23,10 @@ def main():
 
     from paper_2512_08555_b200 import Solver
     from workloads import configs as C
-    cfg = getattr(C, a.cfg)()
+    name = a.cfg[:-3] if a.cfg.endswith("_m6") else a.cfg
+    cfg = getattr(C, name)()
+    if a.cfg.endswith("_m6"):  # the 6th-order variant
+        cfg = dict(cfg, order=6, name=a.cfg)
     dom, leaves, f = C.build(cfg)
     S = Solver(cfg, leaves)
     S.set_rhs(torch.from_numpy(f).cuda())
