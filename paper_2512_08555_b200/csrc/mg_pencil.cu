@@ -32,6 +32,8 @@ namespace {
 constexpr int PB = 16;             // block edge
 constexpr int PB3 = PB * PB * PB;
 constexpr int PMAXL = 16;          // longest pencil (blocks)
+constexpr int D6 = 2;              // M = 6 sweep: planes staged ahead
+constexpr int RB6_NREG = 96;       // M = 6 sweep register cap
 
 __device__ __forceinline__ int reg16(int x) { return x < 0 ? -1 : (x >= PB ? 1 : 0); }
 
@@ -338,6 +340,248 @@ __global__ void __maxnreg__(NREG)
   const int w = tid >> 5, lane = tid & 31;
   if (w < 3) rb_body<ORDER, D, RR, 0, SW>(L, cx, w, lane, omega, inv_h2, inv_d);
   else rb_body<ORDER, D, RR, 1, SW>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
+}
+
+// ---------------------------------------------------------------------------------
+// Red-black sweep, M = 6 (27-point LHS, E13 / fig:stencils): same tile, pair threads
+// and partial-sum scheme as the M = 2/4 sweep, but the black update also reads the
+// new red values at its 8 corners (planes b±1, rows y±1), which other warps compute
+// one step after the red plane is staged; the black half-sweep therefore runs three
+// planes behind the loads instead of two:
+//   step s: load plane s | red at s-1 | γ of the red column at s-2 | black at s-3.
+// With (times 30 h^2)  α = 14c + 3 S4 + D4,  β = 14 S4 + 3 D4 - 128 c  (old values),
+//   γ(z) = 14 n(z) + 3 S4(z) + D4n(z)  (n, D4n: new red values; S4: old black faces):
+//   red node at r:   α(r-1) + β(r) + α(r+1)
+//   black node at b: -128 c(b) + 3 D4(b) + 14 S4n(b) + γ(b-1) + γ(b+1).
+// Steps run in groups of 8 (base ≡ 0 mod 8), so the plane rings (u: 4 planes, red
+// values: 4, f: 8 — the black update reads f three planes back) have compile-time
+// slots; the last group takes one extra step (black at the last plane).
+// ---------------------------------------------------------------------------------
+struct RB6Shape {
+  static constexpr int T = PB + 4, TW = 26, TP = T * TW;
+  static constexpr int R = 4, FR = 8;
+  static constexpr int NT = 192;
+  static constexpr int NPAIR = T * T / 2, NLD = (NPAIR + NT - 1) / NT;
+  static constexpr int SNW = 13, SNP = 18 * SNW, SNR = 4;
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + SNR * SNP + FR * NT * 2);
+};
+
+template <int RP, bool SW>
+__device__ __forceinline__ void rb6_body(const LevelView& L, const RBCtx& cx, int wg, int lane, double omega,
+                                         double inv_h2, double inv_d) {
+  using S = RB6Shape;
+  constexpr int TW = S::TW, TP = S::TP, R = S::R, FR = S::FR, NT = S::NT, NLD = S::NLD, SNW = S::SNW,
+                SNP = S::SNP;
+  constexpr int PC = RP;  // column red at even planes
+  const int* snb = cx.snb;
+  const int zlo = SW ? cx.z0 : 0, zhi = SW ? cx.z0 + cx.nz : PB * cx.len;  // zlo ≡ 0 (mod 8)
+  double* su = cx.su;
+  const int tid = threadIdx.x;
+  double2* sfme = cx.sf + tid;
+  const bool valid = lane < 30;
+  const int ri = valid ? 3 * wg + lane / 10 : 3 * wg + 2;
+  const int pi = valid ? lane % 10 : 9;
+  const int cy = 2 * ri - RP, x0 = 2 * pi - 2;
+  const int i0 = (cy + 2) * TW + (x0 + 2);
+  double* snme = cx.sn + (cy + 1) * SNW + pi;
+  const int dxc = reg16(x0), dyc = reg16(cy);
+  const int sxy = (dxc + 1) + 3 * (dyc + 1);
+  const int fxy = (cy - PB * dyc) * PB + (x0 - PB * dxc);
+  const bool inner = valid && dxc == 0 && dyc == 0;
+
+  const double* ip[NLD];
+  const double* fp = nullptr;
+  auto seek_issue = [&](int z) {
+    int k, dz, zl;
+    const int len = *cx.glen;
+    plane_src(z, PB * len, len, k, dz, zl);
+    const int o = zl * (PB * PB);
+#pragma unroll
+    for (int d = 0; d < NLD; ++d)
+      ip[d] = cx.ld_sxy[d] < 0 ? nullptr
+                               : L.u + (size_t)snb[k * 27 + cx.ld_sxy[d] + 9 * (dz + 1)] * PB3 + o + cx.ld_xy[d];
+    fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
+  };
+  auto issue = [&](int z, auto checked) {
+    if (!decltype(checked)::value || z < zhi + 2) {
+      if ((z & 15) == 0) seek_issue(z);
+      double* dst = su + ((z + 2) & (R - 1)) * TP;
+#pragma unroll
+      for (int d = 0; d < NLD; ++d) {
+        if (cx.ld_sxy[d] < 0) continue;
+        cpa16(dst + cx.ld_dst[d], ip[d]);
+        ip[d] += PB * PB;
+      }
+      if (valid && (!decltype(checked)::value || (z >= zlo - 1 && z <= zhi)))
+        cpa16(sfme + ((z + 2) & (FR - 1)) * NT, fp);
+      fp += PB * PB;
+    }
+    cpa_commit();
+  };
+  bool live = false;
+  auto seek_live = [&](int z) {
+    int k, dz, zl;
+    const int len = *cx.glen;
+    plane_src(z, PB * len, len, k, dz, zl);
+    live = valid && ((cx.sreal[k] >> (sxy + 9 * (dz + 1))) & 1u);
+  };
+  seek_issue(zlo - 2);
+  seek_live(zlo - 1);
+#pragma unroll
+  for (int q = 0; q < D6; ++q) issue(zlo - 2 + q, std::true_type{});
+
+  double accR[2] = {0, 0}, cR[2] = {0, 0};  // red plane in flight: α(r-1) + β(r), c(r)
+  double s4r[2] = {0, 0};                   // S4 (old) at the column's last red plane
+  double nv[2] = {0, 0};                    // the column's last new red value
+  double accB[2][2] = {{0, 0}, {0, 0}};     // black planes in flight (slot (b >> 1) & 1)
+  double cB[2][2] = {{0, 0}, {0, 0}};
+  const double h30 = inv_h2 * (1.0 / 30.0);
+  const double wd = omega * inv_d;
+  // output offset of this pair at plane b = s-3 (one plane per step, re-seeked at block starts)
+  int ooff = snb[(zlo >> 4) * 27 + 13] * PB3 + ((zlo & 15) - 5) * (PB * PB) + fxy;
+
+  auto group = [&](const int base, auto mode) {
+    constexpr int MODE = decltype(mode)::value;
+    constexpr bool FIRST = MODE == 0, LAST = MODE == 2;
+    constexpr int NSTEP = LAST ? 5 : 8;
+#pragma unroll
+    for (int j = 0; j < NSTEP; ++j) {
+      const int s = base - 2 + j;
+      const int X = (j & 1) ? PC : 1 - PC;  // black at s, red at s-1
+      const int O = 1 - X;                  // red at s and s-2, black at s-1 and s-3
+      const bool plane = !LAST || j <= 3;   // plane s exists (s <= zhi+1)
+      cpa_wait<D6 - 1>();
+      __syncthreads();
+      issue(s + D6, std::integral_constant<bool, LAST>{});
+      double cq[2] = {0, 0}, s4q[2] = {0, 0}, d4q[2] = {0, 0};
+      if (plane) {
+        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+        const double2 m = *reinterpret_cast<const double2*>(U - TW);
+        const double2 cc = *reinterpret_cast<const double2*>(U);
+        const double2 p = *reinterpret_cast<const double2*>(U + TW);
+        const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
+        const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
+        cq[0] = cc.x;
+        cq[1] = cc.y;
+        s4q[0] = (l + cc.y) + (m.x + p.x);
+        s4q[1] = (cc.x + r) + (m.y + p.y);
+        d4q[0] = (ml + m.y) + (pl + p.y);
+        d4q[1] = (m.x + mr) + (p.x + pr);
+      }
+      // γ of column O at its red plane s-2 (red values of plane s-2 written last step)
+      double gam;
+      {
+        const double* Nz = snme + ((s - 2) & 3) * SNP;
+        const double wv = Nz[-SNW] + Nz[SNW];               // rows y±1 at x_O ± 1: own pair …
+        const double wn = O == 0 ? shfl_up1(wv) : shfl_dn1(wv);  // … and the adjacent pair
+        gam = (14.0 * nv[O] + 3.0 * s4r[O]) + (wv + wn);
+      }
+      // black half-sweep at plane b = s-3 (column O): S4n from the own pair's red column,
+      // the adjacent lane's, and rows y±1 of the red plane b
+      {
+        const double nxn = O == 0 ? shfl_up1(nv[X]) : shfl_dn1(nv[X]);
+        const int b = s - 3;
+        if (!FIRST || j >= 5) {
+          if ((b & 15) == 0) ooff = snb[(b >> 4) * 27 + 13] * PB3 + fxy;
+          if (inner) {
+            const double* Nb = snme + (b & 3) * SNP;
+            const int sl = (b >> 1) & 1;
+            const double S4n = (nv[X] + nxn) + (Nb[-SNW] + Nb[SNW]);
+            const double Lu = ((accB[O][sl] + gam) + 14.0 * S4n) * h30;
+            const double2 fb2 = sfme[((b + 2) & (FR - 1)) * NT];
+            const double vb = cB[O][sl] + wd * ((O ? fb2.y : fb2.x) - Lu);
+            *reinterpret_cast<double2*>(L.u_out + (size_t)ooff) =
+                O ? make_double2(nv[X], vb) : make_double2(vb, nv[X]);
+          }
+        }
+        ooff += PB * PB;
+      }
+      accB[O][((s - 1) >> 1) & 1] += gam;  // γ(b-1) of O's black plane b = s-1
+      // red half-sweep at plane r = s-1 (column X)
+      if ((!FIRST || j >= 2) && plane) {
+        if (((s - 1) & 15) == 0) seek_live(s - 1);
+        const double2 fr = sfme[((s + 1) & (FR - 1)) * NT];
+        const double alpha = (14.0 * cq[X] + 3.0 * s4q[X]) + d4q[X];
+        double v = cR[X];
+        if (live) {
+          const double Lu = (accR[X] + alpha) * h30;
+          v = cR[X] + wd * ((X ? fr.y : fr.x) - Lu);
+        }
+        if (valid) snme[((s - 1) & 3) * SNP] = v;
+        nv[X] = v;
+      }
+      if (plane) {
+        // column X black at s: start its black partial sum
+        accB[X][(s >> 1) & 1] = 3.0 * d4q[X] - 128.0 * cq[X];
+        cB[X][(s >> 1) & 1] = cq[X];
+        accR[X] = (14.0 * cq[X] + 3.0 * s4q[X]) + d4q[X];  // α(s): first term of X's red plane s+1
+        // column O red at s
+        accR[O] += (14.0 * s4q[O] + 3.0 * d4q[O]) - 128.0 * cq[O];
+        cR[O] = cq[O];
+        s4r[O] = s4q[O];
+      }
+    }
+  };
+  // bases written as 8 * (…) so that the compiler sees base ≡ 0 (mod 8)
+  const int zq = zlo >> 3, zr = zhi >> 3;
+  group(8 * zq, std::integral_constant<int, 0>{});
+  for (int t = zq + 1; t < zr; ++t) group(8 * t, std::integral_constant<int, 1>{});
+  group(8 * zr, std::integral_constant<int, 2>{});
+  cpa_wait<0>();
+}
+
+template <int NREG, bool SW>
+__global__ void __maxnreg__(NREG) k_rb6_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
+  using S = RB6Shape;
+  constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int snb[PMAXL * 27];
+  __shared__ uint32_t sreal[PMAXL];
+  __shared__ int slen;
+  const int tid = threadIdx.x;
+  RBCtx cx;
+  cx.len = __ldg((SW ? L.sw_pen_len : L.pen_len) + blockIdx.x);
+  cx.nzb = PB * cx.len;
+  if (SW) {
+    const int zr = __ldg(L.sw_pen_z + blockIdx.x);
+    cx.z0 = zr & 0xff;
+    cx.nz = zr >> 8;
+  } else {
+    cx.z0 = 0;
+    cx.nz = cx.nzb;
+  }
+  cx.snb = snb;
+  cx.sreal = sreal;
+  cx.glen = &slen;
+  if (tid == 0) slen = cx.len;
+  cx.su = sm;
+  cx.sn = sm + R * TP;
+  cx.sf = reinterpret_cast<double2*>(sm + R * TP + S::SNR * S::SNP);
+  const int32_t* pb = SW ? L.sw_pen_blk + (size_t)blockIdx.x * L.sw_pen_lmax
+                         : L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  for (int i = tid; i < cx.len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  if (tid < cx.len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
+#pragma unroll
+  for (int d = 0; d < NLD; ++d) {
+    const int j = tid + d * NT;
+    int py, px;
+    if (j < 8 * T) {
+      py = j / 8;
+      px = 2 + 2 * (j % 8);
+    } else {
+      const int hh = j - 8 * T;
+      py = hh / 2;
+      px = (hh & 1) ? PB + 2 : 0;
+    }
+    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
+    cx.ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
+    cx.ld_sxy[d] = j < NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
+    cx.ld_dst[d] = py * TW + px;
+  }
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  if (w < 3) rb6_body<0, SW>(L, cx, w, lane, omega, inv_h2, inv_d);
+  else rb6_body<1, SW>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
 }
 
 // ---------------------------------------------------------------------------------
@@ -887,6 +1131,8 @@ void prepare_pencil_kernels() {
   setup((const void*)v.k4, v.smem);
   setup((const void*)v.k2s, v.smem);
   setup((const void*)v.k4s, v.smem);
+  setup((const void*)k_rb6_pencil<RB6_NREG, false>, RB6Shape::SMEM);
+  setup((const void*)k_rb6_pencil<RB6_NREG, true>, RB6Shape::SMEM);
   setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
   setup((const void*)k_rr2_pencil<4>, RR2Shape::SMEM);
   setup((const void*)k_rr2_pencil<6>, RR2Shape::SMEM);
@@ -916,8 +1162,15 @@ static bool res_pencil_launch(const LevelView& L, int order, unsigned long long*
 }
 
 bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s) {
-  if (order == 6) return false;  // M = 6 runs on the generic 27-point kernels
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  if (order == 6) {
+    const double inv_h2 = 1.0 / (L.h * L.h);
+    const double inv_d = 1.0 / ((-128.0 / 30.0) * inv_h2);
+    if (L.sw_npen > 0) k_rb6_pencil<RB6_NREG, true><<<L.sw_npen, 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
+    else k_rb6_pencil<RB6_NREG, false><<<L.npen, 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
+    note_launch();
+    return true;
+  }
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
   const RBVar& v = rb_pick();

@@ -148,6 +148,41 @@ def test_cfg2_fullsize_closed_form_and_sampled_ops():
 
 
 @pytest.mark.gpu
+def test_cfg2_m6_fullsize_closed_form_and_sampled_ops():
+    """cfg2 with the sixth-order scheme (E13, fig:stencils): the M = 6
+    pencil sweep (lag-3 black half-sweep) at full size against node-by-node oracle
+    values, convergence, and the per-mode exact discrete solution of the M = 6 pair
+    (LHS symbol over RHS symbol)."""
+    cfg = dict(C.cfg2(), order=6, name="cfg2_m6")
+    dom, leaves, f = C.build(cfg)
+    s = _solver(cfg, leaves, f)
+    rng = np.random.default_rng(6)
+    s.vcycle(2)
+    w, used = _sweep_check(cfg, leaves, f, s, rng)
+    assert used > 200 and w < OP_TOL, (w, used)
+    cyc, rel, ok = s.solve(cfg["tol"], 15)
+    assert ok and cyc <= 12 and rel <= cfg["tol"]
+    N = 256
+    k, a, phi = S.fourier_modes(2)
+    J = np.arange(N) / N
+    uh = np.zeros((N, N, N))
+    for kk, aa, pp in zip(k, a, phi):
+        c = [np.cos(2 * np.pi * kd / N) for kd in kk]
+        sd = [2 * cd - 2 for cd in c]
+        lhs = (-128 + 28 * sum(c) + 12 * (c[0] * c[1] + c[1] * c[2] + c[2] * c[0]) + 8 * c[0] * c[1] * c[2]) / 30
+        rho = (1 + sum(sd) / 12 + (sd[0] * sd[1] + sd[1] * sd[2] + sd[2] * sd[0]) / 90
+               - sum(x * x for x in sd) / 240)
+        uh += aa * rho / (lhs * N * N) * np.cos(2 * np.pi * (kk[0] * J[:, None, None] + kk[1] * J[None, :, None]
+                                                             + kk[2] * J[None, None, :]) + pp)
+    ub = S.dense_to_blocks(dom, leaves, uh)
+    u = s.get_solution().cpu().numpy()
+    err = np.abs((u - u.mean()) - (ub - ub.mean())).max() / np.abs(ub).max()
+    assert err < 1e-8, err
+    r, fmax, used = _sampled_residual(cfg, leaves, f, u, rng)
+    assert used > 300 and r <= cfg["tol"] * fmax * 1.5, (r, fmax)
+
+
+@pytest.mark.gpu
 def test_cfg1_fullsize_closed_form():
     cfg = C.cfg1()
     dom, leaves, f = C.build(cfg)
