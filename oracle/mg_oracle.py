@@ -40,8 +40,9 @@ from . import lgf as LGF
 
 PERIODIC, UNBOUNDED = 0, 1
 JACOBI, RBGS = 0, 1
-E = 6          # pad width of extended arrays
-GE = 5         # exterior band width computed by the coarse solve (reading Z21/U1)
+E = 8          # pad width of extended arrays (even; > the widest exterior band)
+GE = 5         # exterior band width computed by the coarse solve (reading Z21/U1), M <= 4
+GE6 = 7        # M = 6: the I = 8 c2f chain of U1 reaches 6 nodes beyond the faces (Z6/U1)
 
 
 # ----------------------------------------------------------------------------------
@@ -142,6 +143,7 @@ class Oracle:
     def __init__(self, desc, leaves):
         self.order = int(desc["order"])
         self.I = self.order + 2                       # interpolation order M+2
+        self.GE = GE6 if self.order == 6 else GE      # exterior band of the coarse solve
         self.w_c2f = lagrange_midpoint_weights(self.I)
         self.smoother = int(desc["smoother"])
         self.omega = float(desc["omega"])
@@ -415,7 +417,7 @@ class Oracle:
         if len(self.unb) == 0:
             self.coarse_kind = "PPP"
             return
-        shape = [N[ax] if self.per[ax] else LGF.pad_size(N[ax], GE) for ax in range(3)]
+        shape = [N[ax] if self.per[ax] else LGF.pad_size(N[ax], self.GE) for ax in range(3)]
         self.coarse_shape = shape
         th = [2 * np.pi * np.fft.fftfreq(s) for s in shape]
         TH = np.meshgrid(*th, indexing="ij")
@@ -480,6 +482,7 @@ class Oracle:
         U = np.fft.ifftn(np.fft.fftn(Fp) * self.coarse_mult).real
         c.u = U[:N[0], :N[1], :N[2]].copy()
         # exterior band: outputs at J in [-GE, N+GE) along unbounded axes
+        GEb = self.GE
         band = np.full(tuple(c.N + 2 * E), np.nan)
         idx = []
         for ax in range(3):
@@ -487,7 +490,7 @@ class Oracle:
                 idx.append(np.arange(-E, N[ax] + E) % N[ax])
             else:
                 J = np.arange(-E, N[ax] + E)
-                ok = (J >= -GE) & (J < N[ax] + GE)
+                ok = (J >= -GEb) & (J < N[ax] + GEb)
                 idx.append(np.where(ok, J % shape[ax], -1))
         sub = U[np.ix_(*[np.where(i < 0, 0, i) for i in idx])]
         valid = np.ones(band.shape, dtype=bool)

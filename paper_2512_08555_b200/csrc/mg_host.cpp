@@ -31,7 +31,9 @@ using namespace mg;
 
 namespace {
 
-constexpr int GE = 5;  // exterior band width produced by the coarse solve (reading Z21/U1)
+// exterior band width produced by the coarse solve (reading Z21/U1): 5 nodes, or 7 for
+// M = 6 under U1 (the I = 8 c2f chain reaches 6 nodes beyond the unbounded faces)
+constexpr int GE_M4 = 5, GE_M6U1 = 7;
 
 struct MgError : std::runtime_error {
   int code;
@@ -118,7 +120,7 @@ struct Level {
 struct mg_handle {
   mg_desc d{};
   int per[3] = {1, 1, 1};
-  int order = 4, I = 6, smoother = 1, eta1 = 2, eta2 = 2;
+  int order = 4, I = 6, GE = 5, smoother = 1, eta1 = 2, eta2 = 2;
   double omega = 1.0;
   int nsub = 0;
   std::vector<Level> L;
@@ -280,6 +282,7 @@ void validate_and_build(mg_handle* h) {
   }
   h->order = d.order;
   h->I = d.order + 2;
+  h->GE = (d.order == 6 && d.allow_unbounded_refined) ? GE_M6U1 : GE_M4;
   h->smoother = d.smoother;
   h->omega = d.omega;
   h->eta1 = d.eta1;
@@ -502,7 +505,7 @@ void build_ghosts(mg_handle* h) {
         if (ext && m > 0) l.ext_chain = true;
         if (m == 0) {
           for (int a = 0; a < 3; ++a)
-            if (!h->per[a] && (J[a] < -GE || J[a] >= l.N[a] + GE))
+            if (!h->per[a] && (J[a] < -h->GE || J[a] >= l.N[a] + h->GE))
               throw MgError(MG_ERR_LAYOUT_GHOST, "exterior ghost beyond the coarse-solve band");
         }
         l.c2f_dst.push_back((l.nreal + gi) * l.B3 + loc);
@@ -858,7 +861,7 @@ void setup_coarse(mg_handle* h) {
   Level& c = h->L[0];
   int nunb = 0;
   for (int a = 0; a < 3; ++a) {
-    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * c.N[a] + 2 * GE - 1);
+    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * c.N[a] + 2 * h->GE - 1);
     nunb += !h->per[a];
   }
   // 0: all periodic (spectral, zero mode -> 0); 1: all unbounded (3D LGF table);

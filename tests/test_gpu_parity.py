@@ -83,6 +83,9 @@ def _cfg(name):
     elif name == "cfg2_64_m6":           # 6th-order Mehrstellen (E13)
         c = C.cfg2(64)
         c["order"] = 6
+    elif name == "cfg3_64_m6":           # M = 6 under U1 (exterior band GE = 7)
+        c = C.cfg3(64, coarse_n=16)
+        c["order"] = 6
     elif name == "puu1_m6":
         d, lv, f = _puu_adaptive(1)
         d["order"] = 6
@@ -115,7 +118,7 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("ppu", 2), ("upu", 2),
+                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("ppu", 2), ("upu", 2),
                                          ("upp", 2), ("cfg2_64_m6", 3), ("puu1_m6", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
@@ -171,7 +174,7 @@ def _prepared(name, warm=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6", "cfg3_64_m6"])
 def test_op_smooth(name):
     p = _prepared(name)
     for m in range(1, len(p.o.levels)):
@@ -183,7 +186,7 @@ def test_op_smooth(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6"])
 def test_op_residual(name):
     p = _prepared(name)
     for m in range(0, len(p.o.levels)):
@@ -197,7 +200,7 @@ def test_op_residual(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6"])
 def test_op_restrict(name):
     p = _prepared(name)
     for m in range(len(p.o.levels) - 1, 0, -1):
@@ -212,7 +215,7 @@ def test_op_restrict(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6"])
 def test_op_prolong(name):
     p = _prepared(name)
     rng = np.random.default_rng(5)
@@ -261,7 +264,7 @@ def test_set_rhs_fstar_parity(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6"])
+@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6", "cfg3_64_m6"])
 def test_op_ghost_fill(name):
     """Boundary-ghost fill (a1: f2c injection + c2f, exterior chain U1) of every level:
     GPU ghost-block values vs the oracle's lookup V_m(J) at every halo node (within
