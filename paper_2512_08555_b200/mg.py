@@ -176,6 +176,25 @@ class Solver:
                                            C.byref(v)))
         return c.value, v.value, rc == MG_OK
 
+    def solve_vector(self, f_components, tol, max_cycles=50, criterion=MG_CRIT_RESIDUAL):
+        """Vector Poisson problem, one scalar solve per component on this handle (the
+        Biot–Savart law ∇²u = -∇×ω of P:627-631: layout, tables, LGF multipliers and
+        CUDA graphs are shared by the components).  f_components: sequence of
+        leaf-ordered device tensors; returns ([u_c], [(cycles, rel, converged)]).
+        A zero component is solved exactly by u = 0 without cycling."""
+        import torch
+        us, stats = [], []
+        for f in f_components:
+            if not bool(torch.any(f != 0)):
+                us.append(torch.zeros_like(f))
+                stats.append((0, 0.0, True))
+                continue
+            self.set_rhs(f)
+            self.set_solution(torch.zeros_like(f))
+            stats.append(self.solve(tol, max_cycles, criterion))
+            us.append(self.get_solution())
+        return us, stats
+
     def run_host(self, f_host: np.ndarray, u_host: np.ndarray, ncycles: int) -> float:
         r = C.c_double()
         self._check(self.lib.mg_run_host(self.h, C.c_void_p(f_host.ctypes.data), C.c_void_p(u_host.ctypes.data),

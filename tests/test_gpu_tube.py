@@ -1,0 +1,42 @@
+"""Vortex-tube vector solve on the GPU: parity of each
+velocity component with the oracle on a small adaptive layout, and the full-size
+adaptive tube against the paper's closed-form velocity (E32–E33)."""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import Pair, rel_err
+from workloads import configs as C
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [4, 6])
+def test_tube_small_parity(order):
+    cfg = C.tube(base=4, max_level=1, nz_blocks=1, target=60, order=order)
+    dom, lv, f3, u3 = C.build_vector(cfg)
+    for comp in (0, 1):
+        p = Pair(cfg, lv, f3[comp])
+        for _ in range(3):
+            p.o.vcycle(1)
+            p.g.vcycle(1)
+        assert rel_err(p.solution(), p.o.get_solution()) < 1e-9
+
+
+@pytest.mark.gpu
+def test_tube_fullsize_vector_solve_vs_analytic():
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    cfg = C.tube()
+    dom, lv, f3, u3 = C.build_vector(cfg)
+    s = Solver(cfg, lv)
+    s.use_graph(True)
+    us, stats = s.solve_vector([torch.from_numpy(f).cuda() for f in f3], cfg["tol"], 30)
+    assert all(ok for _, _, ok in stats), stats
+    assert stats[2][0] == 0 and float(us[2].abs().max()) == 0.0        # f_z = 0 -> u_z = 0
+    for comp in (0, 1):
+        u = us[comp].cpu().numpy()
+        err = np.abs(u - u3[comp]).max()
+        # discretisation error of the 2-level grid (h = 1/256 in the tube, 1/128
+        # outside): 1.66e-6 on the B200 and in the oracle on the same x-y layout; a
+        # wrong sign, component or scaling is O(1)
+        assert err < 4e-6, (comp, err)

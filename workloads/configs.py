@@ -71,7 +71,32 @@ def cfg5(base=8, max_level=4, target=30000):
                 target_leaves=target, cycles=0, tol=1e-10)
 
 
-CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+def tube(base=8, max_level=1, target=1400, nz_blocks=None, order=4, R=0.25):
+    """Biot–Savart vortex tube (E29–E33): unit cube, x and y
+    unbounded, z periodic, tube of radius R along z at (1/2, 1/2); the grid is refined
+    on the vorticity (as the paper adapts on ω), here by the same τ-bisection as
+    cfg4/cfg5 on |ω| h²; V(2,2) RB, M = order, each velocity component solved to 1e-10.
+    `nz_blocks` shortens the (z-independent) periodic axis for small test grids."""
+    nzb = nz_blocks or base
+    return dict(name=f"tube_b{base}_l{max_level}_z{nzb}_m{order}", origin=(0.0, 0.0, 0.0),
+                h0=1 / (16 * base), base_blocks=(base, base, nzb), B=16,
+                bc=(UNBOUNDED, UNBOUNDED, PERIODIC), order=order, smoother=RBGS, omega=1.0,
+                eta1=2, eta2=2, coarse_n=0, max_level=max_level, source="tube", tube_R=R,
+                target_leaves=target, cycles=0, tol=1e-10)
+
+
+def build_vector(cfg):
+    """(Domain, leaves, [f_x, f_y, f_z], [u_x, u_y, u_z] analytic) for the vortex tube:
+    f = -∇×ω sampled at leaf nodes, u the closed-form velocity (E32–E33)."""
+    dom = domain(cfg)
+    leaves = leaves_for(cfg)
+    R = cfg.get("tube_R", 0.25)
+    f = [S.sample_on_leaves(dom, leaves, lambda x, y, z, c=c: S.tube_rhs(x, y, z, c, R)) for c in range(3)]
+    u = [S.sample_on_leaves(dom, leaves, lambda x, y, z, c=c: S.tube_velocity(x, y, z, c, R)) for c in range(3)]
+    return dom, leaves, f, u
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5, "tube": tube}
 
 
 def domain(cfg) -> Domain:
@@ -92,6 +117,9 @@ def source_fn(cfg):
     if s == "torus":
         p = S.torus_params(cfg.get("seed", 5))
         return lambda x, y, z: S.torus_eval(p, x, y, z)
+    if s == "tube":   # refinement score only (the solve takes the components of -∇×ω)
+        R = cfg.get("tube_R", 0.25)
+        return lambda x, y, z: S.tube_omega(x, y, z, R)
     raise KeyError(s)
 
 
@@ -100,7 +128,7 @@ CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cache")
 
 
 def _cache_path(cfg) -> str:
-    keys = ("source", "seed", "base_blocks", "max_level", "target_leaves", "h0", "origin", "bc", "B")
+    keys = ("source", "seed", "base_blocks", "max_level", "target_leaves", "h0", "origin", "bc", "B", "tube_R")
     txt = json.dumps({k: cfg.get(k) for k in keys}, sort_keys=True, default=list) + f"v{LAYOUT_VERSION}"
     return os.path.join(CACHE_DIR, f"{cfg['name']}_{hashlib.sha1(txt.encode()).hexdigest()[:12]}.npz")
 

@@ -177,3 +177,55 @@ def d2u_unb(x):
     gtt = -20 / (q * q) - 80 * ts * ts / (q ** 3)  # d2g/dt2
     u = np.exp(10 * (1 - 1 / q))
     return np.where(inside, 4 * (gt * gt + gtt) * u, 0.0)
+
+
+# ------------------------------------------------------------------ vortex tube (NEXT #4)
+# Biot–Savart test of the paper's performance section (E29–E33): a compact
+# vortex tube along z, centred in the unit cube (x, y unbounded, z periodic); the
+# velocity solves the vector Poisson problem ∇²u = -∇×ω.  R is not given in the
+# paper (reading T1: R = 0.25).
+def _e2_1():
+    from scipy.special import expn
+    return float(expn(2, 1.0))
+
+
+def tube_omega(x, y, z, R=0.25, c=(0.5, 0.5)):
+    """ω_z(r) = (1/2π)(2/R²)(1/E₂(1)) exp(-1/(1 - (r/R)²)) for r < R, else 0 (E31)."""
+    rho2 = ((x - c[0]) ** 2 + (y - c[1]) ** 2) / (R * R) + 0.0 * z
+    inside = rho2 < 1.0
+    q = np.where(inside, 1.0 - rho2, 1.0)
+    return np.where(inside, (1 / (2 * np.pi)) * (2 / (R * R)) / _e2_1() * np.exp(-1.0 / q), 0.0)
+
+
+def tube_rhs(x, y, z, comp, R=0.25, c=(0.5, 0.5)):
+    """Component comp of f = -∇×ω = (-∂_y ω_z, ∂_x ω_z, 0), with
+    ∂_x ω_z = -2 ω_z (x - c_x) / (R² (1 - ρ²)²) (ρ = r/R; smooth, compact)."""
+    w = tube_omega(x, y, z, R, c)
+    rho2 = ((x - c[0]) ** 2 + (y - c[1]) ** 2) / (R * R) + 0.0 * z
+    q = np.where(rho2 < 1.0, 1.0 - rho2, 1.0)
+    g = -2.0 * w / (R * R * q * q)
+    if comp == 0:
+        return -g * (y - c[1])
+    if comp == 1:
+        return g * (x - c[0])
+    return 0.0 * w
+
+
+def tube_velocity(x, y, z, comp, R=0.25, c=(0.5, 0.5)):
+    """Analytic velocity (E32–E33): u = u_θ(r) (-sin θ, cos θ, 0), u_θ = (1/2πr)[1 -
+    (1/E₂(1))(1 - ρ²) E₂(1/(1 - ρ²))] for r <= R, 1/(2πr) outside."""
+    from scipy.special import expn
+    dx, dy = x - c[0] + 0.0 * z, y - c[1] + 0.0 * z
+    r2 = dx * dx + dy * dy
+    rho2 = r2 / (R * R)
+    inside = rho2 < 1.0
+    q = np.where(inside, 1.0 - rho2, 1.0)
+    frac = np.where(inside, 1.0 - q * expn(2, 1.0 / q) / _e2_1(), 1.0)  # 2π r u_θ
+    # u_θ / r = frac / (2π r²), finite at r -> 0 (frac ~ r²)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ur = np.where(r2 > 0, frac / (2 * np.pi * np.where(r2 > 0, r2, 1.0)), 0.0)
+    if comp == 0:
+        return -dy * ur
+    if comp == 1:
+        return dx * ur
+    return 0.0 * ur
