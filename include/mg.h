@@ -153,6 +153,39 @@ int mg_profile_read(mg_handle* h, double* ms, int64_t* counts);
 /* Number of kernels this library has launched so far in the process (all handles). */
 int64_t mg_kernel_launches(void);
 
+/* ---- Grid adaptation (§2.1; readings A1, A2).
+ * No handle: adaptation produces a new leaf list, from which the caller creates a new
+ * solver handle (mg_create).
+ *
+ * mg_detail: detail coefficient γ of every leaf block ("detail coefficient γ"):
+ *   γ = max over the block's nodes of |u - P_W u|, P_W the order-W tensor-product
+ *   Lagrange interpolation of the block's all-even nodes (x, then y, then z; an odd
+ *   local index j uses the even positions j-(W-1) … j+(W-1), shifted by 2 to stay in
+ *   the block).  field_dev: leaf-ordered [n_leaf][B][B][B] fp64 DEVICE array (x
+ *   fastest, the mg_set_rhs layout); gamma_dev: [n_leaf] fp64 DEVICE output.  B in
+ *   {8, 16}; W in {2, 4, 6} with 2(W-1) <= B-2.  Enqueued on `stream` (a cudaStream_t;
+ *   NULL = legacy default stream), asynchronous.  NaN nodes are skipped by the max.
+ *   Returns MG_OK, MG_ERR_ARG (bad size / pointer) or MG_ERR_CUDA (launch failure).
+ */
+int mg_detail(const double* field_dev, int32_t n_leaf, int32_t B, int32_t W, double* gamma_dev, void* stream);
+
+/* mg_adapt: refine / coarsen / 2:1-balance a leaf list from per-leaf γ: leaves
+ * with γ > eps_r below max_level are refined into 8; complete octets of leaves, none
+ * refined, all γ < eps_c, are coarsened into their parent when the parent keeps the
+ * 2:1 constraint; then refinements restore the 26-neighbour 2:1 balance.  Leaves
+ * touching an unbounded face stay at level 0 unless allow_unbounded_refined;
+ * suppressed refinements are counted in *n_suppressed (may be NULL).
+ *   base_blocks[3], bc[6]: as in mg_desc; leaves: HOST int32 [n_leaf][4] rows
+ *   (level, bi, bj, bk); gamma: HOST fp64 [n_leaf]; out_leaves: HOST int32
+ *   [out_capacity][4], filled sorted by (level, bi, bj, bk); *n_out = number of output
+ *   leaves (also when out_capacity is too small, then MG_ERR_ARG is returned).
+ *   Caller owns every buffer.  Pure host code, no CUDA.
+ */
+int mg_adapt(const int32_t base_blocks[3], const int32_t bc[6], int32_t allow_unbounded_refined,
+             const int32_t* leaves, int32_t n_leaf, const double* gamma, double eps_r, double eps_c,
+             int32_t max_level, int32_t* out_leaves, int32_t out_capacity, int32_t* n_out,
+             int32_t* n_suppressed);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,7 +26,7 @@ MG_ALL_BLOCKS = 0x10000
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
            "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
-           "mg_profile_read", "mg_kernel_launches"]
+           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt"]
 STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm"]
 
 
@@ -78,8 +78,14 @@ def load_library(path: str = _LIB_PATH):
     lib.mg_profile_read.argtypes = [P, C.POINTER(D), C.POINTER(C.c_int64)]
     lib.mg_kernel_launches.argtypes = []
     lib.mg_kernel_launches.restype = C.c_int64
+    I32P = C.POINTER(C.c_int32)
+    lib.mg_detail.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, P, P]
+    lib.mg_adapt.argtypes = [I32P, I32P, C.c_int32, I32P, C.c_int32, C.POINTER(D), D, D, C.c_int32, I32P,
+                             C.c_int32, I32P, I32P]
+    lib.mg_detail.restype = C.c_int
+    lib.mg_adapt.restype = C.c_int
     for name in EXPORTS:
-        if name not in ("mg_destroy", "mg_last_error"):
+        if name not in ("mg_destroy", "mg_last_error", "mg_kernel_launches"):
             getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -91,6 +97,47 @@ def _ptr(t):
     if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
         raise ValueError("expected a contiguous float64 CUDA tensor")
     return C.c_void_p(t.data_ptr())
+
+
+def detail(field, B, W, stream=None):
+    """mg_detail: detail coefficient γ per leaf block of a leaf-ordered device field
+    [n, B, B, B] (fp64 CUDA tensor); returns a [n] fp64 CUDA tensor."""
+    import torch
+    lib = load_library()
+    n = int(field.shape[0])
+    g = torch.empty(n, dtype=torch.float64, device=field.device)
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    rc = lib.mg_detail(_ptr(field) if n else None, n, int(B), int(W), _ptr(g) if n else None,
+                       C.c_void_p(stream.cuda_stream))
+    if rc < 0:
+        raise MgError(rc, "mg_detail")
+    return g
+
+
+def adapt(cfg, leaves, gamma, eps_r, eps_c, max_level):
+    """mg_adapt: new leaf list (int32 [m, 4], sorted) and the number of suppressed
+    refinements, from per-leaf γ (host array) — host code in libmg.so."""
+    lib = load_library()
+    lv = np.ascontiguousarray(np.asarray(leaves, dtype=np.int32).reshape(-1, 4))
+    g = np.ascontiguousarray(np.asarray(gamma, dtype=np.float64).reshape(-1))
+    bb = (C.c_int32 * 3)(*[int(v) for v in cfg["base_blocks"]])
+    bc3 = [int(v) for v in cfg["bc"]]
+    bc = (C.c_int32 * 6)(bc3[0], bc3[0], bc3[1], bc3[1], bc3[2], bc3[2])
+    n_out, n_sup = C.c_int32(), C.c_int32()
+    cap = max(8 * len(lv), 64)
+    while True:
+        out = np.zeros((cap, 4), dtype=np.int32)
+        rc = lib.mg_adapt(bb, bc, int(cfg.get("allow_unbounded_refined", 0)),
+                          lv.ctypes.data_as(C.POINTER(C.c_int32)), len(lv),
+                          g.ctypes.data_as(C.POINTER(C.c_double)), float(eps_r), float(eps_c), int(max_level),
+                          out.ctypes.data_as(C.POINTER(C.c_int32)), cap, C.byref(n_out), C.byref(n_sup))
+        if rc == MG_OK:
+            return out[:n_out.value].copy(), n_sup.value
+        if n_out.value > cap:
+            cap = n_out.value
+            continue
+        raise MgError(rc, "mg_adapt")
 
 
 class Solver:
