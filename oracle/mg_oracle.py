@@ -143,7 +143,9 @@ class Oracle:
     def __init__(self, desc, leaves):
         self.order = int(desc["order"])
         self.I = self.order + 2                       # interpolation order M+2
-        self.GE = GE6 if self.order == 6 else GE      # exterior band of the coarse solve
+        # exterior band of the coarse solve: GE6 only where the I = 8 chain of U1 needs it
+        # (the padded LGF sizes then match the GPU's, Z6/U1)
+        self.GE = GE6 if (self.order == 6 and int(desc.get("allow_unbounded_refined", 0))) else GE
         self.w_c2f = lagrange_midpoint_weights(self.I)
         self.smoother = int(desc["smoother"])
         self.omega = float(desc["omega"])
