@@ -36,7 +36,7 @@ def test_tube_fullsize_vector_solve_vs_analytic():
     for comp in (0, 1):
         u = us[comp].cpu().numpy()
         err = np.abs(u - u3[comp]).max()
-        # discretisation error of the 2-level grid (h = 1/256 in the tube, 1/128
-        # outside): 1.66e-6 on the B200 and in the oracle on the same x-y layout; a
-        # wrong sign, component or scaling is O(1)
-        assert err < 4e-6, (comp, err)
+        # discretisation error of the 2-level grid (h = 1/256 in and around the tube,
+        # 1/128 outside): 4.24e-7 on the B200 and in the oracle on the same x-y layout
+        # (the uniform 1/256 grid: 4.1e-7); a wrong sign, component or scaling is O(1)
+        assert err < 1e-6, (comp, err)

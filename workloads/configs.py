@@ -71,11 +71,11 @@ def cfg5(base=8, max_level=4, target=30000):
                 target_leaves=target, cycles=0, tol=1e-10)
 
 
-def tube(base=8, max_level=1, target=1400, nz_blocks=None, order=4, R=0.25):
+def tube(base=8, max_level=1, target=3000, nz_blocks=None, order=4, R=0.25):
     """Biot–Savart vortex tube (E29–E33): unit cube, x and y
     unbounded, z periodic, tube of radius R along z at (1/2, 1/2); the grid is refined
     on the vorticity (as the paper adapts on ω), here by the same τ-bisection as
-    cfg4/cfg5 on |ω| h²; V(2,2) RB, M = order, each velocity component solved to 1e-10.
+    cfg4/cfg5 on |ω| h² of a tube widened by 4 level-0 spacings; V(2,2) RB, M = order, each velocity component solved to 1e-10.
     `nz_blocks` shortens the (z-independent) periodic axis for small test grids."""
     nzb = nz_blocks or base
     return dict(name=f"tube_b{base}_l{max_level}_z{nzb}_m{order}", origin=(0.0, 0.0, 0.0),
@@ -118,7 +118,10 @@ def source_fn(cfg):
         p = S.torus_params(cfg.get("seed", 5))
         return lambda x, y, z: S.torus_eval(p, x, y, z)
     if s == "tube":   # refinement score only (the solve takes the components of -∇×ω)
-        R = cfg.get("tube_R", 0.25)
+        # ω of a tube widened by 4 level-0 spacings: the level-0 nodes next to the
+        # refined region must not reach the steep edge of the compact bump with the
+        # radius-2 M = 6 right-hand-side stencil (T1)
+        R = cfg.get("tube_R", 0.25) + 4 * cfg["h0"]
         return lambda x, y, z: S.tube_omega(x, y, z, R)
     raise KeyError(s)
 
