@@ -738,158 +738,14 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
 }
 
 // ---------------------------------------------------------------------------------
-// Fused residual + restriction (Alg. 1): r = f - Δ_h^M u on the fine
-// pencil and its xy halo ring [-1, 17)^2 (the full-weighting footprint), r := 0 at
-// fine positions outside the level's blocks (reading Z14), then per coarse node of
-// each block's parent octant  u_c = u(2i) (E7) and r_c = Σ w w w r(2i + ·) (E6),
-// nested x, y, z as the definition.  The fine residual is never written to HBM.
-// Step s: load plane s | r at plane s-1 (-> shared ring) | xy-weighted plane sums
-// T(s-2) | coarse r at the even plane 2cz = s-3 from T(s-4), T(s-3), T(s-2).
-// ---------------------------------------------------------------------------------
-struct RRShape {
-  static constexpr int T = PB + 4, TP = T * T;   // u/f plane tile x, y in [-2, 18)
-  static constexpr int RW = PB + 2, RP = RW * RW; // r plane x, y in [-1, 17)
-  static constexpr int D = 2, R = 4;             // prefetch depth, plane ring
-  static constexpr int NT = 416;                 // warps 0-10: 324 residual columns; 11-12: 64 coarse columns
-  static constexpr int NPAIR = TP / 2;           // 200 pairs per field and plane
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(2 * R * TP + 2 * RP);
-};
-
-template <int ORDER>
-__global__ void __launch_bounds__(RRShape::NT, 2) k_res_restrict_pencil(LevelView L, LevelView C, double inv_h2) {
-  using S = RRShape;
-  constexpr int T = S::T, TP = S::TP, RW = S::RW, RP = S::RP, D = S::D, R = S::R, NT = S::NT;
-  extern __shared__ __align__(16) double sm[];
-  double* su = sm;               // [R][TP] u
-  double* sfp = sm + R * TP;     // [R][TP] f
-  double* sr = sm + 2 * R * TP;  // [2][RP] residual planes
-  __shared__ int snb[PMAXL * 27];
-  __shared__ uint32_t sreal[PMAXL];
-  __shared__ int spar[PMAXL * 4];
-  const int tid = threadIdx.x;
-  const int len = __ldg(L.pen_len + blockIdx.x);
-  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
-  for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
-  if (tid < len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
-  if (tid < 4 * len) spar[tid] = __ldg(L.parent + 4 * (size_t)__ldg(pb + tid / 4) + tid % 4);
-  const int nz = PB * len;
-
-  // load descriptors: pairs j < 200 -> u, 200 <= j < 400 -> f (x, y in [-2, 18))
-  int ld_xy[2], ld_sxy[2], ld_dst[2];
-#pragma unroll
-  for (int d = 0; d < 2; ++d) {
-    const int j = tid + d * NT;
-    const int jj = j % S::NPAIR;
-    const int py = jj / (T / 2), px = 2 * (jj % (T / 2));
-    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
-    ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
-    ld_sxy[d] = j < 2 * S::NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
-    ld_dst[d] = (j >= S::NPAIR ? R * TP : 0) + py * T + px;
-  }
-  __syncthreads();
-
-  auto issue = [&](int z) {
-    if (z < nz + 2) {
-      int k, dz, zl;
-      plane_src(z, nz, len, k, dz, zl);
-      const int slot = (z + 2) & (R - 1);
-#pragma unroll
-      for (int d = 0; d < 2; ++d) {
-        if (ld_sxy[d] < 0) continue;
-        const int blk = snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)];
-        const double* src = (ld_dst[d] >= R * TP ? L.f : L.u) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
-        cpa16(sm + ld_dst[d] + slot * TP, src);
-      }
-    }
-    cpa_commit();
-  };
-
-  // residual column (tid < 324): x, y in [-1, 17)
-  const bool rcol = tid < RP;
-  const int cx = rcol ? tid % RW - 1 : 0, cy = rcol ? tid / RW - 1 : 0;
-  const int ci = (cy + 2) * T + (cx + 2);
-  const int csxy = (reg16(cx) + 1) + 3 * (reg16(cy) + 1);
-  // coarse column (warps 11-12): coarse (qx, qy) of the block's octant, fine (2qx, 2qy)
-  const bool ccol = tid >= 352;
-  const int qx = (tid - 352) % 8, qy = ((tid - 352) / 8) % 8;
-
-#pragma unroll
-  for (int q = 0; q < D; ++q) issue(-2 + q);
-
-  double c0 = 0, c1 = 0, c2 = 0, a0 = 0, a1 = 0, a2 = 0;
-  double t0 = 0, t1 = 0, t2 = 0;  // T at planes s-2, s-3, s-4
-  const double h6 = inv_h2 * (1.0 / 6.0);
-  for (int s = -2; s <= nz + 2; ++s) {
-    cpa_wait<D - 1>();
-    __syncthreads();
-    issue(s + D);
-    // xy full-weighting of the residual plane s-2 (written last step), z weights below
-    if (ccol && s - 2 >= -1 && s - 2 <= nz) {
-      const double* rp = sr + ((s - 2) & 1) * RP + (2 * qy + 1) * RW + (2 * qx + 1);
-      double sy = 0.0;
-#pragma unroll
-      for (int dy = -1; dy <= 1; ++dy) {
-        const double* row = rp + dy * RW;
-        const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
-        sy += (dy == 0 ? 0.5 : 0.25) * sx;
-      }
-      t2 = t1; t1 = t0; t0 = sy;
-      const int zc = s - 3;  // the even plane whose z-neighbours s-4, s-2 are now complete
-      if (zc >= 0 && zc < nz && (zc & 1) == 0) {
-        const double sz = (0.25 * t2 + 0.5 * t1) + 0.25 * t0;
-        const int k = zc >> 4, qz = (zc & 15) >> 1;
-        const int* pr = spar + 4 * k;
-        const size_t cidx = (size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx);
-        C.r[cidx] = sz;
-      }
-    }
-    if (s > nz + 1) continue;
-    // coarse u = fine u(2i) at even interior planes (E7)
-    if (ccol && s >= 0 && s < nz && (s & 1) == 0) {
-      const int k = s >> 4, qz = (s & 15) >> 1;
-      const int* pr = spar + 4 * k;
-      C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] =
-          su[((s + 2) & (R - 1)) * TP + (2 * qy + 2) * T + (2 * qx + 2)];
-    }
-    if (!rcol) continue;
-    c2 = c1; c1 = c0;
-    a2 = a1; a1 = a0;
-    {
-      const double* U = su + ((s + 2) & (R - 1)) * TP + ci;
-      c0 = U[0];
-      a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
-    }
-    if (s >= 0) {  // residual at plane r = s-1 in [-1, nz]
-      const int r = s - 1;
-      int k, dz, zl;
-      plane_src(r, nz, len, k, dz, zl);
-      double res = 0.0;  // r := 0 outside the level's blocks (reading Z14)
-      if ((sreal[k] >> (csxy + 9 * (dz + 1))) & 1u) {
-        const int sl = (r + 2) & (R - 1);
-        const double f = sfp[sl * TP + ci];
-        double Lu;
-        if (ORDER == 2) {
-          Lu = ((a1 + (c2 + c0)) - 6.0 * c1) * inv_h2;
-        } else {
-          const double* U = su + sl * TP + ci;
-          const double Dg = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
-          const double F = a1 + (c2 + c0);
-          const double E = Dg + (a2 + a0);
-          Lu = (2.0 * F + E - 24.0 * c1) * h6;
-        }
-        res = f - Lu;
-      }
-      sr[(r & 1) * RP + tid] = res;
-    }
-  }
-  cpa_wait<0>();
-}
-
-// Fused residual + restriction, column-pair version: the residual of the pencil and
-// its halo ring is computed as in the RB sweep (pairs of columns, shuffles for the
-// in-row neighbours, Mehrstellen partial sums per column: r(z) = f(z) - h6 [α(z-1) +
-// β(z) + α(z+1)]) and kept in a 2-plane shared ring; 2 extra warps form the
-// full-weighting sums of each plane and the coarse values (u injection at even planes).
+// Fused residual + restriction (Alg. 1), column-pair version: the residual
+// of the pencil and its halo ring [-1, 17)^2 (the full-weighting footprint; r := 0 at
+// fine positions outside the level's blocks, reading Z14) is computed as in the RB
+// sweep (pairs of columns, shuffles for the in-row neighbours, Mehrstellen partial
+// sums per column: r(z) = f(z) - h6 [α(z-1) + β(z) + α(z+1)]); each pair also forms
+// the x-weighted sum at its even column (one shuffle) into a 2-plane shared ring, and
+// 2 extra warps form the y- and z-weights and the coarse values (u injection at even
+// planes, E7; r_c = Σ w w w r, E6).  The fine residual is never written to HBM.
 // Step s: load plane s | r at plane s-1 | xy weights of r(s-2) | coarse r at s-3.
 struct RR2Shape {
   static constexpr int T = PB + 4, TW = 26, TP = T * TW;  // u tile as in the RB sweep
@@ -898,9 +754,11 @@ struct RR2Shape {
   static constexpr int NT = NR + 64;                       // + 2 warps for the coarse nodes
   static constexpr int NPAIR = T * T / 2;                  // 200 u pairs per plane
   static constexpr int NLD = (NPAIR + NT - 1) / NT;        // 1
-  static constexpr int RRW = 20, RRP = 18 * RRW;           // r planes: rows [-1, 17), x in [-2, 18)
-  // [R][TP] u | [R][NR] f pairs | [2][RRP] r
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + R * NR * 2 + 2 * RRP);
+  // x-weighted residual rows sx (one per pair, at its even column): rows [-1, 17),
+  // pairs 0..9, odd pitch
+  static constexpr int SXW = 11, SXP = 18 * SXW;
+  // [R][TP] u | [R][NR] f pairs | [2][SXP] sx
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + R * NR * 2 + 2 * SXP);
 };
 
 template <int ORDER>
@@ -908,11 +766,11 @@ __global__ void __maxnreg__(80)
     k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
   using S = RR2Shape;
   constexpr int T = S::T, TW = S::TW, TP = S::TP, D = S::D, R = S::R, NR = S::NR, NT = S::NT;
-  constexpr int RRW = S::RRW, RRP = S::RRP;
+  constexpr int SXW = S::SXW, SXP = S::SXP;
   extern __shared__ __align__(16) double sm[];
   double* su = sm;
   double2* sf = reinterpret_cast<double2*>(sm + R * TP);  // [R][NR]
-  double* sr = sm + R * TP + R * NR * 2;                   // [2][RRP]
+  double* sxr = sm + R * TP + R * NR * 2;                  // [2][SXP]
   __shared__ int snb[PMAXL * 27];
   __shared__ uint32_t sreal[PMAXL];
   __shared__ int spar[PMAXL * 4];
@@ -1036,7 +894,11 @@ __global__ void __maxnreg__(80)
             rr.x = fq.x - (aP[0] + alpha_of(cq[0], s4q[0], d4q[0])) * h6;
             rr.y = fq.y - (aP[1] + alpha_of(cq[1], s4q[1], d4q[1])) * h6;
           }
-          if (valid) *reinterpret_cast<double2*>(sr + ((s - 1) & 1) * RRP + (ry + 1) * RRW + (x0 + 2)) = rr;
+          // full weighting along x at this pair's even column x0: r(x0-1) is the left
+          // lane's second column (the definition's order: 0.25 r(-1) + 0.5 r(0) + 0.25 r(1))
+          const double rl = shfl_up1(rr.y);
+          const double sx = 0.25 * rl + 0.5 * rr.x + 0.25 * rr.y;
+          if (valid) sxr[((s - 1) & 1) * SXP + (ry + 1) * SXW + pi] = sx;
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -1053,14 +915,10 @@ __global__ void __maxnreg__(80)
         }
         // full weighting of the residual plane s-2 (written last step): x, then y, then z
         if (!EDGE || s >= 1) {
-          const double* rp = sr + ((s - 2) & 1) * RRP + (2 * qy + 1) * RRW + (2 * qx + 2);
+          const double* rp = sxr + ((s - 2) & 1) * SXP + (2 * qy + 1) * SXW + (qx + 1);  // pair qx+1: x0 = 2qx
           double sy = 0.0;
 #pragma unroll
-          for (int dy = -1; dy <= 1; ++dy) {
-            const double* row = rp + dy * RRW;
-            const double sx = 0.25 * row[-1] + 0.5 * row[0] + 0.25 * row[1];
-            sy += (dy == 0 ? 0.5 : 0.25) * sx;
-          }
+          for (int dy = -1; dy <= 1; ++dy) sy += (dy == 0 ? 0.5 : 0.25) * rp[dy * SXW];
           t2 = t1; t1 = t0; t0 = sy;
           const int zc = s - 3;  // even when j is odd
           if ((j & 1) == 1 && zc >= 0 && zc < nz) {
