@@ -309,7 +309,7 @@ template <int B, int ORDER, int MODE, bool RES, int NT>
 __global__ void __launch_bounds__(NT, (MODE == SM_RB && RES) ? 2 : (MODE < 0 ? 4 : 3))
     k_smooth2(LevelView L, const uint32_t* __restrict__ tab, double omega, double inv_h2, double inv_d) {
   using SH = SmoothShape<B, MODE, RES>;
-  constexpr int NS = SH::NS, H = SH::H, T = SH::T, B3 = SH::B3;
+  constexpr int NS = SH::NS, T = SH::T, B3 = SH::B3;
   constexpr int MAXU = (SH::CNT(0) + NT - 1) / NT;  // pass 0 is the largest
   constexpr int MAXR = (B3 + NT - 1) / NT;
   constexpr int MAXF = MAXU > MAXR ? MAXU : MAXR;
