@@ -722,7 +722,7 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 // Same operation with ε = u_c - û_c on the (B/2+1)^3 coarse nodes under the fine
 // block staged once in shared memory; same nesting/rounding as k_prolong.
 template <int B>
-__global__ void __launch_bounds__(256) k_prolong2(LevelView F, LevelView C) {
+__global__ void __launch_bounds__(256, 5) k_prolong2(LevelView F, LevelView C) {
   constexpr int E = B / 2 + 1, B3 = B * B * B;
   __shared__ double eps[E * E * E];
   __shared__ int snb[27];
