@@ -91,6 +91,10 @@ struct Level {
   bool ext_chain = false;                   // exterior ghosts filled by c2f (reading U1)
   // host tables
   std::vector<int32_t> nbr, parent, bmap, c2f_dst, c2f_J, inj_dst, inj_src, pen_blk, pen_len, gbox;
+  // exterior chains: the injections of refresh(this level) composed into one list of
+  // (dst level | src level << 4, dst index, src index), every source on the finest level
+  std::vector<int32_t> chain_lev, chain_dst, chain_src;
+  int32_t *d_chain_lev = nullptr, *d_chain_dst = nullptr, *d_chain_src = nullptr;
   int gbox_szA = 0, gbox_szB = 0;  // c2f box kernel shared memory (doubles), max over the level's boxes
   std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
@@ -575,6 +579,34 @@ void build_ghosts(mg_handle* h) {
     }
   }
 
+  // Composed injection lists of the exterior-chain refresh of level m (reading U1): the
+  // lists m, m-1, …, 1 are applied in that order, so a level-j source that list j+1
+  // (j+1 <= m) injects from level j+1 is the same value as that level-(j+1) node; follow
+  // such sources up to level m and the whole chain becomes one launch of independent
+  // copies (identical values).
+  for (int m = 2; m < nlev; ++m) {
+    Level& T = h->L[m];
+    if (!T.ext_chain) continue;
+    std::vector<std::unordered_map<int32_t, int32_t>> inj(m + 1);
+    for (int j = 1; j <= m; ++j)
+      for (size_t e = 0; e < h->L[j].inj_dst.size(); ++e) inj[j][h->L[j].inj_dst[e]] = h->L[j].inj_src[e];
+    for (int j = m; j >= 1; --j) {
+      const Level& F = h->L[j];
+      for (size_t e = 0; e < F.inj_dst.size(); ++e) {
+        int lev = j, idx = F.inj_src[e];
+        while (lev < m) {
+          auto it = inj[lev + 1].find(idx);
+          if (it == inj[lev + 1].end()) break;
+          idx = it->second;
+          ++lev;
+        }
+        T.chain_lev.push_back((j - 1) | (lev << 4));
+        T.chain_dst.push_back(F.inj_dst[e]);
+        T.chain_src.push_back(idx);
+      }
+    }
+  }
+
   // neighbour tables and block maps
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
@@ -824,6 +856,9 @@ void alloc_device(mg_handle* h) {
     l.d_c2f_ext = dev_upload(l.c2f_ext);
     l.d_inj_dst = dev_upload(l.inj_dst);
     l.d_inj_src = dev_upload(l.inj_src);
+    l.d_chain_lev = dev_upload(l.chain_lev);
+    l.d_chain_dst = dev_upload(l.chain_dst);
+    l.d_chain_src = dev_upload(l.chain_src);
     l.d_pen_blk = dev_upload(l.pen_blk);
     l.d_pen_len = dev_upload(l.pen_len);
     l.d_gbox = dev_upload(l.gbox);
@@ -957,9 +992,16 @@ void refresh(mg_handle* h, int m) {
   for (int j = lo; j <= m; ++j) any = any || !h->L[j].inj_dst.empty() || !h->L[j].gbox.empty();
   if (!any) return;  // ghost-free level (no events either: keeps the stage profile honest)
   Prof pr(h, ST_GHOST, m);
-  for (int j = m; j >= lo; --j) {
-    Level &F = h->L[j], &C = h->L[j - 1];
-    if (!F.inj_dst.empty()) launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->s);
+  if (lo < m && m < MAX_CHAIN_LEVELS && !h->L[m].chain_dst.empty()) {
+    double* fields[MAX_CHAIN_LEVELS] = {};
+    for (int j = 0; j <= m && j < MAX_CHAIN_LEVELS; ++j) fields[j] = h->L[j].u[h->L[j].cur];
+    const Level& T = h->L[m];
+    launch_inject_chain((int)T.chain_dst.size(), T.d_chain_lev, T.d_chain_dst, T.d_chain_src, fields, h->s);
+  } else {
+    for (int j = m; j >= lo; --j) {
+      Level &F = h->L[j], &C = h->L[j - 1];
+      if (!F.inj_dst.empty()) launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->s);
+    }
   }
   for (int j = lo; j <= m; ++j) {
     Level& F = h->L[j];
@@ -1223,7 +1265,8 @@ void destroy(mg_handle* h) {
     for (void* p : {(void*)l.u[0], (void*)l.u[1], (void*)l.f, (void*)l.r, (void*)l.uhat, (void*)l.d_nbr,
                     (void*)l.d_nbr_real, (void*)l.d_nbr_ext, (void*)l.d_covmask, (void*)l.d_parent, (void*)l.d_bmap, (void*)l.d_c2f_dst,
                     (void*)l.d_c2f_J, (void*)l.d_c2f_ext, (void*)l.d_inj_dst, (void*)l.d_inj_src, (void*)l.d_pen_blk,
-                    (void*)l.d_pen_len, (void*)l.d_gbox, (void*)l.d_sw_blk, (void*)l.d_sw_len, (void*)l.d_sw_z})
+                    (void*)l.d_pen_len, (void*)l.d_gbox, (void*)l.d_sw_blk, (void*)l.d_sw_len, (void*)l.d_sw_z,
+                    (void*)l.d_chain_lev, (void*)l.d_chain_dst, (void*)l.d_chain_src})
       if (p) cudaFree(p);
   }
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,

@@ -84,6 +84,11 @@ void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_
                     int szB, double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void prepare_ghost_kernels();
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);
+// composed exterior-chain injections: fields[lev] = current u of level lev; entry e copies
+// fields[lev_e >> 4][src_e] to fields[lev_e & 15][dst_e]
+constexpr int MAX_CHAIN_LEVELS = 16;
+void launch_inject_chain(int n, const int32_t* lev, const int32_t* dst, const int32_t* src,
+                         double* const fields[MAX_CHAIN_LEVELS], cudaStream_t s);
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s);

@@ -572,6 +572,28 @@ __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_
   if (i < n) d[dst[i]] = sv[src[i]];
 }
 
+struct ChainFields {
+  double* f[MAX_CHAIN_LEVELS];
+};
+
+__global__ void k_copy_chain(int n, const int32_t* __restrict__ lev, const int32_t* __restrict__ dst,
+                             const int32_t* __restrict__ src, ChainFields F) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int l = lev[i];
+    F.f[l & 15][dst[i]] = F.f[l >> 4][src[i]];
+  }
+}
+
+void launch_inject_chain(int n, const int32_t* lev, const int32_t* dst, const int32_t* src,
+                         double* const fields[MAX_CHAIN_LEVELS], cudaStream_t s) {
+  if (n <= 0) return;
+  ChainFields F;
+  for (int j = 0; j < MAX_CHAIN_LEVELS; ++j) F.f[j] = fields[j];
+  k_copy_chain<<<(n + 255) / 256, 256, 0, s>>>(n, lev, dst, src, F);
+  ++g_nlaunch;
+}
+
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s) {
   if (l.n == 0) return;
   { k_copy_list<<<(l.n + 255) / 256, 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field); ++g_nlaunch; }
