@@ -964,7 +964,9 @@ static RBVar rb_var() {
 static const RBVar& rb_pick() {
   // cfg2 256^3 finest sweep on B200 (tools/time_ops.py): <2,4,80> 108.7 us (4 CTAs/SM),
   // <2,4,96> 116.5, <5,8,96> 120.9, <2,4,72> 124.6 (spills), <3,8,80> 129.4 (smem: 3 CTAs/SM)
-  // <3,5,80> 115.3, <4,6,80> 112.9, <3,6,80> 116.7 us (deeper rings do not help)
+  // <3,5,80> 115.3, <4,6,80> 112.9, <3,6,80> 116.7 us (deeper rings do not help).
+  // After the 4-step-group rewrite: <2,4,80> 96.8 us, <2,4,72> 102.4 (spills, still 4
+  // CTAs/SM), <2,4,64> 100.6 (5 CTAs/SM, 88 B of spills)
   static RBVar vars[] = {rb_var<2, 4, 80>(), rb_var<2, 4, 96>(), rb_var<5, 8, 96>()};
   static int sel = [] {
     const char* e = std::getenv("MG_RB_VAR");
