@@ -257,8 +257,6 @@ def run_mine(args, ws, rank, local, dist):
     # kernels (sweep, then residual), 24 B/unknown each; also against the 32 B/unknown a
     # single fused sweep+residual pass would need (the pair's lower bound)
     pair_ms = kernels["smooth"]["avg_ms"] + kernels["residual_standalone"]["avg_ms"]
-    fused_ms = pair_ms
-    fused = (None, [1] * nlev)
     fused_gbs = 48 * Nf / (pair_ms * 1e-3) / 1e9
     coarse_ms = prof["coarse"][0][0] / max(1, prof["coarse"][1][0])
     stage_ms = {s: round(sum(prof[s][0]) / kp, 5) for s in prof}
