@@ -137,8 +137,12 @@ def test_vcycle_parity(name, cycles):
 
 
 @pytest.mark.gpu
-def test_vcycle_parity_graph_and_determinism():
-    cfg, lv, f = _cfg("puu1")
+@pytest.mark.parametrize("name", ["puu1", "cfg3_64", "puu1_m6"])
+def test_vcycle_parity_graph_and_determinism(name):
+    """CUDA-graph launched V-cycles (the bench configuration) vs the oracle, and bitwise
+    determinism of two fresh runs; cfg3_64 exercises the composed exterior-chain
+    injections, puu1_m6 the M = 6 pencil sweep."""
+    cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
     p.g.use_graph(True)
     for _ in range(2):
