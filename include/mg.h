@@ -72,8 +72,9 @@ typedef struct mg_desc {
   int32_t block_size;        /* B: nodes per block edge; 16 (also 8) */
   int32_t bc[6];             /* per face, MG_BC_* */
   int32_t order;             /* M = 2 (cross stencil E8), 4 (Mehrstellen E12) or 6 (27-point Mehrstellen
-                                E13 with its radius-2 right-hand side, reading Z24; not with
-                                allow_unbounded_refined: the I = 8 c2f chain leaves the band) */
+                                E13 with its radius-2 right-hand side, reading Z24; with
+                                allow_unbounded_refined the coarse solve's exterior band is 7 nodes
+                                wide instead of 5, for the I = 8 c2f chain) */
   int32_t coarse_n;          /* nodes along x of the coarsest MG level (uniform sub-base
                                 coarsening N0/2^j, reading Z5); 0 = AMR level 0 is coarsest */
   int32_t smoother;          /* MG_SMOOTHER_* */
