@@ -3,7 +3,8 @@
  *
  * Solves the Poisson equation ∇²u = f (PAPER.md E1) in 3D on a
  * block-structured, collocated (node-centred) multiresolution grid (§2.1,
- * P:58-65) with per-axis periodic or unbounded directions (§2.2), by
+ * P:58-65) with per-axis periodic, unbounded or semi-unbounded directions (§2.2,
+ * P:67-100), by
  * the adaptive FAS V(η1,η2)-cycle of Alg. 1, the compact
  * Mehrstellen stencils Δ_h^M u = R_h^M f (E10-E12; M = 2 uses the
  * cross stencil E8), full-weighting restriction (E6),
@@ -42,8 +43,14 @@ extern "C" {
 
 typedef struct mg_handle mg_handle;
 
-/* boundary conditions, per face (-x,+x,-y,+y,-z,+z); both faces of an axis must match */
-enum { MG_BC_PERIODIC = 0, MG_BC_UNBOUNDED = 1, MG_BC_EVEN = 2, MG_BC_ODD = 3 /* reserved */ };
+/* boundary conditions, per face (-x,+x,-y,+y,-z,+z).  Per axis (low, high):
+ * (PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), or semi-unbounded:
+ * (EVEN or ODD, UNBOUNDED) — homogeneous Neumann / Dirichlet as a mirror about the
+ * node plane x = 0 (EVEN: u(-k) = u(k); ODD: u(-k) = -u(k), so u(0) = 0 and f(0) is
+ * ignored) with an unbounded high face (reading S1).  Blocks touching EVEN/ODD faces stay
+ * on AMR level 0, which must be the coarse-solve level (coarse_n = 0, no U1).  Other
+ * pairs (DST/DCT both sides) -> MG_ERR_BC. */
+enum { MG_BC_PERIODIC = 0, MG_BC_UNBOUNDED = 1, MG_BC_EVEN = 2, MG_BC_ODD = 3 };
 /* smoother ("an iteration of the Gauss-Seidel method"; readings Z10) */
 enum { MG_SMOOTHER_JACOBI = 0, MG_SMOOTHER_RBGS = 1 };
 /* stopping criterion of mg_solve: relative ∞-norm residual or Cauchy (E20) */
@@ -56,7 +63,7 @@ enum {
   MG_ERR_LAYOUT_NESTING = -2,    /* leaves overlap, partial refinement, level 0 not covered */
   MG_ERR_LAYOUT_2TO1 = -3,       /* 26-neighbour 2:1 constraint violated */
   MG_ERR_UNBOUNDED_REFINED = -4, /* refined block touches an unbounded face */
-  MG_ERR_BC = -5,                /* unpaired periodic faces or EVEN/ODD requested */
+  MG_ERR_BC = -5,                /* unsupported face pair (see MG_BC_*) */
   MG_ERR_ORDER = -6,             /* order not in {2,4,6} */
   MG_ERR_STATE = -7,             /* e.g. mg_vcycle before mg_set_rhs */
   MG_ERR_CUDA = -8,              /* CUDA / cuFFT failure or no device */
@@ -95,7 +102,8 @@ void mg_destroy(mg_handle* h);
 const char* mg_last_error(const mg_handle* h);
 
 /* f on the leaves (device, leaf layout).  Injects f up the tree, fills its ghosts
- * (f := 0 beyond unbounded faces), stores f* = R_h^M f on leaf nodes and
+ * (f := 0 beyond unbounded faces, mirror images beyond EVEN/ODD faces), stores
+ * f* = R_h^M f on leaf nodes and
  * ‖f*‖∞.  Resets u to 0 (Alg. 1 initial solution, reading Z28). */
 int mg_set_rhs(mg_handle* h, const double* f_dev);
 /* Initial guess / read-back of u on the leaves (device, leaf layout). */

@@ -38,7 +38,14 @@ import numpy as np
 
 from . import lgf as LGF
 
-PERIODIC, UNBOUNDED = 0, 1
+PERIODIC, UNBOUNDED, EVEN, ODD = 0, 1, 2, 3
+
+
+def face_bc(b):
+    """(low-face, high-face) condition of one axis: an int means both faces."""
+    if isinstance(b, (tuple, list)):
+        return int(b[0]), int(b[1])
+    return int(b), int(b)
 JACOBI, RBGS = 0, 1
 E = 8          # pad width of extended arrays (even; > the widest exterior band)
 GE = 5         # exterior band width computed by the coarse solve (reading Z21/U1), M <= 4
@@ -151,8 +158,16 @@ class Oracle:
         self.omega = float(desc["omega"])
         self.eta1, self.eta2 = int(desc["eta1"]), int(desc["eta2"])
         self.B = int(desc["B"])
-        self.bc = tuple(int(b) for b in desc["bc"])
-        self.per = tuple(b == PERIODIC for b in self.bc)
+        # per face: periodic pairs, unbounded pairs, or semi-unbounded = even /
+        # odd symmetry at the low face with an unbounded high face (reading S1)
+        self.bcf = tuple(face_bc(b) for b in desc["bc"])
+        for lo, hi in self.bcf:
+            if (lo, hi) not in ((PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), (EVEN, UNBOUNDED), (ODD, UNBOUNDED)):
+                raise ValueError(f"unsupported face pair {(lo, hi)}")
+        self.per = tuple(lo == PERIODIC for lo, hi in self.bcf)
+        self.bc = tuple(PERIODIC if p else UNBOUNDED for p in self.per)   # per-axis kind (legacy use)
+        # mirror sign of the low face of each axis: +1 even, -1 odd, 0 none
+        self.sym = tuple({EVEN: 1, ODD: -1}.get(lo, 0) for lo, hi in self.bcf)
         self.origin = np.asarray(desc["origin"], dtype=np.float64)
         self.leaves = np.asarray(leaves, dtype=np.int64)
         base = np.asarray(desc["base_blocks"], dtype=np.int64)
@@ -291,6 +306,16 @@ class Oracle:
                 G[ext] = L.band[ext]
             else:
                 G[ext] = 0.0
+                if any(self.sym):
+                    # f beyond a symmetric low face is the mirror image (even +, odd -);
+                    # beyond unbounded faces it stays 0 (Z16, reading S1)
+                    G = np.where(ext, G, A)
+                    for ax in range(3):
+                        if self.sym[ax]:
+                            Gm = np.moveaxis(G, ax, 0)
+                            for p in range(E):             # extended p <-> J = p - E < 0
+                                Gm[p] = self.sym[ax] * Gm[2 * E - p]
+                            G = np.moveaxis(Gm, 0, ax)
         else:
             G = self.c2f(self.source_W(m - 1, vals, exterior), L)
             if exterior == "zero":
@@ -414,7 +439,13 @@ class Oracle:
     # --------------------------------------------------------------- coarse solve (a6)
     def _coarse_setup(self):
         c = self.levels[0]
-        N = [int(n) for n in c.N]
+        # semi-unbounded axes ("adequate symmetries"; reading S1): the source is
+        # extended by its mirror image across the symmetric low face to the unbounded
+        # domain [-(N-1), N-1] (even: +, odd: - with f(0) := 0) and solved as an
+        # unbounded axis of 2N-1 nodes; node J of the level is extended node J + N - 1.
+        N = [int(n) if self.sym[ax] == 0 else 2 * int(n) - 1 for ax, n in enumerate(c.N)]
+        self.coff = [0 if self.sym[ax] == 0 else int(c.N[ax]) - 1 for ax in range(3)]
+        self.cN = N
         self.unb = [ax for ax in range(3) if not self.per[ax]]
         if len(self.unb) == 0:
             self.coarse_kind = "PPP"
@@ -480,9 +511,18 @@ class Oracle:
             return
         shape = self.coarse_shape
         Fp = np.zeros(shape)
-        Fp[:N[0], :N[1], :N[2]] = c.f
+        fe = c.f
+        for ax in range(3):               # mirror images across symmetric low faces
+            if self.sym[ax]:
+                fm = np.moveaxis(fe, ax, 0)
+                img = self.sym[ax] * fm[:0:-1]            # x = -(N-1) … -1  <->  f(N-1) … f(1)
+                mid = fm[:1] if self.sym[ax] > 0 else 0.0 * fm[:1]   # odd: f(0) := 0
+                fe = np.moveaxis(np.concatenate([img, mid, fm[1:]], axis=0), 0, ax)
+        NE = self.cN
+        Fp[:NE[0], :NE[1], :NE[2]] = fe
         U = np.fft.ifftn(np.fft.fftn(Fp) * self.coarse_mult).real
-        c.u = U[:N[0], :N[1], :N[2]].copy()
+        o = self.coff
+        c.u = U[o[0]:o[0] + N[0], o[1]:o[1] + N[1], o[2]:o[2] + N[2]].copy()
         # exterior band: outputs at J in [-GE, N+GE) along unbounded axes
         GEb = self.GE
         band = np.full(tuple(c.N + 2 * E), np.nan)
@@ -493,7 +533,7 @@ class Oracle:
             else:
                 J = np.arange(-E, N[ax] + E)
                 ok = (J >= -GEb) & (J < N[ax] + GEb)
-                idx.append(np.where(ok, J % shape[ax], -1))
+                idx.append(np.where(ok, (J + self.coff[ax]) % shape[ax], -1))
         sub = U[np.ix_(*[np.where(i < 0, 0, i) for i in idx])]
         valid = np.ones(band.shape, dtype=bool)
         for ax in range(3):

@@ -124,6 +124,13 @@ struct Level {
 struct mg_handle {
   mg_desc d{};
   int per[3] = {1, 1, 1};
+  int sym[3] = {0, 0, 0};  // semi-unbounded axes: mirror sign of the low face (+1 even, -1 odd)
+  int coff[3] = {0, 0, 0};  // coarse solve: level-0 node J is extended node J + coff
+  // level 0: exterior f ghosts beyond symmetric faces = signed mirror copies (reading S1)
+  std::vector<int32_t> fm_dst, fm_src;
+  std::vector<int8_t> fm_sgn;
+  int32_t *d_fm_dst = nullptr, *d_fm_src = nullptr;
+  int8_t* d_fm_sgn = nullptr;
   int order = 4, I = 6, GE = 5, smoother = 1, eta1 = 2, eta2 = 2;
   double omega = 1.0;
   int nsub = 0;
@@ -279,10 +286,16 @@ void validate_and_build(mg_handle* h) {
   if (d.eta1 < 0 || d.eta2 < 0 || !(d.h0 > 0)) throw MgError(MG_ERR_ARG, "bad eta/h0");
   for (int a = 0; a < 3; ++a) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
-    if (d.bc[2 * a] != d.bc[2 * a + 1]) throw MgError(MG_ERR_BC, "both faces of an axis must have the same bc");
-    if (d.bc[2 * a] != MG_BC_PERIODIC && d.bc[2 * a] != MG_BC_UNBOUNDED)
-      throw MgError(MG_ERR_BC, "EVEN/ODD boundary conditions are reserved");
-    h->per[a] = d.bc[2 * a] == MG_BC_PERIODIC;
+    // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
+    // the low face with an unbounded high face (reading S1)
+    const int lo = d.bc[2 * a], hi = d.bc[2 * a + 1];
+    const bool ok = (lo == MG_BC_PERIODIC && hi == MG_BC_PERIODIC) || (lo == MG_BC_UNBOUNDED && hi == MG_BC_UNBOUNDED) ||
+                    ((lo == MG_BC_EVEN || lo == MG_BC_ODD) && hi == MG_BC_UNBOUNDED);
+    if (!ok) throw MgError(MG_ERR_BC, "supported face pairs: P/P, U/U, EVEN/U, ODD/U");
+    h->per[a] = lo == MG_BC_PERIODIC;
+    h->sym[a] = lo == MG_BC_EVEN ? 1 : (lo == MG_BC_ODD ? -1 : 0);
+    if (h->sym[a] && (d.coarse_n > 0 || d.allow_unbounded_refined))
+      throw MgError(MG_ERR_BC, "symmetric faces need AMR level 0 as the coarse-solve level and no U1");
   }
   h->order = d.order;
   h->I = d.order + 2;
@@ -896,7 +909,10 @@ void setup_coarse(mg_handle* h) {
   Level& c = h->L[0];
   int nunb = 0;
   for (int a = 0; a < 3; ++a) {
-    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * c.N[a] + 2 * h->GE - 1);
+    // semi-unbounded: the mirror-extended axis of 2N-1 nodes, solved as unbounded
+    const int Ne = h->sym[a] ? 2 * c.N[a] - 1 : c.N[a];
+    h->coff[a] = h->sym[a] ? c.N[a] - 1 : 0;
+    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * Ne + 2 * h->GE - 1);
     nunb += !h->per[a];
   }
   // 0: all periodic (spectral, zero mode -> 0); 1: all unbounded (3D LGF table);
@@ -976,6 +992,33 @@ void setup_coarse(mg_handle* h) {
     cudaFree(dLow);
   }
   CUDA_OK(cudaStreamSynchronize(h->s));
+  // level-0 exterior f ghosts beyond symmetric low faces: signed mirror copies of real
+  // level-0 nodes (f := 0 beyond unbounded faces, Z16; reading S1)
+  if (h->sym[0] || h->sym[1] || h->sym[2]) {
+    const Level& l = h->L[0];
+    for (size_t e = 0; e < l.c2f_dst.size(); ++e) {
+      int J[3] = {l.c2f_J[3 * e], l.c2f_J[3 * e + 1], l.c2f_J[3 * e + 2]};
+      int sg = 1;
+      bool zero = false;
+      for (int a = 0; a < 3 && !zero; ++a) {
+        if (h->per[a]) continue;
+        if (J[a] >= l.N[a] || (J[a] < 0 && !h->sym[a])) zero = true;   // beyond an unbounded face
+        else if (J[a] < 0) {
+          J[a] = -J[a];
+          sg *= h->sym[a];
+        }
+      }
+      if (zero) continue;
+      int src;
+      if (!is_real_node(h, l, J[0], J[1], J[2], &src)) continue;
+      h->fm_dst.push_back(l.c2f_dst[e]);
+      h->fm_src.push_back(src);
+      h->fm_sgn.push_back((int8_t)sg);
+    }
+    h->d_fm_dst = dev_upload(h->fm_dst);
+    h->d_fm_src = dev_upload(h->fm_src);
+    h->d_fm_sgn = dev_upload(h->fm_sgn);
+  }
 }
 
 // ----------------------------------------------------------------------------------
@@ -1089,12 +1132,12 @@ void prolong_level(mg_handle* h, int m) {
 void coarse_solve(mg_handle* h) {
   Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
-  launch_coarse_gather(c, h->d_dense, h->P, h->s);
+  launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->coff, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
   if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
   else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
   CUFFT_OK(cufftExecZ2D(h->plan_b, (cufftDoubleComplex*)h->d_spec, h->d_dense));
-  launch_coarse_scatter(c, h->d_dense, h->P, c2f_list(h->L[0]), h->s);
+  launch_coarse_scatter(c, h->d_dense, h->P, h->coff, c2f_list(h->L[0]), h->s);
 }
 
 void inject_up_all(mg_handle* h) {
@@ -1244,6 +1287,8 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
                    h->s);
   }
+  if (!h->fm_dst.empty())
+    launch_copy_signed((int)h->fm_dst.size(), h->d_fm_dst, h->d_fm_src, h->d_fm_sgn, h->L[0].f, h->L[0].f, h->s);
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
     launch_correct_rhs(view(h, m), h->order, l.r, h->s);
@@ -1269,6 +1314,8 @@ void destroy(mg_handle* h) {
                     (void*)l.d_chain_lev, (void*)l.d_chain_dst, (void*)l.d_chain_src})
       if (p) cudaFree(p);
   }
+  for (void* p : {(void*)h->d_fm_dst, (void*)h->d_fm_src, (void*)h->d_fm_sgn})
+    if (p) cudaFree(p);
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
                   (void*)h->d_leafbuf2, (void*)h->d_dense, h->d_spec, (void*)h->d_mult})
     if (p) cudaFree(p);

@@ -938,26 +938,56 @@ void launch_zero(double* p, int64_t n, cudaStream_t s) {
 // ---------------------------------------------------------------------------------
 // Coarse direct solve (a6) around cuFFT (library call, timed separately).
 // ---------------------------------------------------------------------------------
-__global__ void k_coarse_gather(LevelView L, double* dense, int Px, int Py, int Pz) {
+// Gather of level-0 f into the dense transform array.  Per axis, dense index q maps to
+// level node J: periodic / unbounded axes J = q (q < N; padding 0); semi-unbounded axes
+// (reading S1) hold the mirror-extended source on x = q - (N-1) in [-(N-1), N-1]:
+// J = |x|, times the face's sign for x < 0, and 0 at x = 0 for an odd face.
+struct CoarseAxes {
+  int P[3], sym[3], off[3];
+};
+
+__global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = (int64_t)Px * Py * Pz;
+  const int64_t n = (int64_t)A.P[0] * A.P[1] * A.P[2];
   if (i >= n) return;
-  const int x = (int)(i % Px), y = (int)((i / Px) % Py), z = (int)(i / ((int64_t)Px * Py));
+  const int q[3] = {(int)(i % A.P[0]), (int)((i / A.P[0]) % A.P[1]), (int)(i / ((int64_t)A.P[0] * A.P[1]))};
+  int J[3];
+  double sg = 1.0;
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (A.sym[a]) {
+      const int x = q[a] - A.off[a];
+      ok = ok && x > -L.N[a] && x < L.N[a] && !(A.sym[a] < 0 && x == 0);
+      J[a] = x < 0 ? -x : x;
+      if (x < 0) sg *= (double)A.sym[a];
+    } else {
+      ok = ok && q[a] < L.N[a];
+      J[a] = q[a];
+    }
+  }
   double v = 0.0;
-  if (x < L.N[0] && y < L.N[1] && z < L.N[2]) {
-    const int bx = x / L.B, by = y / L.B, bz = z / L.B;
+  if (ok) {
+    const int bx = J[0] / L.B, by = J[1] / L.B, bz = J[2] / L.B;
     const int blk = L.bmap[((bz - L.bmap_lo[2]) * L.bmap_n[1] + (by - L.bmap_lo[1])) * L.bmap_n[0] + (bx - L.bmap_lo[0])];
-    v = L.f[(size_t)blk * L.B3 + ((z - bz * L.B) * L.B + (y - by * L.B)) * L.B + (x - bx * L.B)];
+    v = sg * L.f[(size_t)blk * L.B3 + ((J[2] - bz * L.B) * L.B + (J[1] - by * L.B)) * L.B + (J[0] - bx * L.B)];
   }
   dense[i] = v;
 }
 
-void launch_coarse_gather(const LevelView& L, double* dense, const int* P, cudaStream_t s) {
+void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* off,
+                          cudaStream_t s) {
+  CoarseAxes A;
+  for (int a = 0; a < 3; ++a) {
+    A.P[a] = P[a];
+    A.sym[a] = sym[a];
+    A.off[a] = off[a];
+  }
   const int64_t n = (int64_t)P[0] * P[1] * P[2];
-  { k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1], P[2]); ++g_nlaunch; }
+  { k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
 }
 
-__global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, int Px, int Py) {
+__global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, CoarseAxes A) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
   if (i >= n) return;
@@ -965,23 +995,41 @@ __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ d
   const int bx = x / L.B, by = y / L.B, bz = z / L.B;
   const int blk = L.bmap[((bz - L.bmap_lo[2]) * L.bmap_n[1] + (by - L.bmap_lo[1])) * L.bmap_n[0] + (bx - L.bmap_lo[0])];
   L.u[(size_t)blk * L.B3 + ((z - bz * L.B) * L.B + (y - by * L.B)) * L.B + (x - bx * L.B)] =
-      dense[((int64_t)z * Py + y) * Px + x];
+      dense[((int64_t)(z + A.off[2]) * A.P[1] + (y + A.off[1])) * A.P[0] + (x + A.off[0])];
 }
 
-__global__ void k_coarse_band(C2FList g, double* u, const double* __restrict__ dense, int Px, int Py, int Pz) {
+__global__ void k_coarse_band(C2FList g, double* u, const double* __restrict__ dense, CoarseAxes A) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
-  const int P[3] = {Px, Py, Pz};
   int q[3];
-  for (int a = 0; a < 3; ++a) q[a] = ((g.J[3 * i + a] % P[a]) + P[a]) % P[a];
-  u[g.dst[i]] = dense[((int64_t)q[2] * Py + q[1]) * Px + q[0]];
+  for (int a = 0; a < 3; ++a) q[a] = ((g.J[3 * i + a] + A.off[a]) % A.P[a] + A.P[a]) % A.P[a];
+  u[g.dst[i]] = dense[((int64_t)q[2] * A.P[1] + q[1]) * A.P[0] + q[0]];
 }
 
-void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const C2FList& band,
+void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s) {
+  CoarseAxes A;
+  for (int a = 0; a < 3; ++a) {
+    A.P[a] = P[a];
+    A.sym[a] = 0;
+    A.off[a] = off[a];
+  }
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
-  { k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, P[0], P[1]); ++g_nlaunch; }
-  if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, P[0], P[1], P[2]); ++g_nlaunch; }
+  { k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
+  if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, A); ++g_nlaunch; }
+}
+
+__global__ void k_copy_signed(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
+                              const int8_t* __restrict__ sgn, double* d, const double* sv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[dst[i]] = (double)sgn[i] * sv[src[i]];
+}
+
+void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
+                        cudaStream_t s) {
+  if (n <= 0) return;
+  k_copy_signed<<<(n + 255) / 256, 256, 0, s>>>(n, dst, src, sgn, d, sv);
+  ++g_nlaunch;
 }
 
 // spectral symbol σ_M(θ) h² from ŝ = 2cosθ - 2

@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libmg.so")
 
-MG_BC_PERIODIC, MG_BC_UNBOUNDED = 0, 1
+MG_BC_PERIODIC, MG_BC_UNBOUNDED, MG_BC_EVEN, MG_BC_ODD = 0, 1, 2, 3
 MG_SMOOTHER_JACOBI, MG_SMOOTHER_RBGS = 0, 1
 MG_CRIT_RESIDUAL, MG_CRIT_CAUCHY = 0, 1
 MG_FIELD_U, MG_FIELD_F, MG_FIELD_R, MG_FIELD_UHAT = 0, 1, 2, 3
@@ -154,8 +154,9 @@ class Solver:
         d.h0 = float(cfg["h0"])
         d.base_blocks[:] = [int(v) for v in cfg["base_blocks"]]
         d.block_size = int(cfg["B"])
-        bc = [int(v) for v in cfg["bc"]]
-        d.bc[:] = [bc[0], bc[0], bc[1], bc[1], bc[2], bc[2]]
+        # per axis: an int (both faces) or a (low, high) pair, e.g. (MG_BC_ODD, MG_BC_UNBOUNDED)
+        faces = [(int(v[0]), int(v[1])) if isinstance(v, (tuple, list)) else (int(v), int(v)) for v in cfg["bc"]]
+        d.bc[:] = [faces[0][0], faces[0][1], faces[1][0], faces[1][1], faces[2][0], faces[2][1]]
         d.order = int(cfg["order"])
         d.coarse_n = int(cfg.get("coarse_n", 0) or 0)
         d.smoother = int(cfg["smoother"])

@@ -1,0 +1,71 @@
+"""Semi-unbounded directions ("an odd or even condition is enforced in a first
+direction ... while an unbounded one is imposed in the opposite"; reading S1): the
+oracle's mirror-image coarse solve pinned by the image-charge closed form of a Gaussian
+next to the symmetric face, the odd plane, and the discrete equation at the wall."""
+import numpy as np
+import pytest
+
+from oracle import mg_oracle as MO
+from workloads import configs as C
+from workloads import layouts as Lay
+from workloads import sources as S
+
+EVEN, ODD, U, P = 2, 3, 1, 0
+SIG, CX = 0.08, 0.3
+
+
+def _case(n, sym, others=(U, U), order=4):
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / (16 * n), base_blocks=(n, n, n), B=16,
+               bc=((sym, U), others[0], others[1]), order=order, smoother=1, omega=1.0, eta1=2, eta2=2,
+               coarse_n=0)
+    dom = C.domain(cfg)
+    lv = Lay.uniform_leaves(dom)
+    s = 1.0 if sym == EVEN else -1.0
+    c, ci = (CX, 0.5, 0.5), (-CX, 0.5, 0.5)          # the charge and its mirror image
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_charge(x, y, z, sigma=SIG, c=c)
+                           + s * S.gaussian_charge(x, y, z, sigma=SIG, c=ci))
+    ua = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_potential(x, y, z, sigma=SIG, c=c)
+                            + s * S.gaussian_potential(x, y, z, sigma=SIG, c=ci))
+    return cfg, lv, f, ua
+
+
+def _solve(cfg, lv, f):
+    o = MO.Oracle(cfg, lv)
+    o.set_rhs(f)
+    o.vcycle(1)                    # single level: the direct solve is exact
+    return o
+
+
+@pytest.mark.parametrize("sym", [EVEN, ODD])
+def test_image_charge_closed_form_4th_order(sym):
+    errs = []
+    for n in (2, 4):
+        cfg, lv, f, ua = _case(n, sym)
+        o = _solve(cfg, lv, f)
+        assert o.residual_norm()[1] < 1e-11          # discrete equation incl. the wall nodes
+        errs.append(np.abs(o.get_solution() - ua).max())
+    assert errs[0] / errs[1] > 12, errs             # 4th order (Mehrstellen + LGF)
+    assert errs[1] < 2e-5 * np.abs(ua).max()
+
+
+def test_odd_face_plane_is_zero_and_even_face_symmetric():
+    cfg, lv, f, ua = _case(2, ODD)
+    o = _solve(cfg, lv, f)
+    u0 = o.levels[0].u
+    assert np.abs(u0[0]).max() <= 1e-13 * np.abs(u0).max()       # u(0, y, z) = 0
+    # even face: the band below x = 0 mirrors the interior
+    cfg, lv, f, ua = _case(2, EVEN)
+    o = _solve(cfg, lv, f)
+    L0, E = o.levels[0], MO.E
+    for k in (1, 2):
+        assert np.allclose(L0.band[E - k, E:E + 32, E:E + 32], L0.u[k], rtol=0, atol=1e-13 * np.abs(L0.u).max())
+
+
+@pytest.mark.parametrize("others", [(P, U), (U, P)])
+def test_semi_unbounded_mixed_with_periodic(others):
+    """x semi-unbounded with one periodic and one unbounded axis: the discrete solution
+    satisfies the discrete equation everywhere (incl. wall nodes) and is odd/even."""
+    cfg, lv, f, ua = _case(2, ODD, others)
+    o = _solve(cfg, lv, f)
+    assert o.residual_norm()[1] < 1e-11
+    assert np.abs(o.levels[0].u[0]).max() <= 1e-13 * np.abs(o.levels[0].u).max()

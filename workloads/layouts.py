@@ -65,6 +65,8 @@ class Tree:
         self.dom = dom
         nb = dom.nblocks(0)
         self._nb0 = tuple(int(v) for v in nb)
+        # an axis entry is PERIODIC, UNBOUNDED, or a (low, high) face pair (semi-unbounded:
+        # an even/odd low face with an unbounded high face); only PERIODIC wraps
         self._per = tuple(dom.bc[d] == PERIODIC for d in range(3))
         self.nodes: dict[int, set] = {0: {(i, j, k) for i in range(nb[0]) for j in range(nb[1]) for k in range(nb[2])}}
 
@@ -111,7 +113,7 @@ class Tree:
 
     def touches_unbounded_face(self, lev, b):
         nb = self.dom.nblocks(lev)
-        return any(self.dom.bc[d] == UNBOUNDED and (b[d] == 0 or b[d] == nb[d] - 1) for d in range(3))
+        return any(self.dom.bc[d] != PERIODIC and (b[d] == 0 or b[d] == nb[d] - 1) for d in range(3))
 
     def ensure(self, lev, b, forbid):
         """Make block (lev, b) exist by refining ancestors. Returns the forbidden
