@@ -44,12 +44,13 @@ extern "C" {
 typedef struct mg_handle mg_handle;
 
 /* boundary conditions, per face (-x,+x,-y,+y,-z,+z).  Per axis (low, high):
- * (PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), or semi-unbounded:
- * (EVEN or ODD, UNBOUNDED) — homogeneous Neumann / Dirichlet as a mirror about the
- * node plane x = 0 (EVEN: u(-k) = u(k); ODD: u(-k) = -u(k), so u(0) = 0 and f(0) is
- * ignored) with an unbounded high face (reading S1).  Blocks touching EVEN/ODD faces stay
- * on AMR level 0, which must be the coarse-solve level (coarse_n = 0, no U1).  Other
- * pairs (DST/DCT both sides) -> MG_ERR_BC. */
+ * (PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), semi-unbounded (EVEN or ODD, UNBOUNDED)
+ * (reading S1), or symmetric on both faces (ODD, ODD) / (EVEN, ODD) (homogeneous
+ * Dirichlet / Neumann-Dirichlet; reading S2).  The low face mirrors about the node
+ * plane x = 0 (EVEN: u(-k) = u(k); ODD: u(-k) = -u(k), so u(0) = 0 and f on that plane
+ * is ignored); an ODD high face mirrors about the unstored node N (u(N) = 0).  Blocks
+ * touching EVEN/ODD faces stay on AMR level 0, which must be the coarse-solve level
+ * (coarse_n = 0, no U1).  An EVEN high face -> MG_ERR_BC (its wall node is not stored). */
 enum { MG_BC_PERIODIC = 0, MG_BC_UNBOUNDED = 1, MG_BC_EVEN = 2, MG_BC_ODD = 3 };
 /* smoother ("an iteration of the Gauss-Seidel method"; readings Z10) */
 enum { MG_SMOOTHER_JACOBI = 0, MG_SMOOTHER_RBGS = 1 };

@@ -162,12 +162,15 @@ class Oracle:
         # odd symmetry at the low face with an unbounded high face (reading S1)
         self.bcf = tuple(face_bc(b) for b in desc["bc"])
         for lo, hi in self.bcf:
-            if (lo, hi) not in ((PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), (EVEN, UNBOUNDED), (ODD, UNBOUNDED)):
+            if (lo, hi) not in ((PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), (EVEN, UNBOUNDED), (ODD, UNBOUNDED),
+                                (ODD, ODD), (EVEN, ODD)):
                 raise ValueError(f"unsupported face pair {(lo, hi)}")
         self.per = tuple(lo == PERIODIC for lo, hi in self.bcf)
         self.bc = tuple(PERIODIC if p else UNBOUNDED for p in self.per)   # per-axis kind (legacy use)
-        # mirror sign of the low face of each axis: +1 even, -1 odd, 0 none
+        # mirror sign of the low face of each axis: +1 even, -1 odd, 0 none; an odd high
+        # face mirrors about the (unstored) node N: u(N) = 0, u(N+k) = -u(N-k) (reading S2)
         self.sym = tuple({EVEN: 1, ODD: -1}.get(lo, 0) for lo, hi in self.bcf)
+        self.hi_odd = tuple(hi == ODD for lo, hi in self.bcf)
         self.origin = np.asarray(desc["origin"], dtype=np.float64)
         self.leaves = np.asarray(leaves, dtype=np.int64)
         base = np.asarray(desc["base_blocks"], dtype=np.int64)
@@ -315,6 +318,11 @@ class Oracle:
                             Gm = np.moveaxis(G, ax, 0)
                             for p in range(E):             # extended p <-> J = p - E < 0
                                 Gm[p] = self.sym[ax] * Gm[2 * E - p]
+                            if self.hi_odd[ax]:            # J = N + k <-> -(N - k); f(N) = 0
+                                n = int(L.N[ax])
+                                Gm[E + n] = 0.0
+                                for k in range(1, E):
+                                    Gm[E + n + k] = -Gm[E + n - k]
                             G = np.moveaxis(Gm, 0, ax)
         else:
             G = self.c2f(self.source_W(m - 1, vals, exterior), L)
@@ -443,9 +451,13 @@ class Oracle:
         # extended by its mirror image across the symmetric low face to the unbounded
         # domain [-(N-1), N-1] (even: +, odd: - with f(0) := 0) and solved as an
         # unbounded axis of 2N-1 nodes; node J of the level is extended node J + N - 1.
-        N = [int(n) if self.sym[ax] == 0 else 2 * int(n) - 1 for ax, n in enumerate(c.N)]
-        self.coff = [0 if self.sym[ax] == 0 else int(c.N[ax]) - 1 for ax in range(3)]
+        semi = [self.sym[ax] != 0 and not self.hi_odd[ax] for ax in range(3)]
+        N = [2 * int(n) - 1 if semi[ax] else int(n) for ax, n in enumerate(c.N)]
+        self.coff = [int(c.N[ax]) - 1 if semi[ax] else 0 for ax in range(3)]
         self.cN = N
+        if any(self.hi_odd):
+            self.coarse_kind = "SS"        # a both-sided symmetric axis: _coarse_solve_ss
+            return
         self.unb = [ax for ax in range(3) if not self.per[ax]]
         if len(self.unb) == 0:
             self.coarse_kind = "PPP"
@@ -493,12 +505,95 @@ class Oracle:
         K = np.where(zero_per, Kl.reshape(shp), K)
         self.coarse_mult = K
 
+    def _coarse_solve_ss(self):
+        """Coarse solve with a both-sided symmetric axis ("sine or cosine transform
+        instead of the standard discrete Fourier transform"; reading S2): ODD/ODD axes
+        by the DST-I of the nodes 1..N-1 (u(0) = u(N) = 0, θ_k = πk/N), EVEN/ODD axes by
+        the DCT-III of the nodes 0..N-1 (θ_k = π(2k+1)/(2N)), periodic axes by the DFT,
+        unbounded (and semi-unbounded, mirror-extended) axes by the zero-padded DFT.  No
+        mode has all-zero wavenumbers, so every mode takes 1/σ_M(θ) (reading Z22)."""
+        import scipy.fft as sf
+        c = self.levels[0]
+        N = [int(n) for n in c.N]
+        X = c.f.astype(np.float64).copy()
+        for ax in range(3):               # mirror images across semi-unbounded low faces
+            if self.sym[ax] and not self.hi_odd[ax]:
+                fm = np.moveaxis(X, ax, 0)
+                img = self.sym[ax] * fm[:0:-1]
+                mid = fm[:1] if self.sym[ax] > 0 else 0.0 * fm[:1]
+                X = np.moveaxis(np.concatenate([img, mid, fm[1:]], axis=0), 0, ax)
+        thetas = []
+        for ax in range(3):
+            n = N[ax]
+            if self.hi_odd[ax] and self.sym[ax] < 0:          # ODD / ODD
+                X = np.take(X, np.arange(1, n), axis=ax)
+                X = sf.dst(X, type=1, axis=ax, norm="ortho")
+                thetas.append(np.pi * np.arange(1, n) / n)
+            elif self.hi_odd[ax]:                              # EVEN / ODD
+                # unnormalised DCT-III = Σ_j w_j f_j cos(θ_k j), w_0 = 1/2: the left
+                # eigenvectors of the (non-symmetric) mirrored operator
+                X = sf.dct(X, type=3, axis=ax)
+                thetas.append(np.pi * (2 * np.arange(n) + 1) / (2 * n))
+            elif self.per[ax]:
+                thetas.append(None)
+            else:                                              # unbounded / semi-unbounded
+                Pp = LGF.pad_size(self.cN[ax], self.GE)
+                shp = list(X.shape)
+                shp[ax] = Pp - X.shape[ax]
+                X = np.concatenate([X, np.zeros(shp)], axis=ax)
+                thetas.append(None)
+        fft_axes = [ax for ax in range(3) if not self.hi_odd[ax]]
+        for ax in fft_axes:
+            thetas[ax] = 2 * np.pi * np.fft.fftfreq(X.shape[ax])
+        Xc = np.fft.fftn(X, axes=fft_axes) if fft_axes else X
+        TH = np.meshgrid(*thetas, indexing="ij")
+        Xc = Xc / symbol(self.order, TH, c.h)
+        X = np.fft.ifftn(Xc, axes=fft_axes).real if fft_axes else Xc
+        for ax in range(3):
+            if self.hi_odd[ax] and self.sym[ax] < 0:
+                X = sf.dst(X, type=1, axis=ax, norm="ortho")
+                shp = list(X.shape)
+                shp[ax] = 1
+                X = np.concatenate([np.zeros(shp), X], axis=ax)   # u(0) = 0
+            elif self.hi_odd[ax]:
+                X = sf.idct(X, type=3, axis=ax)
+        # interior and exterior band: per axis a source index into X and a sign
+        GEb = self.GE
+        band = np.full(tuple(c.N + 2 * E), np.nan)
+        idx, sgn = [], []
+        for ax in range(3):
+            n = N[ax]
+            J = np.arange(-E, n + E)
+            if self.per[ax]:
+                i, sg = J % n, np.ones(len(J))
+            elif self.hi_odd[ax]:
+                i = np.where(J < 0, -J, np.where(J < n, J, 2 * n - J))
+                sg = np.where(J < 0, float(self.sym[ax]), np.where(J < n, 1.0, -1.0))
+                sg = np.where((J == n) | (J < -(n - 1)) | (J > 2 * n - 1), 0.0, sg)
+                i = np.clip(i, 0, n - 1)
+            else:
+                ok = (J >= -GEb) & (J < n + GEb)
+                i = np.where(ok, (J + self.coff[ax]) % X.shape[ax], 0)
+                sg = np.where(ok, 1.0, np.nan)
+            idx.append(i)
+            sgn.append(sg)
+        V = X[np.ix_(*idx)] * sgn[0][:, None, None] * sgn[1][None, :, None] * sgn[2][None, None, :]
+        o = self.coff
+        inner = tuple(slice(E, E + N[ax]) for ax in range(3))
+        c.u = V[inner].copy()
+        ext = self._exterior_ext(c)
+        band[ext] = V[ext]
+        c.band = band
+
     def coarse_solve(self):
         """u_0 <- S_0 f_0 (Alg. 1).  PPP: F^-1[F f / σ_M], zero mode -> 0
         (zero average).  Unbounded: zero-padded convolution with the LGF
         of Δ_h^M, computed on [-GE, N+GE) for the exterior band."""
         c = self.levels[0]
         N = [int(n) for n in c.N]
+        if self.coarse_kind == "SS":
+            self._coarse_solve_ss()
+            return
         if self.coarse_kind == "PPP":
             F = np.fft.fftn(c.f)
             th = [2 * np.pi * np.fft.fftfreq(n) for n in N]
@@ -556,6 +651,11 @@ class Oracle:
         for m in range(len(self.levels) - 1, 0, -1):
             C = self.levels[m - 1]
             fraw[m - 1] = np.where(C.cov, fraw[m][::2, ::2, ::2], fraw[m - 1])
+        for ax in range(3):
+            if self.sym[ax] < 0:          # odd face: the wall plane is u = 0, f there ignored (S1)
+                sl = [slice(None)] * 3
+                sl[ax] = 0
+                fraw[0][tuple(sl)] = 0.0
         for m, L in enumerate(self.levels):
             X = self.lookup(m, fraw, exterior="zero")
             fs = self._interior(apply_R(X, self.order), L)

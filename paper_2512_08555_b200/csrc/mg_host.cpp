@@ -124,7 +124,11 @@ struct Level {
 struct mg_handle {
   mg_desc d{};
   int per[3] = {1, 1, 1};
-  int sym[3] = {0, 0, 0};  // semi-unbounded axes: mirror sign of the low face (+1 even, -1 odd)
+  int sym[3] = {0, 0, 0};  // symmetric low face: mirror sign (+1 even, -1 odd), 0 none
+  int hi_odd[3] = {0, 0, 0};  // odd high face (mirror about the unstored node N; reading S2)
+  int fper[3] = {1, 1, 1};    // axis periodic in the coarse-solve transform (P, or both faces symmetric)
+  std::vector<int32_t> fwall;  // level-0 nodes on an odd low face: f := 0 there (u = 0)
+  int32_t* d_fwall = nullptr;
   int coff[3] = {0, 0, 0};  // coarse solve: level-0 node J is extended node J + coff
   // level 0: exterior f ghosts beyond symmetric faces = signed mirror copies (reading S1)
   std::vector<int32_t> fm_dst, fm_src;
@@ -290,10 +294,12 @@ void validate_and_build(mg_handle* h) {
     // the low face with an unbounded high face (reading S1)
     const int lo = d.bc[2 * a], hi = d.bc[2 * a + 1];
     const bool ok = (lo == MG_BC_PERIODIC && hi == MG_BC_PERIODIC) || (lo == MG_BC_UNBOUNDED && hi == MG_BC_UNBOUNDED) ||
-                    ((lo == MG_BC_EVEN || lo == MG_BC_ODD) && hi == MG_BC_UNBOUNDED);
-    if (!ok) throw MgError(MG_ERR_BC, "supported face pairs: P/P, U/U, EVEN/U, ODD/U");
+                    ((lo == MG_BC_EVEN || lo == MG_BC_ODD) && (hi == MG_BC_UNBOUNDED || hi == MG_BC_ODD));
+    if (!ok) throw MgError(MG_ERR_BC, "supported face pairs: P/P, U/U, EVEN/U, ODD/U, ODD/ODD, EVEN/ODD");
     h->per[a] = lo == MG_BC_PERIODIC;
     h->sym[a] = lo == MG_BC_EVEN ? 1 : (lo == MG_BC_ODD ? -1 : 0);
+    h->hi_odd[a] = hi == MG_BC_ODD;
+    h->fper[a] = h->per[a] || h->hi_odd[a];
     if (h->sym[a] && (d.coarse_n > 0 || d.allow_unbounded_refined))
       throw MgError(MG_ERR_BC, "symmetric faces need AMR level 0 as the coarse-solve level and no U1");
   }
@@ -909,11 +915,14 @@ void setup_coarse(mg_handle* h) {
   Level& c = h->L[0];
   int nunb = 0;
   for (int a = 0; a < 3; ++a) {
-    // semi-unbounded: the mirror-extended axis of 2N-1 nodes, solved as unbounded
-    const int Ne = h->sym[a] ? 2 * c.N[a] - 1 : c.N[a];
-    h->coff[a] = h->sym[a] ? c.N[a] - 1 : 0;
-    h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * Ne + 2 * h->GE - 1);
-    nunb += !h->per[a];
+    // semi-unbounded: the mirror-extended axis of 2N-1 nodes, solved as unbounded;
+    // both faces symmetric: the odd (2N) or even-odd (4N) periodic extension (S2)
+    const bool semi = h->sym[a] && !h->hi_odd[a];
+    const int Ne = semi ? 2 * c.N[a] - 1 : c.N[a];
+    h->coff[a] = semi ? c.N[a] - 1 : 0;
+    if (h->hi_odd[a]) h->P[a] = (h->sym[a] < 0 ? 2 : 4) * c.N[a];
+    else h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * Ne + 2 * h->GE - 1);
+    nunb += !h->fper[a];
   }
   // 0: all periodic (spectral, zero mode -> 0); 1: all unbounded (3D LGF table);
   // 2: any other mix (generalised E14: lower-dimensional LGF on zero periodic
@@ -946,7 +955,7 @@ void setup_coarse(mg_handle* h) {
   } else if (h->coarse_kind == 2) {
     int ua = -1, ub = -1;  // the unbounded axes (ub = -1: only one)
     for (int a = 0; a < 3; ++a)
-      if (!h->per[a]) (ua < 0 ? ua : ub) = a;
+      if (!h->fper[a]) (ua < 0 ? ua : ub) = a;
     double* dLow = nullptr;  // transform of the lower-dimensional LGF, x h^2 / (Px Py Pz)
     if (ub >= 0) {
       const int Pa = h->P[ua], Pb = h->P[ub];
@@ -987,7 +996,7 @@ void setup_coarse(mg_handle* h) {
       dLow = dev_upload(T1);
     }
     CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
-    launch_build_mult(h->d_mult, h->P, h->per, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, h->s);
+    launch_build_mult(h->d_mult, h->P, h->fper, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, h->s);
     CUDA_OK(cudaStreamSynchronize(h->s));
     cudaFree(dLow);
   }
@@ -995,17 +1004,21 @@ void setup_coarse(mg_handle* h) {
   // level-0 exterior f ghosts beyond symmetric low faces: signed mirror copies of real
   // level-0 nodes (f := 0 beyond unbounded faces, Z16; reading S1)
   if (h->sym[0] || h->sym[1] || h->sym[2]) {
-    const Level& l = h->L[0];
+    const Level& l = h->L[0];  // f beyond odd high faces mirrors too (hi_odd, reading S2)
     for (size_t e = 0; e < l.c2f_dst.size(); ++e) {
       int J[3] = {l.c2f_J[3 * e], l.c2f_J[3 * e + 1], l.c2f_J[3 * e + 2]};
       int sg = 1;
       bool zero = false;
       for (int a = 0; a < 3 && !zero; ++a) {
         if (h->per[a]) continue;
-        if (J[a] >= l.N[a] || (J[a] < 0 && !h->sym[a])) zero = true;   // beyond an unbounded face
+        if ((J[a] >= l.N[a] && !h->hi_odd[a]) || (J[a] < 0 && !h->sym[a])) zero = true;  // beyond an unbounded face
         else if (J[a] < 0) {
           J[a] = -J[a];
           sg *= h->sym[a];
+        } else if (J[a] >= l.N[a]) {   // odd high face: f(N) = 0, f(N + k) = -f(N - k)
+          if (J[a] == l.N[a]) zero = true;
+          J[a] = 2 * l.N[a] - J[a];
+          sg = -sg;
         }
       }
       if (zero) continue;
@@ -1018,6 +1031,16 @@ void setup_coarse(mg_handle* h) {
     h->d_fm_dst = dev_upload(h->fm_dst);
     h->d_fm_src = dev_upload(h->fm_src);
     h->d_fm_sgn = dev_upload(h->fm_sgn);
+    // odd low faces: the wall-plane nodes (u = 0 there; their f is ignored)
+    for (int i = 0; i < l.nreal; ++i)
+      for (int loc = 0; loc < l.B3; ++loc) {
+        const int q[3] = {loc % l.B, (loc / l.B) % l.B, loc / (l.B * l.B)};
+        bool wall = false;
+        for (int a = 0; a < 3; ++a)
+          if (h->sym[a] < 0 && l.coords[i][a] * l.B + q[a] == 0) wall = true;
+        if (wall) h->fwall.push_back(i * l.B3 + loc);
+      }
+    h->d_fwall = dev_upload(h->fwall);
   }
 }
 
@@ -1132,7 +1155,7 @@ void prolong_level(mg_handle* h, int m) {
 void coarse_solve(mg_handle* h) {
   Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
-  launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->coff, h->s);
+  launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->hi_odd, h->coff, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
   if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
   else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
@@ -1287,6 +1310,7 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
                    h->s);
   }
+  if (!h->fwall.empty()) launch_zero_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, h->s);
   if (!h->fm_dst.empty())
     launch_copy_signed((int)h->fm_dst.size(), h->d_fm_dst, h->d_fm_src, h->d_fm_sgn, h->L[0].f, h->L[0].f, h->s);
   for (int m = 0; m < nlev; ++m) {
@@ -1314,7 +1338,7 @@ void destroy(mg_handle* h) {
                     (void*)l.d_chain_lev, (void*)l.d_chain_dst, (void*)l.d_chain_src})
       if (p) cudaFree(p);
   }
-  for (void* p : {(void*)h->d_fm_dst, (void*)h->d_fm_src, (void*)h->d_fm_sgn})
+  for (void* p : {(void*)h->d_fm_dst, (void*)h->d_fm_src, (void*)h->d_fm_sgn, (void*)h->d_fwall})
     if (p) cudaFree(p);
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
                   (void*)h->d_leafbuf2, (void*)h->d_dense, h->d_spec, (void*)h->d_mult})

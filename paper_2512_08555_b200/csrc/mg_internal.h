@@ -99,9 +99,11 @@ void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* sr
                          int nlev, bool to_levels, cudaStream_t s);
 void launch_zero(double* p, int64_t n, cudaStream_t s);
 // coarse solve helpers
-void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* off, cudaStream_t s);
+void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
+                          const int* off, cudaStream_t s);
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s);
+void launch_zero_list(int n, const int32_t* idx, double* d, cudaStream_t s);
 void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
                         cudaStream_t s);
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s);

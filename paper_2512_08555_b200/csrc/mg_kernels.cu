@@ -943,7 +943,7 @@ void launch_zero(double* p, int64_t n, cudaStream_t s) {
 // (reading S1) hold the mirror-extended source on x = q - (N-1) in [-(N-1), N-1]:
 // J = |x|, times the face's sign for x < 0, and 0 at x = 0 for an odd face.
 struct CoarseAxes {
-  int P[3], sym[3], off[3];
+  int P[3], sym[3], hi_odd[3], off[3];
 };
 
 __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
@@ -956,7 +956,21 @@ __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
   bool ok = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (A.sym[a]) {
+    if (A.hi_odd[a]) {
+      // both faces symmetric: periodic extension of period 2N (odd/odd) or 4N (even/odd)
+      const int n = L.N[a], p = q[a];
+      if (A.sym[a] < 0) {
+        ok = ok && p != 0 && p != n;
+        J[a] = p < n ? p : 2 * n - p;
+        if (p > n) sg = -sg;
+      } else {
+        ok = ok && p != n && p != 3 * n;
+        if (p < n) J[a] = p;
+        else if (p <= 2 * n) { J[a] = 2 * n - p; sg = -sg; }
+        else if (p < 3 * n) { J[a] = p - 2 * n; sg = -sg; }
+        else J[a] = 4 * n - p;
+      }
+    } else if (A.sym[a]) {
       const int x = q[a] - A.off[a];
       ok = ok && x > -L.N[a] && x < L.N[a] && !(A.sym[a] < 0 && x == 0);
       J[a] = x < 0 ? -x : x;
@@ -975,12 +989,13 @@ __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
   dense[i] = v;
 }
 
-void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* off,
-                          cudaStream_t s) {
+void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
+                          const int* off, cudaStream_t s) {
   CoarseAxes A;
   for (int a = 0; a < 3; ++a) {
     A.P[a] = P[a];
     A.sym[a] = sym[a];
+    A.hi_odd[a] = hi_odd[a];
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)P[0] * P[1] * P[2];
@@ -1012,11 +1027,23 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
   for (int a = 0; a < 3; ++a) {
     A.P[a] = P[a];
     A.sym[a] = 0;
+    A.hi_odd[a] = 0;
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
   { k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
   if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, A); ++g_nlaunch; }
+}
+
+__global__ void k_zero_list(int n, const int32_t* __restrict__ idx, double* d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[idx[i]] = 0.0;
+}
+
+void launch_zero_list(int n, const int32_t* idx, double* d, cudaStream_t s) {
+  if (n <= 0) return;
+  k_zero_list<<<(n + 255) / 256, 256, 0, s>>>(n, idx, d);
+  ++g_nlaunch;
 }
 
 __global__ void k_copy_signed(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,

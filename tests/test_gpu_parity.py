@@ -51,6 +51,21 @@ def _mixed_adaptive(bc):
     return d, lv, f
 
 
+def _ss_adaptive(pair, others):
+    """x with both faces symmetric (ODD/ODD or EVEN/ODD, reading S2), 2 levels."""
+    d = dict(origin=(0.0, 0.0, 0.0), h0=1 / 64, base_blocks=(4, 4, 4), B=16, bc=(pair, others[0], others[1]),
+             order=4, smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(d)
+    t = Lay.Tree(dom)
+    for b in sorted(t.nodes[0]):
+        if all(1 <= b[a] <= 2 for a in range(3)):
+            t.refine(0, b)
+    lv = t.leaves()
+    Lay.check_layout(dom, lv)
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_charge(x, y, z, sigma=0.07, c=(0.45, 0.5, 0.55)))
+    return d, lv, f
+
+
 def _semi_adaptive(sym, others):
     """Semi-unbounded x (even/odd low face, unbounded high face, reading S1) with
     the given y, z conditions: base 4^3 blocks, the interior refined once around a
@@ -110,6 +125,14 @@ def _cfg(name):
         d, lv, f = _puu_adaptive(1)
         d["order"] = 6
         return d, lv, f
+    elif name == "oo_pp":               # x Dirichlet both faces, y, z periodic
+        return _ss_adaptive((3, 3), (0, 0))
+    elif name == "eo_uu":               # x Neumann / Dirichlet, y, z unbounded
+        return _ss_adaptive((2, 3), (1, 1))
+    elif name == "oo_up_m6":
+        d, lv, f = _ss_adaptive((3, 3), (1, 0))
+        d["order"] = 6
+        return d, lv, f
     elif name == "eu_pu":               # x even / unbounded, y periodic, z unbounded
         return _semi_adaptive(2, (0, 1))
     elif name == "ou_uu":               # x odd / unbounded, y, z unbounded
@@ -146,7 +169,7 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("ppu", 2), ("upu", 2),
+                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("oo_pp", 3), ("eo_uu", 3), ("oo_up_m6", 2), ("ppu", 2), ("upu", 2),
                                          ("upp", 2), ("cfg2_64_m6", 3), ("puu1_m6", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
@@ -212,7 +235,7 @@ def _prepared(name, warm=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
 def test_op_smooth(name):
     p = _prepared(name)
     for m in range(1, len(p.o.levels)):
@@ -224,7 +247,7 @@ def test_op_smooth(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
 def test_op_residual(name):
     p = _prepared(name)
     for m in range(0, len(p.o.levels)):
@@ -238,7 +261,7 @@ def test_op_residual(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
 def test_op_restrict(name):
     p = _prepared(name)
     for m in range(len(p.o.levels) - 1, 0, -1):
@@ -253,7 +276,7 @@ def test_op_restrict(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
 def test_op_prolong(name):
     p = _prepared(name)
     rng = np.random.default_rng(5)
@@ -272,7 +295,7 @@ def test_op_prolong(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
 def test_op_coarse_solve(name):
     p = _prepared(name)
     c = p.o.levels[0]
@@ -292,7 +315,7 @@ def test_op_coarse_solve(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["puu2", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
 def test_set_rhs_fstar_parity(name):
     cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)
@@ -302,7 +325,7 @@ def test_set_rhs_fstar_parity(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_uu", "ou_up_m6"])
+@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
 def test_op_ghost_fill(name):
     """Boundary-ghost fill (a1: f2c injection + c2f, exterior chain U1) of every level:
     GPU ghost-block values vs the oracle's lookup V_m(J) at every halo node (within

@@ -46,3 +46,31 @@ def test_semi_unbounded_image_charge(sym):
     convergence of the same discretisation on the CPU)."""
     e, umax = _run(4, sym, (U, U))
     assert e < 2e-5 * umax, (e, umax)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pair,k", [((ODD, ODD), 3), ((EVEN, ODD), 2)])
+def test_symmetric_both_faces_eigenmode_gpu(pair, k):
+    """Homogeneous Dirichlet / Neumann-Dirichlet along x (reading S2) on a uniform
+    64^3 grid (y, z periodic): a sine / shifted-cosine lattice eigenmode is solved
+    exactly, f (1 + ŝ/12) / (ŝ/h²) (A6), walls included."""
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    n = 4
+    N = 16 * n
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / N, base_blocks=(n, n, n), B=16, bc=(pair, P, P), order=4,
+               smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(cfg)
+    lv = Lay.uniform_leaves(dom)
+    th = np.pi * k / N if pair == (ODD, ODD) else np.pi * (2 * k + 1) / (2 * N)
+    trig = np.sin if pair == (ODD, ODD) else np.cos
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: trig(th * x * N) + 0 * y + 0 * z)
+    s = Solver(cfg, lv)
+    s.set_rhs(torch.from_numpy(f).cuda())
+    s.vcycle(1)                     # one level: the coarse solve is the solution
+    sh = 2 * np.cos(th) - 2
+    uexp = f * (1 + sh / 12) / (sh * N * N)
+    u = s.get_solution().cpu().numpy()
+    assert np.abs(u - uexp).max() <= 1e-11 * np.abs(uexp).max()
+    assert s.residual_norm()[1] < 1e-11

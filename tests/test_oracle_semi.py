@@ -69,3 +69,48 @@ def test_semi_unbounded_mixed_with_periodic(others):
     o = _solve(cfg, lv, f)
     assert o.residual_norm()[1] < 1e-11
     assert np.abs(o.levels[0].u[0]).max() <= 1e-13 * np.abs(o.levels[0].u).max()
+
+
+# ------------------------------------------------------------- both faces symmetric (S2)
+def _ss_case(pair, k, others=(P, P), n=2, order=4):
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / (16 * n), base_blocks=(n, n, n), B=16,
+               bc=(pair, others[0], others[1]), order=order, smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(cfg)
+    lv = Lay.uniform_leaves(dom)
+    N = 16 * n
+    if pair == (ODD, ODD):
+        th = np.pi * k / N                           # DST-I mode sin(π k J / N)
+        fn = lambda x, y, z: np.sin(th * x * N) + 0 * y + 0 * z   # noqa: E731
+    else:
+        th = np.pi * (2 * k + 1) / (2 * N)           # DCT-III mode cos(π (2k+1) J / (2N))
+        fn = lambda x, y, z: np.cos(th * x * N) + 0 * y + 0 * z   # noqa: E731
+    f = S.sample_on_leaves(dom, lv, fn)
+    return cfg, lv, f, th, N
+
+
+@pytest.mark.parametrize("pair,k", [((ODD, ODD), 1), ((ODD, ODD), 5), ((EVEN, ODD), 0), ((EVEN, ODD), 3)])
+def test_symmetric_both_faces_eigenmode_exact(pair, k):
+    """Homogeneous Dirichlet (ODD/ODD) and Neumann-Dirichlet (EVEN/ODD) along x:
+    a sine / shifted-cosine mode is a lattice eigenfunction, so the discrete solution is
+    f (1 + ŝ/12) / (ŝ/h²), ŝ = 2cos θ - 2 (M = 4; A6), including the wall nodes."""
+    cfg, lv, f, th, N = _ss_case(pair, k)
+    o = _solve(cfg, lv, f)
+    h = 1.0 / N
+    sh = 2 * np.cos(th) - 2
+    uexp = f * (1 + sh / 12) / (sh / h ** 2)
+    assert np.abs(o.get_solution() - uexp).max() <= 1e-11 * np.abs(uexp).max()
+    assert o.residual_norm()[1] < 1e-11
+
+
+def test_symmetric_both_faces_with_unbounded_axes():
+    """ODD/ODD x with unbounded y, z: the discrete equation holds everywhere (walls and
+    band) and the solution is odd about x = 0."""
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / 32, base_blocks=(2, 2, 2), B=16,
+               bc=((ODD, ODD), U, U), order=4, smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(cfg)
+    lv = Lay.uniform_leaves(dom)
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_charge(x, y, z, sigma=0.08, c=(0.4, 0.5, 0.5)))
+    o = _solve(cfg, lv, f)
+    assert o.residual_norm()[1] < 1e-11
+    u0 = o.levels[0].u
+    assert np.abs(u0[0]).max() <= 1e-13 * np.abs(u0).max()
