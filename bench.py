@@ -151,6 +151,12 @@ def run_reference(args, ws, rank, dist):
     if rank != 0:
         return
     from oracle.mg_oracle import Oracle
+    # per-step sample sized so that the whole --steps K --warmup W run stays within a few
+    # minutes (measured oracle V-cycle on one core: 128^3 ~1.8 s, 64^3 ~0.25 s, 32^3 ~0.04 s)
+    if args.ref_n <= 0:
+        est = {128: 1.8, 64: 0.25, 32: 0.04}
+        nsteps = args.steps + args.warmup
+        args.ref_n = next((n for n in (128, 64) if est[n] * nsteps <= 150.0), 32)
     cfg, leaves, f = build_workload(args.ref_n)
     o = Oracle(cfg, leaves)
     o.set_rhs(f)
@@ -337,7 +343,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["mine", "reference"], default="mine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-n", type=int, default=128, help="grid of the oracle's bounded sample (--impl reference)")
+    ap.add_argument("--ref-n", type=int, default=0,
+                    help="grid of the oracle's bounded sample (--impl reference); 0 = the largest of "
+                         "128/64/32 that keeps the run within ~2.5 minutes")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
