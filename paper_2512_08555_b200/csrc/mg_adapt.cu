@@ -7,11 +7,11 @@
 // even positions j-(W-1), …, j+(W-1), shifted by steps of 2 to stay inside the block
 // (one-sided near its last node); tensor product applied x, then y, then z.
 //
-// One CTA per leaf block: the even-(y, z) rows are staged in shared memory (coalesced
-// 16-byte loads), the separable passes run from shared memory (x on those rows, y on
-// even z planes), the z pass compares with u read straight from global memory (the
-// staged quarter hits L2), and the max |u - Pu| is a warp-shuffle reduction; 32 KB of
-// shared memory per CTA.  HBM traffic: 8 B per node read once (the kernel's roofline).
+// One CTA per leaf block: every thread loads its 16 (B = 16) nodes into registers at
+// once, the even-(y, z) rows go to shared memory, the separable passes run from there
+// (x on those rows, y on even z planes), the z pass compares with the register values,
+// and the max |u - Pu| is a warp-shuffle reduction; 32 KB of shared memory per CTA.
+// HBM traffic: 8 B per node read once (the kernel's roofline).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -36,12 +36,17 @@ __global__ void __launch_bounds__(DT_NT) k_detail(const double* __restrict__ fie
   __shared__ double s_w[B][W];
   const int tid = threadIdx.x;
   const double* src = field + (size_t)blockIdx.x * B3;
-  // stage the even-(z, y) rows (16-byte loads; the rest is read once, in the last pass)
-  for (int i = tid; i < H * H * B / 2; i += DT_NT) {
-    const int xp = i % (B / 2), r = i / (B / 2);   // pair, row (yh + H zh)
-    const int yh = r % H, zh = r / H;
-    reinterpret_cast<double2*>(A)[i] =
-        __ldg(reinterpret_cast<const double2*>(src + ((2 * zh) * B + 2 * yh) * B) + xp);
+  // the whole block into registers at once (one memory latency, coalesced); the
+  // even-(z, y) rows also go to shared memory for the x pass
+  constexpr int PER = B3 / DT_NT;
+  double uv[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) uv[k] = __ldg(src + tid + k * DT_NT);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = tid + k * DT_NT;
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    if (((y | z) & 1) == 0) A[((z >> 1) * H + (y >> 1)) * B + x] = uv[k];
   }
   // 1D rules: even j -> itself; odd j -> W taps from lo(j), Lagrange weights
   if (tid < B) {
@@ -102,7 +107,9 @@ __global__ void __launch_bounds__(DT_NT) k_detail(const double* __restrict__ fie
   __syncthreads();
   // pass z and the detail
   double m = 0.0;
-  for (int i = tid; i < B3; i += DT_NT) {
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = tid + k * DT_NT;
     const int x = i % B, y = (i / B) % B, z = i / (B * B);
     const double* col = P2 + y * B + x;  // plane z' = e at col[(e/2) * B * B]
     double p;
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(DT_NT) k_detail(const double* __restrict__ fie
       for (int t = 0; t < W; ++t) s += s_w[z][t] * col[((lo >> 1) + t) * B * B];
       p = s;
     }
-    const double d = fabs(__ldg(src + i) - p);
+    const double d = fabs(uv[k] - p);
     m = d > m ? d : m;
   }
 #pragma unroll
