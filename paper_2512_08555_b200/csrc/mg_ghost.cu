@@ -93,8 +93,6 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
                                                    double* __restrict__ ff, const double* __restrict__ cf,
                                                    bool ext_zero, int t1_off) {
   extern __shared__ double sm[];
-  __shared__ int s_l[3][GB<I>::MAXC];          // coarse block-local index per axis and tap
-  __shared__ unsigned char s_s[3][GB<I>::MAXC]; // which of the (<= 3) coarse blocks per axis
   const int32_t* bx = boxes + GBOX_REC * blockIdx.x;
   const int blk = bx[0];
   const int lo[3] = {bx[1], bx[2], bx[3]}, hi[3] = {bx[4], bx[5], bx[6]};
@@ -110,38 +108,41 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
   double* Cs = sm;                   // [nc2][nc1][nc0]
   double* T1 = sm + t1_off;           // [nc2][nc1][nf0]
   double* T2 = Cs;                   // [nc2][nf1][nf0] (reuses Cs after pass x)
-  // ---- coarse addressing, once per box: a box's coarse support spans <= 15 taps per
-  // axis, i.e. at most 2 coarse blocks per axis (3 when the coarse level has B/2
-  // blocks); the record carries the coarse block index of every slot combination
-  {
-    const int bsh = __ffs(C.B) - 1, bmask = C.B - 1;
-    const int q = threadIdx.x;
-    if (q < GB<I>::MAXC) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (q >= nc[a]) continue;
-        int ci = c0[a] + q, cf0 = c0[a];
-        if (C.per[a]) {
-          while (ci < 0) ci += C.N[a];
-          while (ci >= C.N[a]) ci -= C.N[a];
-          while (cf0 < 0) cf0 += C.N[a];
-          while (cf0 >= C.N[a]) cf0 -= C.N[a];
-        }
-        int slot = (ci >> bsh) - (cf0 >> bsh);     // 0, 1, 2 along the taps (arithmetic shifts)
-        if (slot < 0) slot += C.N[a] >> bsh;       // periodic wrap
-        s_l[a][q] = ci & bmask;
-        s_s[a][q] = (unsigned char)slot;
-      }
-    }
-    __syncthreads();
-  }
   // ---- stage the coarse support (nodes outside the coarse level -> 0, only reached
-  // by non-needed nodes of the box)
-  const int CB = C.B;
+  // by non-needed nodes of the box).  A box's coarse support spans <= 15 taps per axis,
+  // i.e. at most 2 coarse blocks per axis (3 when the coarse level has B/2 blocks); the
+  // record carries the coarse block index of every slot combination; each element
+  // computes its block-local index and slot inline (no extra barrier)
+  const int CB = C.B, bsh = __ffs(C.B) - 1, bmask = C.B - 1;
+  int cw0[3], nblk[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    int cf0 = c0[a];
+    if (C.per[a]) {
+      while (cf0 < 0) cf0 += C.N[a];
+      while (cf0 >= C.N[a]) cf0 -= C.N[a];
+    }
+    cw0[a] = cf0 >> bsh;
+    nblk[a] = C.N[a] >> bsh;
+  }
+  auto axis = [&](int a, int q, int& l, int& slot) {
+    int ci = c0[a] + q;
+    if (C.per[a]) {
+      if (ci < 0) ci += C.N[a];
+      if (ci >= C.N[a]) ci -= C.N[a];
+    }
+    l = ci & bmask;
+    slot = (ci >> bsh) - cw0[a];
+    if (slot < 0) slot += nblk[a];
+  };
   box_for(nc, [&](int qx, int qy, int qz) {
-    const int cblk = __ldg(bx + 12 + s_s[0][qx] + 3 * s_s[1][qy] + 9 * s_s[2][qz]);
+    int l0, l1, l2, s0, s1, s2;
+    axis(0, qx, l0, s0);
+    axis(1, qy, l1, s1);
+    axis(2, qz, l2, s2);
+    const int cblk = __ldg(bx + 12 + s0 + 3 * s1 + 9 * s2);
     double v = 0.0;
-    if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (s_l[2][qz] * CB + s_l[1][qy]) * CB + s_l[0][qx]];
+    if (cblk >= 0) v = cf[(size_t)cblk * C.B3 + (l2 * CB + l1) * CB + l0];
     Cs[(qz * nc[1] + qy) * nc[0] + qx] = v;
   });
   __syncthreads();
