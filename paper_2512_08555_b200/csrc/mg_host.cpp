@@ -794,19 +794,28 @@ void build_ghost_boxes(mg_handle* h) {
 void build_pencils(mg_handle* h) {
   // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs.
   // A level with fewer blocks than ~2 resident waves (148 SMs x 4 CTAs) uses 1-block
-  // pencils; larger levels 2 (cfg2 256^3 on B200: 2 beats 4 — shorter tail).
+  // pencils, larger levels 2; ghost-free levels of >= 4 waves whose z-runs average >= 8
+  // blocks 4 — cfg2 256^3 on B200 after the sweep rewrite: sweep 96.9 -> 90.7 us,
+  // V-cycle 0.715 -> 0.694 ms; levels with ghost blocks (cfg3 and cfg5 finest: 1.30 ->
+  // 1.35 ms and 6.53 -> 6.69 ms with 4) stay at 2.
   int lmax_env = 0;
   if (const char* e = std::getenv("MG_PENCIL")) lmax_env = std::max(1, std::min(16, std::atoi(e)));
   const bool off = std::getenv("MG_NO_PENCIL") != nullptr;
   for (auto& l : h->L) {
-    const int lmax = lmax_env ? lmax_env : (l.nreal >= 2 * 148 * 4 ? 2 : 1);
+    std::vector<std::array<int, 4>> cols;  // (bx, by, bz, idx)
+    for (int i = 0; i < l.nreal; ++i) cols.push_back({l.coords[i][0], l.coords[i][1], l.coords[i][2], i});
+    std::sort(cols.begin(), cols.end());
+    int nruns = 0;
+    for (size_t a = 0; a < cols.size(); ++a)
+      if (a == 0 || cols[a][0] != cols[a - 1][0] || cols[a][1] != cols[a - 1][1] || cols[a][2] != cols[a - 1][2] + 1)
+        ++nruns;
+    const bool long_runs = nruns > 0 && l.nreal >= 8 * nruns && l.nghost == 0;
+    const int lmax = lmax_env ? lmax_env
+                              : (l.nreal >= 4 * 148 * 4 && long_runs ? 4 : (l.nreal >= 2 * 148 * 4 ? 2 : 1));
     l.pen_blk.clear();
     l.pen_len.clear();
     l.pen_lmax = lmax;
     if (off || l.B != 16) continue;
-    std::vector<std::array<int, 4>> cols;  // (bx, by, bz, idx)
-    for (int i = 0; i < l.nreal; ++i) cols.push_back({l.coords[i][0], l.coords[i][1], l.coords[i][2], i});
-    std::sort(cols.begin(), cols.end());
     std::vector<std::vector<int>> pens;
     for (size_t a = 0; a < cols.size();) {
       size_t b = a + 1;
