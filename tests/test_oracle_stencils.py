@@ -83,14 +83,19 @@ def test_truncation_order(order, expected):
 
 
 def test_jacobi_single_node_closed_form():
-    # all neighbours zero, u_c = 0: one Jacobi sweep gives u_c = ω f / d
-    for order in (2, 4):
-        h = 0.25
-        d = MO.diag_L(h, order)
-        X = np.zeros((3, 3, 3))
-        Lx = MO.apply_L(X, h, order)
-        f = 3.0
-        unew = X[1, 1, 1] + (2 / 3) * (f - Lx[1, 1, 1]) / d
-        scale = {2: 1.0, 4: 6.0}[order]
-        centre = {2: -6.0, 4: -24.0}[order]
-        assert unew == pytest.approx((2 / 3) * f * h * h * scale / centre, rel=1e-15)
+    # u = 0, f = δ: one damped-Jacobi sweep of Oracle.smooth leaves ω f / d at the node
+    # and nothing elsewhere; d typed from fig:stencils.
+    # (Two-sweep and red-black impulse pins: tests/test_oracle_smoother_pins.py.)
+    from workloads import layouts as Lay
+    for order, centre in ((2, -6.0), (4, -24.0 / 6.0), (6, -128.0 / 30.0)):
+        h = 1 / 32
+        d = dict(origin=(0.0, 0.0, 0.0), h0=h, base_blocks=(2, 2, 2), B=16, bc=(0, 0, 0), order=order,
+                 smoother=MO.JACOBI, omega=2 / 3, eta1=1, eta2=1, coarse_n=0)
+        o = MO.Oracle(d, Lay.uniform_leaves(Lay.Domain((0.0, 0.0, 0.0), h, (2, 2, 2), 16, (0, 0, 0)), 0))
+        L = o.levels[0]
+        L.u = np.zeros(tuple(L.N))
+        L.f = np.zeros(tuple(L.N))
+        L.f[3, 4, 5] = 3.0
+        o.smooth(0)
+        assert L.u[3, 4, 5] == pytest.approx((2 / 3) * 3.0 * h * h / centre, rel=1e-15)
+        assert np.count_nonzero(L.u) == 1

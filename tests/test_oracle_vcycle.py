@@ -120,8 +120,28 @@ def test_adaptive_periodic_singular_stall_and_cauchy():
     f = S.sample_on_leaves(dom, lv, fn)
     o = MO.Oracle(d, lv)
     o.set_rhs(f)
-    cyc, hist = o.solve(1e-9, max_cycles=25, criterion="cauchy")
-    assert hist[-1] < 1e-9
+    res, inc = [], []
+    prev = o.get_solution()
+    for _ in range(16):
+        o.vcycle(1)
+        u = o.get_solution()
+        res.append(o.residual_norm()[1])
+        inc.append(np.abs(u - prev).max() / np.abs(u).max())
+        prev = u
+    # the residual stalls: it stops decreasing at a level far above round-off ...
+    assert res[7] > 1e-8
+    assert abs(res[-1] - res[7]) < 1e-3 * res[7], res
+    # ... while the Cauchy increment (E20) keeps contracting to round-off
+    assert inc[-1] < 1e-13 and inc[-1] < 1e-5 * inc[7], inc
+    # and mg_solve's Cauchy criterion stops, the residual criterion would not
+    o2 = MO.Oracle(d, lv)
+    o2.set_rhs(f)
+    cyc, hist = o2.solve(1e-9, max_cycles=25, criterion="cauchy")
+    assert cyc < 25 and hist[-1] < 1e-9
+    o3 = MO.Oracle(d, lv)
+    o3.set_rhs(f)
+    cyc3, hist3 = o3.solve(1e-9, max_cycles=12, criterion="residual")
+    assert cyc3 == 12 and hist3[-1] > 1e-8
 
 
 def test_cfg3_reduced_free_space_fourth_order():
