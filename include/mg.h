@@ -91,6 +91,16 @@ typedef struct mg_desc {
   int32_t allow_unbounded_refined; /* accept refined levels touching unbounded faces (reading U1) */
   int64_t n_leaf;            /* number of leaf blocks */
   const int32_t* leaves;     /* host array [n_leaf][4] = (level, bi, bj, bk) */
+  /* Kernel-variant controls.  0 everywhere = automatic (the production choice, what a
+   * user wants).  The tests force each variant on small layouts so that the parity
+   * suite runs every code path the automatic choice takes at full size.  Results are
+   * identical up to rounding order for every setting. */
+  int32_t pencil_blocks;     /* blocks per pencil of the z-marching kernels on B = 16 levels:
+                                0 auto (by level size), 1, 2 or 4; else MG_ERR_ARG */
+  int32_t zsplit;            /* RB sweep of 1-block pencils split into two 8-plane z-parts:
+                                0 auto (levels with fewer blocks than SMs), 1 never, 2 always */
+  int32_t fuse;              /* 0 auto: fused pencil kernels where eligible (last pre-sweep +
+                                residual + restriction; residual + restriction); 1 never fuse */
 } mg_desc;
 
 /* Validate the layout (nesting, 2:1, unbounded-face rule), build the level

@@ -182,8 +182,10 @@ def _adapt_once(G, L, gam, eps_r, eps_c, max_level, forbidden):
                 if (m,) + q in blocks:
                     continue
                 a, c = m, q
-                while (a,) + c not in L2:
+                while a > 0 and (a,) + c not in L2:
                     a, c = a - 1, (c[0] >> 1, c[1] >> 1, c[2] >> 1)
+                if (a,) + c not in L2:
+                    raise ValueError("leaves do not cover the domain")
                 if frozen((a,) + c):
                     return "bad", (lf[0] - 1, lf[1] >> 1, lf[2] >> 1, lf[3] >> 1)
                 L2.discard((a,) + c)
@@ -203,10 +205,44 @@ def adapt(base_blocks, bc, leaves, gamma, eps_r, eps_c, max_level, allow_unbound
     G = _Grid(base_blocks, bc, allow_unbounded)
     L = {tuple(int(v) for v in r) for r in leaves}
     gam = {tuple(int(v) for v in r): float(g) for r, g in zip(leaves, gamma)}
+    _validate(G, L, len(leaves))
     forbidden = set()
     while True:
         res = _adapt_once(G, L, gam, eps_r, eps_c, max_level, forbidden)
         if res[0] == "ok":
             out = np.array(sorted(res[1]), dtype=np.int32).reshape(-1, 4)
             return out, res[2]
+        if res[1] in forbidden:          # no progress (cannot happen on a valid input)
+            raise LayoutError("2:1", "adaptation made no progress")
         forbidden.add(res[1])
+
+
+class LayoutError(ValueError):
+    """Invalid input leaf set; `kind` in {"nesting", "2:1", "unbounded"} (the rules of
+    P:65 and P:367 that mg_create also enforces)."""
+
+    def __init__(self, kind, msg):
+        super().__init__(f"{kind}: {msg}")
+        self.kind = kind
+
+
+def _validate(G, L, n_in):
+    """No duplicates, no leaf with a descendant, complete octets, level 0 covered, no
+    refined leaf on an unbounded face unless allowed.  (An input that is not 2:1
+    balanced is accepted: step (3) balances it, or reports "2:1" when that would need
+    a frozen block refined and barring parents makes no progress.)"""
+    if len(L) != n_in:
+        raise LayoutError("nesting", "duplicate leaf")
+    blocks = _blocks_of(L)
+    for lf in L:
+        if any(ch in blocks for ch in _children(lf[0], lf[1:])):
+            raise LayoutError("nesting", "leaf is also refined")
+    for b in blocks:
+        if b not in L and not all(ch in blocks for ch in _children(b[0], b[1:])):
+            raise LayoutError("nesting", "partially refined block")
+    if sum(1 for b in blocks if b[0] == 0) != G.nb0[0] * G.nb0[1] * G.nb0[2]:
+        raise LayoutError("nesting", "level 0 not covered")
+    for lf in L:
+        if lf[0] > 0 and not G.allow and G.touches_unbounded(lf[0], lf[1:]):
+            raise LayoutError("unbounded", "refined leaf on an unbounded face")
+

@@ -142,7 +142,8 @@ bool adapt_once(const Forest& F, const std::set<Key>& L, const std::map<Key, dou
         const Key qk = {m, (int32_t)(n[0] >> 1), (int32_t)(n[1] >> 1), (int32_t)(n[2] >> 1)};
         if (blocks.count(qk)) continue;
         Key a = qk;
-        while (!L2.count(a)) a = parent(a);
+        while (a[0] > 0 && !L2.count(a)) a = parent(a);
+        if (!L2.count(a)) return false;  // not covered: rejected by validate() beforehand
         if (frozen(a)) {
           bad = parent(lf);
           return false;
@@ -160,6 +161,41 @@ bool adapt_once(const Forest& F, const std::set<Key>& L, const std::map<Key, dou
   }
   out.swap(L2);
   return true;
+}
+
+// Input checks: no duplicate leaf, no leaf with a descendant, complete
+// octets, level 0 covered, no refined leaf on an unbounded face unless U1.  An input
+// that is not 2:1 balanced is accepted (step (3) balances it).  MG_OK or the MG_ERR_*
+// code of the first violation.
+int validate(const Forest& F, const std::set<Key>& L, int64_t n_in) {
+  if ((int64_t)L.size() != n_in) return MG_ERR_LAYOUT_NESTING;  // duplicates
+  std::set<Key> blocks;
+  for (const Key& k : L) {
+    if (k[0] < 0 || k[0] > 20) return MG_ERR_ARG;
+    for (int a = 0; a < 3; ++a)
+      if (k[1 + a] < 0 || k[1 + a] >= F.nb(k[0], a)) return MG_ERR_ARG;
+    add_with_ancestors(blocks, k);
+  }
+  for (const Key& k : L) {
+    Key ch[8];
+    children(k, ch);
+    for (auto& c : ch)
+      if (blocks.count(c)) return MG_ERR_LAYOUT_NESTING;  // a leaf that is also refined
+  }
+  for (const Key& b : blocks) {
+    if (L.count(b)) continue;
+    Key ch[8];
+    children(b, ch);
+    for (auto& c : ch)
+      if (!blocks.count(c)) return MG_ERR_LAYOUT_NESTING;  // partially refined block
+  }
+  int64_t n0 = 0;
+  for (const Key& b : blocks) n0 += b[0] == 0;
+  if (n0 != (int64_t)F.nb0[0] * F.nb0[1] * F.nb0[2]) return MG_ERR_LAYOUT_NESTING;
+  for (const Key& k : L) {
+    if (k[0] > 0 && !F.allow && F.touches_unbounded(k)) return MG_ERR_UNBOUNDED_REFINED;
+  }
+  return MG_OK;
 }
 
 }  // namespace
@@ -184,6 +220,8 @@ extern "C" int mg_adapt(const int32_t base_blocks[3], const int32_t bc[6], int32
     L.insert(k);
     gam[k] = gamma[i];
   }
+  const int v = validate(F, L, n_leaf);
+  if (v != MG_OK) return v;
   // When the balance would have to refine a frozen block, bar the parent of the
   // leaf that needs it from refinement and restart from the input (reading A2).
   std::set<Key> forbidden, res;
@@ -191,7 +229,8 @@ extern "C" int mg_adapt(const int32_t base_blocks[3], const int32_t bc[6], int32
   for (;;) {
     Key bad{};
     if (adapt_once(F, L, gam, eps_r, eps_c, max_level, forbidden, res, bad, suppressed)) break;
-    forbidden.insert(bad);
+    // no progress: the conflicting block is already barred (cannot happen on valid input)
+    if (!forbidden.insert(bad).second) return MG_ERR_LAYOUT_2TO1;
   }
   *n_out = (int32_t)res.size();
   if (n_suppressed) *n_suppressed = suppressed;

@@ -164,7 +164,7 @@ struct mg_handle {
   std::vector<cudaEvent_t> evpool;
   std::vector<double> prof_ms;      // [stage][level]
   std::vector<int64_t> prof_n;
-  bool fuse_res = std::getenv("MG_FUSE_RES") != nullptr;  // force the fused sweep+residual kernel
+  int nsm = 148;  // SMs of the device (grid sizing of the pencil kernels)
   // graph
   bool use_graph = false;
   cudaGraphExec_t gexec = nullptr;
@@ -290,6 +290,10 @@ void validate_and_build(mg_handle* h) {
   if (d.eta1 < 0 || d.eta2 < 0 || !(d.h0 > 0)) throw MgError(MG_ERR_ARG, "bad eta/h0");
   for (int a = 0; a < 3; ++a) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
+    if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
+      throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
+    if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1))
+      throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse 0..1");
     // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
     // the low face with an unbounded high face (reading S1)
     const int lo = d.bc[2 * a], hi = d.bc[2 * a + 1];
@@ -668,10 +672,9 @@ void build_ghosts(mg_handle* h) {
 // union of g-thick halo slabs, one per real neighbour — the boxes are at most g thick
 // along some axis, which bounds the kernel's shared memory (~22 KB for I = 6 instead of
 // ~48 KB for a 16^3 bounding box, i.e. more resident CTAs) and skips the unneeded
-// interior of L-shaped unions.  (MG_GBOX_BBOX=1: one bounding box per ghost block.)
+// interior of L-shaped unions.
 void build_ghost_boxes(mg_handle* h) {
   const int I = h->I;
-  const bool bbox = std::getenv("MG_GBOX_BBOX") != nullptr;
   for (size_t m = 1; m < h->L.size(); ++m) {
     Level& l = h->L[m];
     const Level& C = h->L[m - 1];
@@ -719,21 +722,6 @@ void build_ghost_boxes(mg_handle* h) {
         l.gbox_szA = std::max(l.gbox_szA, std::max(nc[0] * nc[1] * nc[2], nf[0] * nf[1] * nc[2]));
         l.gbox_szB = std::max(l.gbox_szB, nf[0] * nc[1] * nc[2]);
       };
-      if (bbox) {
-        int lo[3] = {B, B, B}, hi[3] = {0, 0, 0};
-        for (int z = 0; z < B; ++z)
-          for (int y = 0; y < B; ++y)
-            for (int x = 0; x < B; ++x)
-              if (at(x, y, z)) {
-                const int q[3] = {x, y, z};
-                for (int a = 0; a < 3; ++a) {
-                  lo[a] = std::min(lo[a], q[a]);
-                  hi[a] = std::max(hi[a], q[a] + 1);
-                }
-              }
-        if (hi[0] > lo[0]) emit(lo, hi);
-        continue;
-      }
       // cut points per axis
       std::vector<int> cut[3];
       for (int a = 0; a < 3; ++a) {
@@ -779,9 +767,6 @@ void build_ghost_boxes(mg_handle* h) {
             emit(lo, hi);
           }
     }
-    if (std::getenv("MG_GBOX_STATS"))
-      std::fprintf(stderr, "gbox level %zu: %d ghost blocks, %zu boxes, smem %d+%d doubles\n", m, l.nghost,
-                   l.gbox.size() / GBOX_REC, l.gbox_szA, l.gbox_szB);
     if (sizeof(double) * (size_t)(l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
       throw MgError(MG_ERR_LAYOUT_GHOST, "ghost box exceeds the c2f kernel's shared memory");
   }
@@ -793,14 +778,14 @@ void build_ghost_boxes(mg_handle* h) {
 // pencil per CTA; halos above/below a pencil come through the neighbour tables.
 void build_pencils(mg_handle* h) {
   // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs.
-  // A level with fewer blocks than ~2 resident waves (148 SMs x 4 CTAs) uses 1-block
+  // A level with fewer blocks than ~2 resident waves (#SM x 4 CTAs) uses 1-block
   // pencils, larger levels 2; ghost-free levels of >= 4 waves whose z-runs average >= 8
   // blocks 4 — cfg2 256^3 on B200 after the sweep rewrite: sweep 96.9 -> 90.7 us,
   // V-cycle 0.715 -> 0.694 ms; levels with ghost blocks (cfg3 and cfg5 finest: 1.30 ->
-  // 1.35 ms and 6.53 -> 6.69 ms with 4) stay at 2.
-  int lmax_env = 0;
-  if (const char* e = std::getenv("MG_PENCIL")) lmax_env = std::max(1, std::min(16, std::atoi(e)));
-  const bool off = std::getenv("MG_NO_PENCIL") != nullptr;
+  // 1.35 ms and 6.53 -> 6.69 ms with 4) stay at 2.  mg_desc.pencil_blocks forces one
+  // length (tests), mg_desc.zsplit the z-split of small levels.
+  const int lmax_force = h->d.pencil_blocks;
+  const int nsm = h->nsm;
   for (auto& l : h->L) {
     std::vector<std::array<int, 4>> cols;  // (bx, by, bz, idx)
     for (int i = 0; i < l.nreal; ++i) cols.push_back({l.coords[i][0], l.coords[i][1], l.coords[i][2], i});
@@ -810,12 +795,12 @@ void build_pencils(mg_handle* h) {
       if (a == 0 || cols[a][0] != cols[a - 1][0] || cols[a][1] != cols[a - 1][1] || cols[a][2] != cols[a - 1][2] + 1)
         ++nruns;
     const bool long_runs = nruns > 0 && l.nreal >= 8 * nruns && l.nghost == 0;
-    const int lmax = lmax_env ? lmax_env
-                              : (l.nreal >= 4 * 148 * 4 && long_runs ? 4 : (l.nreal >= 2 * 148 * 4 ? 2 : 1));
+    const int lmax = lmax_force ? lmax_force
+                                : (l.nreal >= 4 * nsm * 4 && long_runs ? 4 : (l.nreal >= 2 * nsm * 4 ? 2 : 1));
     l.pen_blk.clear();
     l.pen_len.clear();
     l.pen_lmax = lmax;
-    if (off || l.B != 16) continue;
+    if (l.B != 16) continue;
     std::vector<std::vector<int>> pens;
     for (size_t a = 0; a < cols.size();) {
       size_t b = a + 1;
@@ -832,14 +817,12 @@ void build_pencils(mg_handle* h) {
       }
       a = b;
     }
-    // launch order: longest first; then (order 1, default) by the z of the first block and
-    // Morton order of (bx, by), so that CTAs resident at the same time are spatial
-    // neighbours and re-read each other's halos from L2; (order 0) column-major.
-    const char* oe = std::getenv("MG_PEN_ORDER");
-    const int order = oe ? std::atoi(oe) : 1;
+    // launch order: longest first; then by the z of the first block and Morton order of
+    // (bx, by), so that CTAs resident at the same time are spatial neighbours and re-read
+    // each other's halos from L2
     auto key = [&](const std::vector<int>& p) {
       const auto& c = l.coords[p[0]];
-      return order == 1 ? ((uint64_t)c[2] << 42) | morton(c[0], c[1], 0) : (uint64_t)0;
+      return ((uint64_t)c[2] << 42) | morton(c[0], c[1], 0);
     };
     std::stable_sort(pens.begin(), pens.end(), [&](const std::vector<int>& x, const std::vector<int>& y) {
       if (x.size() != y.size()) return x.size() > y.size();
@@ -855,7 +838,8 @@ void build_pencils(mg_handle* h) {
     l.sw_blk.clear();
     l.sw_len.clear();
     l.sw_z.clear();
-    if (lmax == 1 && l.nreal < 148 && std::getenv("MG_NO_ZSPLIT") == nullptr) {
+    const bool zsplit = h->d.zsplit == 2 || (h->d.zsplit == 0 && l.nreal < nsm);
+    if (lmax == 1 && zsplit) {
       for (int32_t b : l.pen_blk)
         for (int z0 = 0; z0 < 16; z0 += 8) {
           l.sw_blk.push_back(b);
@@ -1102,7 +1086,7 @@ void sweep(mg_handle* h, int m, bool with_res) {
   // Fuse the residual into the last sweep only on small-block levels: on B = 16
   // levels the halo-3 fused tile is shared-memory-bound, so a
   // halo-2 sweep plus a separate residual pass is faster there.
-  const bool fuse = l.B < 16 || h->fuse_res;
+  const bool fuse = l.B < 16 && h->d.fuse != 1;
   if (with_res && !has_ghosts(h, m) && fuse) {
     Prof pr(h, ST_SMOOTH_RES, m);
     launch_smooth(view(h, m), h->order, mode, h->omega, true, h->s);
@@ -1128,9 +1112,9 @@ void sweep(mg_handle* h, int m, bool with_res) {
 // levels; else residual kernel + restriction kernel), then the level-(m-1) refresh,
 // FAS right-hand side and the û snapshot.
 // Fused residual + restriction (k_rr2_pencil) on B = 16 levels: the fine residual is
-// never written to HBM (cfg2 256^3: 127 us instead of 90 + 62 us); MG_NO_FUSED_RR=1
-// restores the two-kernel path.
-bool fused_res_restrict(mg_handle* h, int m) { return std::getenv("MG_NO_FUSED_RR") == nullptr && h->L[m].B == 16; }
+// never written to HBM (cfg2 256^3: 127 us instead of 90 + 62 us); mg_desc.fuse = 1
+// selects the two-kernel path.
+bool fused_res_restrict(mg_handle* h, int m) { return h->d.fuse != 1 && h->L[m].B == 16; }
 
 void restrict_level(mg_handle* h, int m) {
   Level& C = h->L[m - 1];
@@ -1225,32 +1209,42 @@ void run_vcycles(mg_handle* h, int n) {
     // which cannot be captured), replay on the caller's stream
     cudaStream_t orig = h->s, cap = nullptr;
     CUDA_OK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
-    CUDA_OK(cudaStreamSynchronize(orig));
-    h->s = cap;
-    CUFFT_OK(cufftSetStream(h->plan_f, cap));
-    CUFFT_OK(cufftSetStream(h->plan_b, cap));
-    cudaGraph_t g = nullptr;
     const bool prof = h->prof_on;
-    h->prof_on = false;
-    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-    if (e == cudaSuccess) {
+    cudaGraph_t g = nullptr;
+    // restores the handle (stream, cuFFT streams, profiling) and frees the capture
+    // objects on every exit path, the exception path included
+    auto restore = [&] {
+      h->s = orig;
+      h->prof_on = prof;
+      cufftSetStream(h->plan_f, orig);
+      cufftSetStream(h->plan_b, orig);
+      if (g) cudaGraphDestroy(g);
+      g = nullptr;
+      if (cap) cudaStreamDestroy(cap);
+      cap = nullptr;
+    };
+    try {
+      CUDA_OK(cudaStreamSynchronize(orig));
+      h->s = cap;
+      h->prof_on = false;
+      CUFFT_OK(cufftSetStream(h->plan_f, cap));
+      CUFFT_OK(cufftSetStream(h->plan_b, cap));
+      CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       try {
         vcycle_body(h);
       } catch (...) {
         cudaStreamEndCapture(cap, &g);
-        h->s = orig;
         throw;
       }
-      e = cudaStreamEndCapture(cap, &g);
+      CUDA_OK(cudaStreamEndCapture(cap, &g));
+      CUDA_OK(cudaGraphInstantiate(&h->gexec, g, 0));
+    } catch (...) {
+      restore();
+      h->gexec = nullptr;
+      cudaGetLastError();  // clear a sticky capture error
+      throw;
     }
-    h->s = orig;
-    h->prof_on = prof;
-    cufftSetStream(h->plan_f, orig);
-    cufftSetStream(h->plan_b, orig);
-    cudaStreamDestroy(cap);
-    CUDA_OK(e);
-    CUDA_OK(cudaGraphInstantiate(&h->gexec, g, 0));
-    cudaGraphDestroy(g);
+    restore();
   }
   for (int i = 0; i < n; ++i) CUDA_OK(cudaGraphLaunch(h->gexec, h->s));
 }
@@ -1280,13 +1274,34 @@ double residual_abs(mg_handle* h) {
   return read_norm(h);
 }
 
-void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
+void set_level_ptrs(mg_handle* h, int field) {
   for (size_t m = 0; m < h->L.size(); ++m) {
     Level& l = h->L[m];
     h->h_lvl_ptrs[m] = field == MG_FIELD_F ? l.f : l.u[l.cur];
   }
   CUDA_OK(cudaMemcpyAsync(h->d_lvl_ptrs, h->h_lvl_ptrs.data(), h->L.size() * sizeof(double*), cudaMemcpyHostToDevice,
                           h->s));
+}
+
+// max|u_new - u_old| / max|u_new| over leaf nodes (E20; zero-norm guard:
+// the absolute increment when u_new = 0), u_old in d_leafbuf2 (replaced by u_new)
+double cauchy_increment(mg_handle* h) {
+  set_level_ptrs(h, MG_FIELD_U);
+  CUDA_OK(cudaMemsetAsync(h->d_norm, 0, 2 * sizeof(unsigned long long), h->s));
+  launch_leaf_cauchy((int)h->leaves.size(), h->d.block_size * h->d.block_size * h->d.block_size, h->d_leafmap,
+                     h->d_leafbuf2, h->d_lvl_ptrs, h->d_norm, h->s);
+  unsigned long long bits[2];
+  CUDA_OK(cudaMemcpyAsync(bits, h->d_norm, sizeof(bits), cudaMemcpyDeviceToHost, h->s));
+  CUDA_OK(cudaStreamSynchronize(h->s));
+  double dm, um;
+  std::memcpy(&dm, &bits[0], sizeof(dm));
+  std::memcpy(&um, &bits[1], sizeof(um));
+  if (!std::isfinite(dm) || !std::isfinite(um)) throw MgError(MG_ERR_NONFINITE, "non-finite value in the Cauchy increment");
+  return um > 0 ? dm / um : dm;
+}
+
+void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
+  set_level_ptrs(h, field);
   launch_leaf_scatter((int)h->leaves.size(), h->d.block_size * h->d.block_size * h->d.block_size, h->d_leafmap,
                       leafbuf, h->d_lvl_ptrs, (int)h->L.size(), to_levels, h->s);
   // the pointer table is reused by the next call: order it on the stream
@@ -1396,6 +1411,10 @@ int mg_create(const mg_desc* d, void* stream, mg_handle** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw MgError(MG_ERR_CUDA, "no CUDA device");
     prepare_kernels();
+    int dev = 0, nsm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
+      h->nsm = nsm;
     validate_and_build(h);
     build_ghosts(h);
     build_ghost_boxes(h);
@@ -1457,27 +1476,22 @@ int mg_residual_norm(mg_handle* h, double* abs_inf, double* rel_inf) {
 
 int mg_solve(mg_handle* h, double tol, int max_cycles, int criterion, int* cycles_out, double* value_out) {
   if (!h || max_cycles < 0) return MG_ERR_ARG;
+  if (criterion != MG_CRIT_RESIDUAL && criterion != MG_CRIT_CAUCHY) {
+    h->err = "criterion must be MG_CRIT_RESIDUAL or MG_CRIT_CAUCHY";
+    return MG_ERR_ARG;
+  }
   if (!h->rhs_set) return MG_ERR_STATE;
   int conv = 0;
   const int rc = guard(h, [&] {
     double val = 0.0;
     int c = 0;
+    // Cauchy (E20): the previous iterate stays on the device in leaf layout (d_leafbuf2);
+    // each cycle one kernel forms max|u_new - u_old| and max|u_new| and stores u_new
+    if (criterion == MG_CRIT_CAUCHY) leaf_io(h, h->d_leafbuf2, false, MG_FIELD_U);
     for (c = 1; c <= max_cycles; ++c) {
-      if (criterion == MG_CRIT_CAUCHY) leaf_io(h, h->d_leafbuf2, false, MG_FIELD_U);
       run_vcycles(h, 1);
       if (criterion == MG_CRIT_CAUCHY) {
-        leaf_io(h, h->d_leafbuf, false, MG_FIELD_U);
-        // max |u_new - u_old| / max |u_new| over leaf nodes (E20), on the host copy
-        const size_t n = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
-        std::vector<double> a(n), b(n);
-        CUDA_OK(cudaMemcpy(a.data(), h->d_leafbuf, n * sizeof(double), cudaMemcpyDeviceToHost));
-        CUDA_OK(cudaMemcpy(b.data(), h->d_leafbuf2, n * sizeof(double), cudaMemcpyDeviceToHost));
-        double dm = 0, um = 0;
-        for (size_t i = 0; i < n; ++i) {
-          dm = std::max(dm, std::fabs(a[i] - b[i]));
-          um = std::max(um, std::fabs(a[i]));
-        }
-        val = um > 0 ? dm / um : dm;   // zero-norm guard (absolute increment)
+        val = cauchy_increment(h);
       } else {
         const double a = residual_abs(h);
         val = h->fstar_norm > 0 ? a / h->fstar_norm : a;

@@ -71,8 +71,6 @@ bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s);
 // fused fine residual + full-weighting restriction + u injection into the coarse level
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
 void prepare_pencil_kernels();
-void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
-                const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 // separable box c2f (mg_ghost.cu): boxes = [nbox][12] int32 records (see mg_host.cpp)
 // c2f ghost-box record (int32): dst block, lo[3], hi[3] (fine block-local, hi exclusive),
 // org[3] (level-global fine index of the block's node (0,0,0)), 2 unused, then the
@@ -97,7 +95,9 @@ void launch_norm(const LevelView& L, int order, bool residual, unsigned long lon
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s);
 void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
                          int nlev, bool to_levels, cudaStream_t s);
-void launch_zero(double* p, int64_t n, cudaStream_t s);
+// E20 Cauchy increment on leaf nodes: out[0] max|u - prev|, out[1] max|u|; prev <- u
+void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, double* const* lev_u,
+                        unsigned long long* out, cudaStream_t s);
 // coarse solve helpers
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
                           const int* off, cudaStream_t s);
@@ -111,8 +111,6 @@ void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStre
 // full multiplier table of a mixed periodic / unbounded coarse solve (R2C layout)
 void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
                        double h2, double scale, cudaStream_t s);
-void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s);
-void launch_scale(double* p, int64_t n, double a, cudaStream_t s);
 void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s);
 
 }  // namespace mg

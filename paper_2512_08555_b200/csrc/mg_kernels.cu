@@ -18,24 +18,10 @@
 
 namespace mg {
 
-__constant__ double c_w4[4];
-__constant__ double c_w6[6];
-
-static bool g_weights_ready = false;
 static unsigned long long g_nlaunch = 0;  // kernels launched by this library (bench evidence)
 
 unsigned long long launches_issued() { return g_nlaunch; }
 void note_launch() { ++g_nlaunch; }
-
-static void upload_weights() {
-  if (g_weights_ready) return;
-  // I-point centred Lagrange midpoint weights (reading Z7), I = M + 2
-  const double w4[4] = {-1.0 / 16, 9.0 / 16, 9.0 / 16, -1.0 / 16};
-  const double w6[6] = {3.0 / 256, -25.0 / 256, 150.0 / 256, 150.0 / 256, -25.0 / 256, 3.0 / 256};
-  cudaMemcpyToSymbol(c_w4, w4, sizeof(w4));
-  cudaMemcpyToSymbol(c_w6, w6, sizeof(w6));
-  g_weights_ready = true;
-}
 
 __device__ __forceinline__ int region(int x, int B) { return x < 0 ? -1 : (x >= B ? 1 : 0); }
 
@@ -46,8 +32,6 @@ __device__ __forceinline__ double fetch(const double* __restrict__ a, const int3
   const int blk = __ldg(nb + (dx + 1) + 3 * (dy + 1) + 9 * (dz + 1));
   return a[(size_t)blk * (B * B * B) + ((z - dz * B) * B + (y - dy * B)) * B + (x - dx * B)];
 }
-
-__device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 // ---------------------------------------------------------------------------------
 // Stencils on a shared-memory tile (strides 1, T, T*T).  M=2: cross stencil E8;
@@ -484,7 +468,6 @@ static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res
 }
 
 void prepare_kernels() {
-  upload_weights();
   prepare_pencil_kernels();
   prepare_ghost_kernels();
   prepare_b<16, 2>(); prepare_b<16, 4>(); prepare_b<16, 6>();
@@ -502,68 +485,6 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s) {
   if (order == 2) smooth_dispatch<2>(L, -1, 0.0, true, s);
   else if (order == 4) smooth_dispatch<4>(L, -1, 0.0, true, s);
   else smooth_dispatch<6>(L, -1, 0.0, true, s);
-}
-
-// ---------------------------------------------------------------------------------
-// Boundary ghosts: c2f tensor-product Lagrange interpolation (a1-iii) from the
-// coarse level's current values (already f2c-injected), one thread per entry.
-// Summation order x, then y, then z (mirrors the separable definition).
-// ---------------------------------------------------------------------------------
-template <int I>
-__global__ void k_c2f(C2FList g, double* __restrict__ ff, const double* __restrict__ cf, LevelView C, bool ext_zero) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  if (ext_zero && g.ext[i]) {
-    ff[g.dst[i]] = 0.0;
-    return;
-  }
-  int nt[3], cb[3][I], cl[3][I];
-  double w[3][I];
-  for (int a = 0; a < 3; ++a) {
-    const int J = g.J[3 * i + a];
-    int base, n;
-    if ((J & 1) == 0) {
-      n = 1;
-      base = J >> 1;  // arithmetic shift = floor(J/2) for even J
-      w[a][0] = 1.0;
-    } else {
-      n = I;
-      base = ((J - 1) >> 1) - I / 2 + 1;
-      for (int t = 0; t < I; ++t) w[a][t] = (I == 4) ? c_w4[t] : c_w6[t];
-    }
-    nt[a] = n;
-    for (int t = 0; t < n; ++t) {
-      int ci = base + t;
-      if (C.per[a]) ci = ((ci % C.N[a]) + C.N[a]) % C.N[a];
-      const int blk = floordiv(ci, C.B);
-      cb[a][t] = blk - C.bmap_lo[a];
-      cl[a][t] = ci - blk * C.B;
-    }
-  }
-  double sz = 0.0;
-  for (int tz = 0; tz < nt[2]; ++tz) {
-    double sy = 0.0;
-    for (int ty = 0; ty < nt[1]; ++ty) {
-      double sx = 0.0;
-      const int rowmap = (cb[2][tz] * C.bmap_n[1] + cb[1][ty]) * C.bmap_n[0];
-      for (int tx = 0; tx < nt[0]; ++tx) {
-        const int blk = __ldg(C.bmap + rowmap + cb[0][tx]);
-        const double v = cf[(size_t)blk * C.B3 + (cl[2][tz] * C.B + cl[1][ty]) * C.B + cl[0][tx]];
-        sx += w[0][tx] * v;
-      }
-      sy += w[1][ty] * sx;
-    }
-    sz += w[2][tz] * sy;
-  }
-  ff[g.dst[i]] = sz;
-}
-
-void launch_c2f(const LevelView& fine, const LevelView& coarse, const C2FList& g, double* fine_field,
-                const double* coarse_field, int I, bool ext_zero, cudaStream_t s) {
-  if (g.n == 0) return;
-  const int nt = 128, nb = (g.n + nt - 1) / nt;
-  if (I == 4) { k_c2f<4><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero); ++g_nlaunch; }
-  else { k_c2f<6><<<nb, nt, 0, s>>>(g, fine_field, coarse_field, coarse, ext_zero); ++g_nlaunch; }
 }
 
 __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
@@ -926,13 +847,48 @@ void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* sr
   if (nleaf) { k_leaf_scatter<<<nleaf, 256, 0, s>>>(B3, map, src, dst_by_level, to_levels); ++g_nlaunch; }
 }
 
-__global__ void k_fill(double* p, int64_t n, double v) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] = v;
+// Cauchy increment of one V-cycle (E20) over the leaf nodes, on the device:
+// out[0] <- max |u_new - u_old|, out[1] <- max |u_new| (bit patterns of non-negative
+// doubles, atomicMax; NaN -> the quiet-NaN pattern), and prev <- u_new for the next cycle.
+__global__ void k_leaf_cauchy(int B3, const int64_t* __restrict__ map, double* __restrict__ prev,
+                              double* const* __restrict__ lev_u, unsigned long long* out) {
+  const int n = blockIdx.x;
+  const int64_t m = map[n];
+  const double* u = lev_u[(int)(m >> 32)] + (size_t)(m & 0xffffffff) * B3;
+  double* p = prev + (size_t)n * B3;
+  unsigned long long dm = 0ull, um = 0ull;
+  for (int i = threadIdx.x; i < B3; i += blockDim.x) {
+    const double v = u[i], d = fabs(v - p[i]), a = fabs(v);
+    p[i] = v;
+    const unsigned long long bd = d != d ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(d);
+    const unsigned long long ba = a != a ? 0x7ff8000000000000ull : (unsigned long long)__double_as_longlong(a);
+    dm = bd > dm ? bd : dm;
+    um = ba > um ? ba : um;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t0 = __shfl_xor_sync(0xffffffffu, dm, o), t1 = __shfl_xor_sync(0xffffffffu, um, o);
+    dm = t0 > dm ? t0 : dm;
+    um = t1 > um ? t1 : um;
+  }
+  __shared__ unsigned long long sm[2][32];
+  if ((threadIdx.x & 31) == 0) {
+    sm[0][threadIdx.x >> 5] = dm;
+    sm[1][threadIdx.x >> 5] = um;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      dm = sm[0][w] > dm ? sm[0][w] : dm;
+      um = sm[1][w] > um ? sm[1][w] : um;
+    }
+    atomicMax(out, dm);
+    atomicMax(out + 1, um);
+  }
 }
 
-void launch_zero(double* p, int64_t n, cudaStream_t s) {
-  if (n) { k_fill<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, 0.0); ++g_nlaunch; }
+void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, double* const* lev_u,
+                        unsigned long long* out, cudaStream_t s) {
+  if (nleaf) { k_leaf_cauchy<<<nleaf, 256, 0, s>>>(B3, map, prev, lev_u, out); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -1098,32 +1054,6 @@ void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStre
   { k_mul_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
 }
 
-// x periodic, y/z unbounded (E14 with the periodic axis x, reading Z22):
-// k_x = 0 -> 2D LGF multiplier table (already × h² / (PxPyPz)); else 1/σ on the padded lattice
-__global__ void k_mul_puu(cuDoubleComplex* spec, int Px, int Py, int Pz, int order, double h2,
-                          const double* __restrict__ tab2) {
-  const int Hx = Px / 2 + 1;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t n = (int64_t)Hx * Py * Pz;
-  if (i >= n) return;
-  const int kx = (int)(i % Hx), ky = (int)((i / Hx) % Py), kz = (int)(i / ((int64_t)Hx * Py));
-  double m;
-  if (kx == 0) {
-    m = tab2[(int64_t)kz * Py + ky];
-  } else {
-    const double tw = 6.283185307179586476925286766559;
-    const double sx = 2.0 * cos(tw * kx / Px) - 2.0, sy = 2.0 * cos(tw * ky / Py) - 2.0,
-                 sz = 2.0 * cos(tw * kz / Pz) - 2.0;
-    m = h2 / symbol_h2(order, sx, sy, sz) / ((double)Px * Py * Pz);
-  }
-  spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
-}
-
-void launch_coarse_mul_puu(void* spec, const int* P, int order, double h, const double* tab2, cudaStream_t s) {
-  const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  { k_mul_puu<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h, tab2); ++g_nlaunch; }
-}
-
 // Multiplier of a mixed periodic / unbounded coarse solve on the R2C spectrum (x halved):
 // modes whose periodic wavenumbers are all zero take the transform of the LGF of the
 // operator restricted to the unbounded axes (`low`, already x h^2 / (Px Py Pz)); all
@@ -1157,15 +1087,6 @@ void launch_build_mult(double* mult, const int* P, const int* per, int ua, int u
   k_build_mult<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mult, P[0], P[1], P[2], per[0], per[1], per[2], ua, ub,
                                                              low, order, h2, scale);
   ++g_nlaunch;
-}
-
-__global__ void k_scale(double* p, int64_t n, double a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) p[i] *= a;
-}
-
-void launch_scale(double* p, int64_t n, double a, cudaStream_t s) {
-  if (n) { k_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p, n, a); ++g_nlaunch; }
 }
 
 __global__ void k_real_part_scale(const cuDoubleComplex* c, double* out, int64_t n, double a) {

@@ -21,7 +21,6 @@
 
 #include <cstdint>
 #include <type_traits>
-#include <cstdlib>
 
 #include "mg_internal.h"
 
@@ -947,34 +946,14 @@ bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, 
 // ---------------------------------------------------------------------------------
 constexpr int RES_D = 3;
 
-// RB sweep variants (prefetch depth D, ring R, register cap): MG_RB_VAR selects one
-// for tuning; the default is the fastest measured on B200.
-struct RBVar {
-  void (*k2)(LevelView, double, double, double);
-  void (*k4)(LevelView, double, double, double);
-  void (*k2s)(LevelView, double, double, double);  // sweep pencils with z-parts
-  void (*k4s)(LevelView, double, double, double);
-  size_t smem;
-};
-template <int D, int RR, int NREG>
-static RBVar rb_var() {
-  return {k_rb_pencil<2, D, RR, NREG, false>, k_rb_pencil<4, D, RR, NREG, false>,
-          k_rb_pencil<2, D, RR, NREG, true>, k_rb_pencil<4, D, RR, NREG, true>, RBShape<D, RR>::SMEM};
-}
-static const RBVar& rb_pick() {
-  // cfg2 256^3 finest sweep on B200 (tools/time_ops.py): <2,4,80> 108.7 us (4 CTAs/SM),
-  // <2,4,96> 116.5, <5,8,96> 120.9, <2,4,72> 124.6 (spills), <3,8,80> 129.4 (smem: 3 CTAs/SM)
-  // <3,5,80> 115.3, <4,6,80> 112.9, <3,6,80> 116.7 us (deeper rings do not help).
-  // After the 4-step-group rewrite: <2,4,80> 96.8 us, <2,4,72> 102.4 (spills, still 4
-  // CTAs/SM), <2,4,64> 100.6 (5 CTAs/SM, 88 B of spills)
-  static RBVar vars[] = {rb_var<2, 4, 80>(), rb_var<2, 4, 96>(), rb_var<5, 8, 96>()};
-  static int sel = [] {
-    const char* e = std::getenv("MG_RB_VAR");
-    const int v = e ? std::atoi(e) : 0;
-    return (v >= 0 && v < (int)(sizeof(vars) / sizeof(vars[0]))) ? v : 0;
-  }();
-  return vars[sel];
-}
+// RB sweep variant (prefetch depth D, ring R, register cap): cfg2 256^3 finest sweep on
+// B200 (tools/time_ops.py): <2,4,80> 108.7 us (4 CTAs/SM), <2,4,96> 116.5, <5,8,96> 120.9,
+// <2,4,72> 124.6 (spills), <3,8,80> 129.4 (smem: 3 CTAs/SM), <3,5,80> 115.3, <4,6,80>
+// 112.9, <3,6,80> 116.7 us (deeper rings do not help).  After the 4-step-group rewrite:
+// <2,4,80> 96.8 us, <2,4,72> 102.4 (spills, still 4 CTAs/SM), <2,4,64> 100.6 (5 CTAs/SM,
+// 88 B of spills).
+constexpr int RB_D = 2, RB_R = 4, RB_NREG = 80;
+using RBS = RBShape<RB_D, RB_R>;
 
 void prepare_pencil_kernels() {
   // the whole unified L1 as shared memory: several pencil CTAs per SM
@@ -982,11 +961,10 @@ void prepare_pencil_kernels() {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   };
-  const RBVar& v = rb_pick();
-  setup((const void*)v.k2, v.smem);
-  setup((const void*)v.k4, v.smem);
-  setup((const void*)v.k2s, v.smem);
-  setup((const void*)v.k4s, v.smem);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, true>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, true>, RBS::SMEM);
   setup((const void*)k_rb6_pencil<RB6_NREG, false>, RB6Shape::SMEM);
   setup((const void*)k_rb6_pencil<RB6_NREG, true>, RB6Shape::SMEM);
   setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
@@ -1029,10 +1007,13 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
   }
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
-  const RBVar& v = rb_pick();
   const int grid = L.sw_npen > 0 ? L.sw_npen : L.npen;
-  if (L.sw_npen > 0) (order == 2 ? v.k2s : v.k4s)<<<grid, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
-  else (order == 2 ? v.k2 : v.k4)<<<grid, 192, v.smem, s>>>(L, omega, inv_h2, inv_d);
+  if (L.sw_npen > 0)
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true>)
+        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d);
+  else
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false>)
+        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d);
   note_launch();
   return true;
 }

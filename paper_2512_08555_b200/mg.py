@@ -35,7 +35,8 @@ class MgDesc(C.Structure):
                 ("block_size", C.c_int32), ("bc", C.c_int32 * 6), ("order", C.c_int32),
                 ("coarse_n", C.c_int32), ("smoother", C.c_int32), ("omega", C.c_double),
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
-                ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32))]
+                ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
+                ("zsplit", C.c_int32), ("fuse", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -164,6 +165,10 @@ class Solver:
         d.eta1 = int(cfg["eta1"])
         d.eta2 = int(cfg["eta2"])
         d.allow_unbounded_refined = int(cfg.get("allow_unbounded_refined", 0))
+        # kernel-variant controls (tests only; 0 = automatic)
+        d.pencil_blocks = int(cfg.get("pencil_blocks", 0))
+        d.zsplit = int(cfg.get("zsplit", 0))
+        d.fuse = int(cfg.get("fuse", 0))
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))
         self.B = int(cfg["B"])

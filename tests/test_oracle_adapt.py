@@ -120,3 +120,49 @@ def test_host_abi_adapt_matches_oracle(bc):
         assert np.array_equal(a, b) and sa == sb
         Lay.check_layout(dom, a)
         lv = a
+
+
+def _unbalanced_nest():
+    """ADVICE r1 regression: 3^3 unbounded base, levels 0/1/2 nested around block
+    (1,1,1) without the 2:1 ring (used to loop forever)."""
+    lv = [(0, i, j, k) for k in range(3) for j in range(3) for i in range(3) if (i, j, k) != (1, 1, 1)]
+    kids = [(1, 2 + i, 2 + j, 2 + k) for k in range(2) for j in range(2) for i in range(2)]
+    lv += [c for c in kids if c != (1, 2, 2, 2)]
+    lv += [(2, 4 + i, 4 + j, 4 + k) for k in range(2) for j in range(2) for i in range(2)]
+    return np.array(lv, dtype=np.int32)
+
+
+def test_adapt_rejects_invalid_input():
+    lv = _unbalanced_nest()
+    g = np.full(len(lv), 0.5)
+    with pytest.raises(OA.LayoutError) as e:
+        OA.adapt((3, 3, 3), (1, 1, 1), lv, g, 1.0, 0.1, 3)
+    assert e.value.kind == "2:1"
+    dup = np.concatenate([lv[:1], lv])
+    with pytest.raises(OA.LayoutError):
+        OA.adapt((3, 3, 3), (1, 1, 1), dup, np.full(len(dup), 0.5), 1.0, 0.1, 3)
+    hole = lv[1:]                                      # level 0 not covered
+    with pytest.raises(OA.LayoutError):
+        OA.adapt((3, 3, 3), (1, 1, 1), hole, np.full(len(hole), 0.5), 1.0, 0.1, 3)
+
+
+def test_host_abi_adapt_rejects_invalid_input():
+    import ctypes as Cc
+    import os
+    from paper_2512_08555_b200.mg import _LIB_PATH, load_library
+    if not os.path.exists(_LIB_PATH):
+        pytest.skip("libmg.so not built")
+    lib = load_library()
+    I32 = Cc.c_int32
+    bb = (I32 * 3)(3, 3, 3)
+    bc = (I32 * 6)(1, 1, 1, 1, 1, 1)
+    for lv, code in ((_unbalanced_nest(), -3), (np.concatenate([_unbalanced_nest()[:1], _unbalanced_nest()]), -2),
+                     (_unbalanced_nest()[1:], -2)):
+        lv = np.ascontiguousarray(lv, dtype=np.int32)
+        g = np.full(len(lv), 0.5)
+        out = np.zeros((4096, 4), dtype=np.int32)
+        n_out = I32()
+        rc = lib.mg_adapt(bb, bc, 0, lv.ctypes.data_as(Cc.POINTER(I32)), len(lv),
+                          g.ctypes.data_as(Cc.POINTER(Cc.c_double)), 1.0, 0.1, 3,
+                          out.ctypes.data_as(Cc.POINTER(I32)), 4096, Cc.byref(n_out), None)
+        assert rc == code, (rc, code)

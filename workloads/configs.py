@@ -132,7 +132,12 @@ CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cache")
 
 def _cache_path(cfg) -> str:
     keys = ("source", "seed", "base_blocks", "max_level", "target_leaves", "h0", "origin", "bc", "B", "tube_R")
-    txt = json.dumps({k: cfg.get(k) for k in keys}, sort_keys=True, default=list) + f"v{LAYOUT_VERSION}"
+    key = {k: cfg.get(k) for k in keys}
+    if cfg.get("source") == "tube":
+        # the refinement indicator of the tube is ω of a tube widened by 4 h0 (source_fn):
+        # part of the recipe, so part of the key
+        key["indicator"] = "omega(R + 4 h0)"
+    txt = json.dumps(key, sort_keys=True, default=list) + f"v{LAYOUT_VERSION}"
     return os.path.join(CACHE_DIR, f"{cfg['name']}_{hashlib.sha1(txt.encode()).hexdigest()[:12]}.npz")
 
 
