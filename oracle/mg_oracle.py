@@ -13,6 +13,11 @@ images by wrap), coarse-to-fine interpolation (c2f) from W_{k-1} at resolution
 jumps / exterior nodes, or the last coarse-solve band at the coarsest level.
 Extended arrays carry a pad of width E on every axis.  NaN marks "undefined";
 a NaN reaching a result means a value outside the method's footprint was used.
+A level whose full lattice is large (deep adaptive layouts, > WINDOW_NODES nodes) is
+stored on a *window*: the bounding box [lo, lo + n) of its blocks (nodes outside it
+are not level-k nodes; the pad beyond the window holds ghost positions like any
+other).  Every inter-level map goes through level-global indices J (coarse J <-> fine
+2J), so a window only shifts array indices; the arithmetic is the same.
 
 Paper passages (PAPER.md line numbers, P:n):
 * Alg. 1 adaptive FAS V(η1,η2)-cycle ............................ P:137-168
@@ -50,6 +55,7 @@ JACOBI, RBGS = 0, 1
 E = 8          # pad width of extended arrays (even; > the widest exterior band)
 GE = 5         # exterior band width computed by the coarse solve (reading Z21/U1), M <= 4
 GE6 = 7        # M = 6: the I = 8 c2f chain of U1 reaches 6 nodes beyond the faces (Z6/U1)
+WINDOW_NODES = 1 << 22   # levels with more lattice nodes are stored on their block bounding box
 
 
 # ----------------------------------------------------------------------------------
@@ -191,47 +197,63 @@ class Oracle:
             L.amr = a
             L.N = (N0 >> (-a)) if a < 0 else (N0 << a)
             L.h = float(desc["h0"]) * (2.0 ** (-a))
-            L.mask = np.zeros(tuple(L.N), dtype=bool)
             self.levels.append(L)
-        # masks: AMR level a holds leaves at a and ancestors of deeper leaves
+        # level-k blocks: leaves at k and ancestors of deeper leaves (sub-base: all)
+        blocks = [set() for _ in self.levels]
         for lev, bi, bj, bk in self.leaves.tolist():
-            c = np.array([bi, bj, bk])
+            c = (bi, bj, bk)
             for a in range(lev, -1, -1):
-                Lv = self.levels[nsub + a]
-                s = c * self.B
-                Lv.mask[s[0]:s[0] + self.B, s[1]:s[1] + self.B, s[2]:s[2] + self.B] = True
-                c = c // 2
-        for m in range(nsub):
-            self.levels[m].mask[...] = True
+                blocks[nsub + a].add(c)
+                c = (c[0] // 2, c[1] // 2, c[2] // 2)
+        for m, L in enumerate(self.levels):
+            # storage window [lo, lo + n): the whole lattice, or the block bounding box
+            if m < nsub or int(np.prod(L.N)) <= WINDOW_NODES:
+                L.lo, L.n = np.zeros(3, dtype=np.int64), L.N.copy()
+            else:
+                cs = np.array(sorted(blocks[m]), dtype=np.int64)
+                L.lo = cs.min(axis=0) * self.B
+                L.n = (cs.max(axis=0) + 1) * self.B - L.lo
+                for ax in range(3):
+                    # a periodic axis is windowed only if the wrap images of the blocks
+                    # stay out of the pad (else stored whole, wrap by index)
+                    if self.per[ax] and L.n[ax] > L.N[ax] - 2 * E:
+                        L.lo[ax], L.n[ax] = 0, L.N[ax]
+            L.full = tuple(bool(L.lo[ax] == 0 and L.n[ax] == L.N[ax]) for ax in range(3))
+            L.mask = np.zeros(tuple(L.n), dtype=bool)
+            if m < nsub:
+                L.mask[...] = True
+            for c in blocks[m]:
+                s0 = np.array(c) * self.B - L.lo
+                L.mask[s0[0]:s0[0] + self.B, s0[1]:s0[1] + self.B, s0[2]:s0[2] + self.B] = True
         for m, L in enumerate(self.levels):
             if m + 1 < len(self.levels):
-                fm = self.levels[m + 1].mask
-                L.cov = fm[::2, ::2, ::2].copy()      # coarse i covered iff fine 2i in a level-(m+1) block
+                # coarse J covered iff fine 2J is a level-(m+1) block node
+                L.cov = self._down(L, self.levels[m + 1], self.levels[m + 1].mask, False)
             else:
-                L.cov = np.zeros(tuple(L.N), dtype=bool)
+                L.cov = np.zeros(tuple(L.n), dtype=bool)
             L.cov &= L.mask
             L.leaf = L.mask & ~L.cov
-            n = tuple(L.N)
+            n = tuple(L.n)
             L.u = np.zeros(n)
             L.f = np.zeros(n)
             L.r = np.zeros(n)
             L.uhat = np.zeros(n)
-            L.mask_ext = self._pad(L.mask.astype(np.float64), fill=0.0) > 0.5
+            L.mask_ext = self._pad(L.mask.astype(np.float64), fill=0.0, L=L) > 0.5
             L.parity_ext = self._parity_ext(L)
         c = self.levels[0]
-        if not c.mask.all():
+        if not c.mask.all() or not all(c.full):
             raise ValueError("coarsest level must cover the domain")
         c.band = np.zeros(tuple(c.N + 2 * E))        # exterior values of the last coarse solve
         self.fstar_norm = None
         self._coarse_setup()
 
     # --------------------------------------------------------------- extended arrays
-    def _pad(self, A, fill=np.nan):
-        """Extend an interior array by E on every axis: periodic axes by wrap,
-        unbounded axes with `fill` (exterior)."""
+    def _pad(self, A, fill=np.nan, L=None):
+        """Extend a level array by E on every axis: periodic axes stored whole by wrap,
+        unbounded axes and windowed axes with `fill` (exterior / not a level node)."""
         X = A
         for ax in range(3):
-            if self.per[ax]:
+            if self.per[ax] and (L is None or L.full[ax]):
                 n = X.shape[ax]
                 X = np.take(X, np.arange(-E, n + E) % n, axis=ax)
             else:
@@ -242,42 +264,59 @@ class Oracle:
         return X
 
     def _parity_ext(self, L):
-        idx = [np.arange(-E, n + E) for n in L.N]
+        idx = [np.arange(-E, n + E) + lo for n, lo in zip(L.n, L.lo)]
         J = np.meshgrid(*idx, indexing="ij")
         return ((J[0] + J[1] + J[2]) % 2 == 0)
 
     def _interior(self, X, L):
-        return X[E:E + L.N[0], E:E + L.N[1], E:E + L.N[2]]
+        return X[E:E + L.n[0], E:E + L.n[1], E:E + L.n[2]]
 
     def _exterior_ext(self, L):
         """True at extended positions outside an unbounded face."""
-        ext = np.zeros(tuple(L.N + 2 * E), dtype=bool)
+        ext = np.zeros(tuple(L.n + 2 * E), dtype=bool)
         for ax in range(3):
             if not self.per[ax]:
-                sl = [slice(None)] * 3
-                sl[ax] = slice(0, E)
-                ext[tuple(sl)] = True
-                sl[ax] = slice(E + L.N[ax], None)
-                ext[tuple(sl)] = True
+                J = np.arange(-E, L.n[ax] + E) + L.lo[ax]
+                out = (J < 0) | (J >= L.N[ax])
+                sh = [1, 1, 1]
+                sh[ax] = -1
+                ext |= out.reshape(sh)
         return ext
 
+    def _down(self, Lc, Lf, A, fill=np.nan):
+        """Coarse-window array of the fine values at the coincident nodes: out(J) =
+        A(2J) (injection geometry, E7), `fill` where 2J lies outside the fine window."""
+        out = np.full(tuple(Lc.n), fill, dtype=A.dtype)
+        idx, ok = [], []
+        for ax in range(3):
+            i = 2 * (np.arange(Lc.n[ax]) + Lc.lo[ax]) - Lf.lo[ax]
+            v = (i >= 0) & (i < Lf.n[ax])
+            idx.append(np.where(v, i, 0))
+            ok.append(v)
+        sub = A[np.ix_(*idx)]
+        valid = ok[0][:, None, None] & ok[1][None, :, None] & ok[2][None, None, :]
+        out[valid] = sub[valid]
+        return out
+
     # --------------------------------------------------------------- c2f (a1-iii)
-    def _c2f_axis(self, W, ax, nf):
-        """Refine W (extended coarse, along ax) to the extended fine lattice of
-        nf interior nodes: fine J even -> coarse J/2; J odd -> centred I-point
-        Lagrange midpoint rule on coarse (J-1)/2 - I/2 + 1 … (J-1)/2 + I/2."""
+    def _c2f_axis(self, W, ax, Lc, Lf):
+        """Refine W (extended coarse array of level Lc, along ax) to the extended fine
+        array of level Lf: fine J even -> coarse J/2; J odd -> centred I-point
+        Lagrange midpoint rule on coarse (J-1)/2 - I/2 + 1 … (J-1)/2 + I/2.
+        Extended position p <-> level-global J = p - E + lo (E and lo are even, so p
+        has the parity of J)."""
         Wm = np.moveaxis(W, ax, 0)
         nce = Wm.shape[0]
+        nf = int(Lf.n[ax])
+        lof, loc = int(Lf.lo[ax]), int(Lc.lo[ax])
         out = np.full((nf + 2 * E,) + Wm.shape[1:], np.nan)
         I = self.I
-        # E is even, so extended position p = J + E has the parity of J.
-        # even J = 2q -> coarse extended index q + E/2 ... written per position set:
         pe = np.arange(0, nf + 2 * E, 2)                 # J even
-        qe = (pe - E) // 2 + E
+        qe = (pe - E + lof) // 2 - loc + E
         ok = (qe >= 0) & (qe < nce)
         out[pe[ok]] = Wm[qe[ok]]
         po = np.arange(1, nf + 2 * E, 2)                 # J odd
-        base = (po - E - 1) // 2 - I // 2 + 1 + E
+        base = (po - E + lof - 1) // 2 - I // 2 + 1 - loc + E
         ok = (base >= 0) & (base + I - 1 < nce)
         po, base = po[ok], base[ok]
         acc = np.zeros((len(po),) + Wm.shape[1:])
@@ -286,11 +325,11 @@ class Oracle:
         out[po] = acc
         return np.moveaxis(out, 0, ax)
 
-    def c2f(self, W, Lf):
+    def c2f(self, W, Lc, Lf):
         """Tensor product of the 1D rule (reading Z7: tensor product at edges/corners)."""
         X = W
         for ax in range(3):
-            X = self._c2f_axis(X, ax, int(Lf.N[ax]))
+            X = self._c2f_axis(X, ax, Lc, Lf)
         return X
 
     # --------------------------------------------------------------- value lookup (O2)
@@ -299,7 +338,7 @@ class Oracle:
         ghosts from c2f of W_{m-1} (jump and exterior nodes, m >= 1), the last
         coarse-solve band (m = 0, exterior='band') or 0 (exterior='zero', for f)."""
         L = self.levels[m]
-        A = self._pad(vals[m])
+        A = self._pad(vals[m], L=L)
         if L.mask_ext.all():
             return A                                  # no ghost nodes on this level
         if m == 0:
@@ -325,7 +364,7 @@ class Oracle:
                                     Gm[E + n + k] = -Gm[E + n - k]
                             G = np.moveaxis(Gm, 0, ax)
         else:
-            G = self.c2f(self.source_W(m - 1, vals, exterior), L)
+            G = self.c2f(self.source_W(m - 1, vals, exterior), self.levels[m - 1], L)
             if exterior == "zero":
                 G[self._exterior_ext(L)] = 0.0       # f := 0 beyond unbounded faces (Z16)
         return np.where(L.mask_ext, A, G)
@@ -337,8 +376,8 @@ class Oracle:
         L = self.levels[m]
         fine = vals[m + 1]
         Am = vals[m].copy()
-        Am[L.cov] = fine[::2, ::2, ::2][L.cov]
-        X = np.where(L.mask_ext, self._pad(Am), np.nan)
+        Am[L.cov] = self._down(L, self.levels[m + 1], fine)[L.cov]
+        X = np.where(L.mask_ext, self._pad(Am, L=L), np.nan)
         ext = self._exterior_ext(L)
         if ext.any():
             v2 = list(vals)
@@ -373,11 +412,11 @@ class Oracle:
         d = diag_L(L.h, self.order)
         if self.smoother == JACOBI:
             Lx = apply_L(X, L.h, self.order)
-            U = X + self.omega * (self._pad(L.f, 0.0) - Lx) / d
+            U = X + self.omega * (self._pad(L.f, 0.0, L) - Lx) / d
             L.u = np.where(L.mask, self._interior(U, L), L.u)
             return
         ghosts = np.where(L.mask_ext, np.nan, X)      # frozen boundary ghosts
-        Fext = self._pad(L.f, 0.0)
+        Fext = self._pad(L.f, 0.0, L)
         for colour in (True, False):
             Lx = apply_L(X, L.h, self.order)
             U = X + self.omega * (Fext - Lx) / d
@@ -386,7 +425,7 @@ class Oracle:
             # re-impose periodic images of the updated interior, keep frozen ghosts
             newu = self._interior(Unew, L)
             L.u = np.where(L.mask, newu, L.u)
-            X = np.where(L.mask_ext, self._pad(L.u), ghosts)
+            X = np.where(L.mask_ext, self._pad(L.u, L=L), ghosts)
 
     def restrict(self, m):
         """Alg. 1: on the Ω_m-covered nodes of level m-1
@@ -395,11 +434,11 @@ class Oracle:
         finally û_{m-1} <- u_{m-1} on every level-(m-1) node (reading Z13-W)."""
         L, C = self.levels[m], self.levels[m - 1]
         r = self.residual(m)
-        C.u = np.where(C.cov, L.u[::2, ::2, ::2], C.u)
-        R = self._pad(np.where(L.mask, r, 0.0), fill=0.0)
+        C.u = np.where(C.cov, self._down(C, L, L.u), C.u)
+        R = self._pad(np.where(L.mask, r, 0.0), fill=0.0, L=L)
         for ax in range(3):
             R = 0.25 * _shift(R, ax, -1) + 0.5 * R + 0.25 * _shift(R, ax, 1)
-        Rint = self._interior(R, L)[::2, ::2, ::2]
+        Rint = self._down(C, L, self._interior(R, L))
         C.r = np.where(C.cov, Rint, 0.0)
         Lc = self.Lu(m - 1)
         C.f = np.where(C.cov, C.r + Lc, C.f)
@@ -415,7 +454,7 @@ class Oracle:
         per axis, fine J even -> coarse J/2, J odd -> mean of (J-1)/2 and (J+1)/2."""
         L, C = self.levels[m], self.levels[m - 1]
         eps = np.where(C.mask, C.u - C.uhat, 0.0)
-        X = self._pad(eps, fill=0.0)
+        X = self._pad(eps, fill=0.0, L=C)
         # exterior band (U1): ε = current exterior value - its snapshot at restriction;
         # jump ghosts keep ε := 0 (Z13-W)
         ext = self._exterior_ext(C)
@@ -425,14 +464,15 @@ class Oracle:
         for ax in range(3):
             Xm = np.moveaxis(X, ax, 0)
             nce = Xm.shape[0]
-            nf = int(L.N[ax])
+            nf = int(L.n[ax])
+            lof, loc = int(L.lo[ax]), int(C.lo[ax])       # extended p <-> J = p - E + lo
             out = np.full((nf + 2 * E,) + Xm.shape[1:], np.nan)
             pe = np.arange(0, nf + 2 * E, 2)
-            qe = (pe - E) // 2 + E
+            qe = (pe - E + lof) // 2 - loc + E
             ok = (qe >= 0) & (qe < nce)
             out[pe[ok]] = Xm[qe[ok]]
             po = np.arange(1, nf + 2 * E, 2)
-            qo = (po - E - 1) // 2 + E
+            qo = (po - E + lof - 1) // 2 - loc + E
             ok = (qo >= 0) & (qo + 1 < nce)
             out[po[ok]] = 0.5 * (Xm[qo[ok]] + Xm[qo[ok] + 1])
             X = np.moveaxis(out, 0, ax)
@@ -442,7 +482,7 @@ class Oracle:
         """u_{m-1}[covered] <- u_m(2i), finest to coarsest (E7; canonical state)."""
         for m in range(len(self.levels) - 1, 0, -1):
             L, C = self.levels[m], self.levels[m - 1]
-            C.u = np.where(C.cov, L.u[::2, ::2, ::2], C.u)
+            C.u = np.where(C.cov, self._down(C, L, L.u), C.u)
 
     # --------------------------------------------------------------- coarse solve (a6)
     def _coarse_setup(self):
@@ -639,18 +679,22 @@ class Oracle:
         c.band = band
 
     # --------------------------------------------------------------- API-level ops
+    def _local(self, lev, bi, bj, bk):
+        """Array index of node (0,0,0) of leaf block (lev, bi, bj, bk) in its level's window."""
+        L = self.levels[self.nsub + lev]
+        return tuple(int(c * self.B - L.lo[a]) for a, c in enumerate((bi, bj, bk)))
+
     def set_rhs(self, f_leaves):
         """O5: place f on leaf nodes, inject up the tree (f2c), f* = R_h^M f on
         leaves via the lookup with f := 0 beyond unbounded faces (Z16)."""
         B = self.B
-        fraw = [np.zeros(tuple(L.N)) for L in self.levels]
+        fraw = [np.zeros(tuple(L.n)) for L in self.levels]
         for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
-            L = fraw[self.nsub + lev]
-            L[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B] = \
-                np.asarray(f_leaves[n]).transpose(2, 1, 0)
+            i, j, k = self._local(lev, bi, bj, bk)
+            fraw[self.nsub + lev][i:i + B, j:j + B, k:k + B] = np.asarray(f_leaves[n]).transpose(2, 1, 0)
         for m in range(len(self.levels) - 1, 0, -1):
             C = self.levels[m - 1]
-            fraw[m - 1] = np.where(C.cov, fraw[m][::2, ::2, ::2], fraw[m - 1])
+            fraw[m - 1] = np.where(C.cov, self._down(C, self.levels[m], fraw[m]), fraw[m - 1])
         for ax in range(3):
             if self.sym[ax] < 0:          # odd face: the wall plane is u = 0, f there ignored (S1)
                 sl = [slice(None)] * 3
@@ -666,17 +710,16 @@ class Oracle:
     def set_solution(self, u_leaves):
         B = self.B
         for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
-            L = self.levels[self.nsub + lev]
-            L.u[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B] = \
-                np.asarray(u_leaves[n]).transpose(2, 1, 0)
+            i, j, k = self._local(lev, bi, bj, bk)
+            self.levels[self.nsub + lev].u[i:i + B, j:j + B, k:k + B] = np.asarray(u_leaves[n]).transpose(2, 1, 0)
         self.inject_up()
 
     def get_solution(self):
         B = self.B
         out = np.empty((len(self.leaves), B, B, B))
         for n, (lev, bi, bj, bk) in enumerate(self.leaves.tolist()):
-            L = self.levels[self.nsub + lev]
-            out[n] = L.u[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B, bk * B:(bk + 1) * B].transpose(2, 1, 0)
+            i, j, k = self._local(lev, bi, bj, bk)
+            out[n] = self.levels[self.nsub + lev].u[i:i + B, j:j + B, k:k + B].transpose(2, 1, 0)
         return out
 
     def vcycle(self, n=1):

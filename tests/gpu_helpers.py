@@ -3,18 +3,21 @@ storage (exported through mg_debug_field) and the oracle's dense level lattices.
 import numpy as np
 
 
-def blocks_to_dense(blocks, coords, B, N, fill=np.nan):
-    """blocks [n, B, B, B] ([b, z, y, x]) at block coords -> dense [Nx, Ny, Nz]."""
-    out = np.full(tuple(N), fill)
-    for b, (i, j, k) in enumerate(coords.tolist()):
-        out[i * B:(i + 1) * B, j * B:(j + 1) * B, k * B:(k + 1) * B] = blocks[b].transpose(2, 1, 0)
+def blocks_to_dense(blocks, coords, B, n, lo=(0, 0, 0), fill=np.nan):
+    """blocks [nb, B, B, B] ([b, z, y, x]) at block coords -> the oracle's level array
+    [nx, ny, nz] over the window [lo, lo + n) of level-global node indices."""
+    out = np.full(tuple(n), fill)
+    for b, c in enumerate(coords.tolist()):
+        i, j, k = (c[a] * B - lo[a] for a in range(3))
+        out[i:i + B, j:j + B, k:k + B] = blocks[b].transpose(2, 1, 0)
     return out
 
 
-def dense_to_blocks(dense, coords, B):
+def dense_to_blocks(dense, coords, B, lo=(0, 0, 0)):
     out = np.empty((len(coords), B, B, B))
-    for b, (i, j, k) in enumerate(coords.tolist()):
-        out[b] = dense[i * B:(i + 1) * B, j * B:(j + 1) * B, k * B:(k + 1) * B].transpose(2, 1, 0)
+    for b, c in enumerate(coords.tolist()):
+        i, j, k = (c[a] * B - lo[a] for a in range(3))
+        out[b] = dense[i:i + B, j:j + B, k:k + B].transpose(2, 1, 0)
     return out
 
 
@@ -49,12 +52,13 @@ class Pair:
         from paper_2512_08555_b200 import MG_FIELD_F, MG_FIELD_R, MG_FIELD_U, MG_FIELD_UHAT
         code = dict(u=MG_FIELD_U, f=MG_FIELD_F, r=MG_FIELD_R, uhat=MG_FIELD_UHAT)[field]
         t = self.g.debug_field(code, m).cpu().numpy()
-        return blocks_to_dense(t, self.coords[m], self.B[m], self.o.levels[m].N)
+        L = self.o.levels[m]
+        return blocks_to_dense(t, self.coords[m], self.B[m], L.n, L.lo)
 
     def push(self, field, m, dense):
         from paper_2512_08555_b200 import MG_FIELD_F, MG_FIELD_R, MG_FIELD_U, MG_FIELD_UHAT
         code = dict(u=MG_FIELD_U, f=MG_FIELD_F, r=MG_FIELD_R, uhat=MG_FIELD_UHAT)[field]
-        t = self.torch.from_numpy(dense_to_blocks(dense, self.coords[m], self.B[m])).cuda()
+        t = self.torch.from_numpy(dense_to_blocks(dense, self.coords[m], self.B[m], self.o.levels[m].lo)).cuda()
         self.g.debug_field(code, m, t)
 
     def push_state(self):
@@ -78,6 +82,7 @@ class Pair:
         nreal = self.g.level_info(m)["nreal"]
         B = self.B[m]
         N = self.o.levels[m].N
+        lo = self.o.levels[m].lo
         per = self.o.per
         for g in range(nreal, len(coords)):
             c = coords[g]
@@ -86,7 +91,7 @@ class Pair:
             for lz in range(B):
                 for ly in range(B):
                     for lx in range(B):
-                        X = (c[0] * B + lx + E, c[1] * B + ly + E, c[2] * B + lz + E)
+                        X = (c[0] * B + lx + E - lo[0], c[1] * B + ly + E - lo[1], c[2] * B + lz + E - lo[2])
                         if all(0 <= X[a] < ext_arr.shape[a] for a in range(3)) and np.isfinite(ext_arr[X]):
                             allb[g, lz, ly, lx] = ext_arr[X]
         self.g.debug_field(code, m, self.torch.from_numpy(allb).cuda(), ghosts=True)

@@ -101,3 +101,33 @@ def test_block_size_8_parity(B):
         p.o.vcycle(1)
         p.g.vcycle(1)
     assert rel_err(p.solution(), p.o.get_solution()) < 1e-9
+
+
+@pytest.mark.gpu
+def test_variant_controls_rejected():
+    d = _base()
+    lv = Lay.uniform_leaves(C.domain(d))
+    assert _err_code(_base(pencil_blocks=3), lv) == MG_ERR_ARG
+    assert _err_code(_base(zsplit=3), lv) == MG_ERR_ARG
+    assert _err_code(_base(fuse=2), lv) == MG_ERR_ARG
+
+
+@pytest.mark.gpu
+def test_cauchy_criterion_on_device_matches_oracle():
+    """E20 on the singular periodic adaptive problem, where the residual
+    stalls: the device-side Cauchy criterion stops after the same number of cycles as
+    the oracle's, with the same increment; an unknown criterion is MG_ERR_ARG."""
+    import torch
+
+    from paper_2512_08555_b200 import MgError
+    from tests.test_gpu_parity import _cfg
+    cfg, lv, f = _cfg("per_adapt")
+    p = Pair(cfg, lv, f)
+    cyc_o, hist = p.o.solve(1e-9, max_cycles=25, criterion="cauchy")
+    cyc_g, val_g, ok = p.g.solve(1e-9, 25, 1)
+    assert ok and cyc_g == cyc_o, (cyc_g, cyc_o)
+    assert abs(val_g - hist[-1]) <= 1e-6 * hist[-1] + 1e-15, (val_g, hist[-1])
+    assert rel_err(p.solution(), p.o.get_solution()) < 1e-9
+    with pytest.raises(MgError) as e:
+        p.g.solve(1e-9, 3, 7)
+    assert e.value.code == MG_ERR_ARG

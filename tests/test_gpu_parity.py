@@ -112,9 +112,19 @@ def _cfg(name):
     elif name == "per_adapt":
         return _periodic_adaptive()
     elif name == "cfg4_small":
-        c = C.cfg4(base=4, max_level=1, target=60)
+        # the cfg4 recipe (3 levels, blobs, PUU) on a 4^3 base: 302 leaves, jumps on
+        # both AMR levels; level 2 on an oracle window (256 x 64 x 64, x periodic whole)
+        c = C.cfg4(base=4, max_level=2, target=300)
+    elif name == "cfg5_small":
+        # the cfg5 recipe (5 levels, perturbed torus, PUU) with a smaller torus on a 4^3
+        # base: 568 leaves, AMR levels 0-4, levels 2-4 on oracle windows (x partial)
+        c = C.cfg5(base=4, max_level=4, target=1000, R=0.12, sigma=0.02)
     elif name == "cfg3_64":
         c = C.cfg3(64, coarse_n=16)
+    elif name == "cfg2_128":             # a level of >= 148 blocks (512)
+        c = C.cfg2(128)
+    elif name == "cfg3_128":
+        c = C.cfg3(128, coarse_n=32)
     elif name == "cfg2_64_m6":           # 6th-order Mehrstellen (E13)
         c = C.cfg2(64)
         c["order"] = 6
@@ -169,7 +179,7 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 2), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("oo_pp", 3), ("eo_uu", 3), ("oo_up_m6", 2), ("ppu", 2), ("upu", 2),
+                                         ("puu2", 2), ("cfg4_small", 3), ("cfg5_small", 3), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("oo_pp", 3), ("eo_uu", 3), ("oo_up_m6", 2), ("ppu", 2), ("upu", 2),
                                          ("upp", 2), ("cfg2_64_m6", 3), ("puu1_m6", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
@@ -235,7 +245,7 @@ def _prepared(name, warm=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg1", "cfg3_64", "cfg2_64_m6", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6", "cfg4_small", "cfg5_small"])
 def test_op_smooth(name):
     p = _prepared(name)
     for m in range(1, len(p.o.levels)):
@@ -247,7 +257,7 @@ def test_op_smooth(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6", "cfg5_small"])
 def test_op_residual(name):
     p = _prepared(name)
     for m in range(0, len(p.o.levels)):
@@ -261,7 +271,7 @@ def test_op_residual(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6", "cfg5_small"])
 def test_op_restrict(name):
     p = _prepared(name)
     for m in range(len(p.o.levels) - 1, 0, -1):
@@ -276,7 +286,7 @@ def test_op_restrict(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu2", "per_adapt", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_up_m6", "oo_pp", "oo_up_m6", "cfg5_small"])
 def test_op_prolong(name):
     p = _prepared(name)
     rng = np.random.default_rng(5)
@@ -325,7 +335,7 @@ def test_set_rhs_fstar_parity(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["puu2", "per_adapt", "cfg4_small", "cfg5_small", "cfg3_64", "puu1_m6", "cfg3_64_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
 def test_op_ghost_fill(name):
     """Boundary-ghost fill (a1: f2c injection + c2f, exterior chain U1) of every level:
     GPU ghost-block values vs the oracle's lookup V_m(J) at every halo node (within
@@ -353,7 +363,7 @@ def test_op_ghost_fill(name):
                 for ly in range(B):
                     for lx in range(B):
                         J = (c[0] * B + lx, c[1] * B + ly, c[2] * B + lz)
-                        X = tuple(J[a] + E for a in range(3))
+                        X = tuple(J[a] + E - L.lo[a] for a in range(3))
                         if not all(0 <= X[a] < halo.shape[a] for a in range(3)) or not halo[X]:
                             continue
                         n += 1

@@ -1,0 +1,128 @@
+"""Parity of every kernel variant the automatic choice takes at full size, on small
+layouts (the production variants — 2- and 4-block pencils, sweeps without
+the z-split, the fused residual+restriction and fused last-pre-sweep kernels next to
+jump and exterior ghost blocks — must match the oracle element-wise).
+
+mg_desc.pencil_blocks / zsplit / fuse force the variant (include/mg.h); the oracle is
+the same for all of them.  Tolerances as in test_gpu_parity: ≤1e-12 per operator,
+≤1e-9 on u after V-cycles.
+"""
+import numpy as np
+import pytest
+
+from tests.gpu_helpers import Pair, rel_err
+from tests.test_gpu_parity import CYCLE_TOL, OP_TOL, _cfg, _prepared
+
+LAYOUTS = ["puu2", "cfg3_64", "ou_uu", "per_adapt", "cfg2_64"]
+VARIANTS = [dict(pencil_blocks=1, zsplit=1), dict(pencil_blocks=1, zsplit=2), dict(pencil_blocks=2),
+            dict(pencil_blocks=4), dict(pencil_blocks=2, fuse=1)]
+
+
+def _vid(v):
+    return "-".join(f"{k[0]}{v[k]}" for k in sorted(v))
+
+
+def _with(name, variant, order=None):
+    cfg, lv, f = _cfg(name)
+    cfg = dict(cfg)
+    cfg.update(variant)
+    if order:
+        cfg["order"] = order
+    return cfg, lv, f
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [4, 6])
+@pytest.mark.parametrize("variant", VARIANTS, ids=_vid)
+@pytest.mark.parametrize("name", LAYOUTS)
+def test_vcycle_parity_variants(name, variant, order):
+    cfg, lv, f = _with(name, variant, order)
+    p = Pair(cfg, lv, f)
+    for c in range(2):
+        p.o.vcycle(1)
+        p.g.vcycle(1)
+        e = rel_err(p.solution(), p.o.get_solution())
+        assert e < CYCLE_TOL, (name, variant, c, e)
+    ro, rg = p.o.residual_norm(), p.g.residual_norm()
+    assert abs(rg[1] - ro[1]) <= 1e-6 * ro[1] + 1e-12, (rg, ro)
+
+
+def _prep(name, variant, order):
+    import tests.test_gpu_parity as T
+    orig = T._cfg
+    T._cfg = lambda n: _with(n, variant, order)
+    try:
+        return _prepared(name)
+    finally:
+        T._cfg = orig
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("order", [4, 6])
+@pytest.mark.parametrize("variant", VARIANTS, ids=_vid)
+@pytest.mark.parametrize("name", ["puu2", "cfg3_64", "ou_uu"])
+def test_ops_parity_variants(name, variant, order):
+    """smooth, residual (and the composite norm), restrict (+ FAS RHS + û), prolong."""
+    p = _prep(name, variant, order)
+    top = len(p.o.levels) - 1
+    # residual first: the per-operator order matters on the oracle side, whose ghost
+    # refresh never writes the coarse covered nodes (the GPU's f2c injection does; in
+    # Alg. 1 the restriction overwrites them before any coarse residual reads them)
+    for m in range(0, top + 1):
+        L = p.o.levels[m]
+        r = p.o.residual(m)
+        p.g.debug_apply("residual", m)
+        Lu = p.o.Lu(m)
+        den = max(np.abs(L.f[L.mask]).max(), np.abs(Lu[L.mask]).max())
+        e = rel_err(p.gpu_field("r", m)[L.mask], r[L.mask], den)
+        assert e < OP_TOL, ("residual", m, e)
+    assert abs(p.g.residual_norm()[0] - p.o.residual_norm()[0]) <= OP_TOL * max(1.0, p.o.fstar_norm) * 1e2
+    for m in range(1, top + 1):
+        p.o.smooth(m)
+        p.g.debug_apply("smooth", m)
+        L = p.o.levels[m]
+        e = rel_err(p.gpu_field("u", m)[L.mask], L.u[L.mask])
+        assert e < OP_TOL, ("smooth", m, e)
+    for m in range(top, 0, -1):
+        p.o.restrict(m)
+        p.g.debug_apply("restrict", m)
+        C_ = p.o.levels[m - 1]
+        for fld, ref in (("u", C_.u), ("f", C_.f), ("uhat", C_.uhat)):
+            e = rel_err(p.gpu_field(fld, m - 1)[C_.cov], ref[C_.cov])
+            assert e < OP_TOL, ("restrict", m, fld, e)
+    for m in range(1, top + 1):
+        p.o.prolong(m)
+        p.g.debug_apply("prolong", m)
+        L = p.o.levels[m]
+        e = rel_err(p.gpu_field("u", m)[L.mask], L.u[L.mask])
+        assert e < OP_TOL, ("prolong", m, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [dict(), dict(pencil_blocks=4), dict(fuse=1)], ids=_vid)
+@pytest.mark.parametrize("name", ["cfg2_128", "cfg3_128"])
+def test_large_level_parity(name, variant):
+    """Levels of >= 148 blocks (512 at 128^3): the automatic choice there is 1-block
+    pencils without z-split; forced 4-block pencils and unfused kernels too."""
+    cfg, lv, f = _with(name, variant)
+    p = Pair(cfg, lv, f)
+    assert p.g.level_info(len(p.o.levels) - 1)["nreal"] >= 148
+    for c in range(2):
+        p.o.vcycle(1)
+        p.g.vcycle(1)
+        e = rel_err(p.solution(), p.o.get_solution())
+        assert e < CYCLE_TOL, (name, c, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", [dict(pencil_blocks=2), dict(pencil_blocks=4), dict(pencil_blocks=1, zsplit=1)],
+                         ids=_vid)
+def test_cfg5_shaped_variants(variant):
+    """The 5-level PUU torus layout (cfg5 recipe, reduced) with forced pencil lengths."""
+    cfg, lv, f = _with("cfg5_small", variant)
+    p = Pair(cfg, lv, f)
+    for c in range(3):
+        p.o.vcycle(1)
+        p.g.vcycle(1)
+        e = rel_err(p.solution(), p.o.get_solution())
+        assert e < CYCLE_TOL, (variant, c, e)

@@ -61,14 +61,16 @@ def cfg4(base=8, max_level=2, target=2000):
                 target_leaves=target, cycles=0, tol=1e-10)
 
 
-def cfg5(base=8, max_level=4, target=30000):
+def cfg5(base=8, max_level=4, target=30000, R=0.5, sigma=0.03):
     """Adaptive 5-level grid (~30k leaf blocks) around a perturbed torus, x periodic,
-    y/z unbounded on [-1,1)^3, M=4, RB V(2,2), to 1e-10 (configs[4])."""
-    return dict(name="cfg5" if base == 8 else f"cfg5_b{base}", origin=(-1.0, -1.0, -1.0),
+    y/z unbounded on [-1,1)^3, M=4, RB V(2,2), to 1e-10 (configs[4]).  A smaller torus
+    (R, sigma) on a smaller base keeps all 5 levels at oracle-sized windows (tests)."""
+    full = base == 8 and R == 0.5 and sigma == 0.03
+    return dict(name="cfg5" if full else f"cfg5_b{base}_l{max_level}_R{R}", origin=(-1.0, -1.0, -1.0),
                 h0=2 / (16 * base), base_blocks=(base,) * 3, B=16,
                 bc=(PERIODIC, UNBOUNDED, UNBOUNDED), order=4, smoother=RBGS, omega=1.0,
                 eta1=2, eta2=2, coarse_n=0, max_level=max_level, source="torus", seed=5,
-                target_leaves=target, cycles=0, tol=1e-10)
+                target_leaves=target, cycles=0, tol=1e-10, torus_R=R, torus_sigma=sigma)
 
 
 def tube(base=8, max_level=1, target=3000, nz_blocks=None, order=4, R=0.25):
@@ -116,7 +118,8 @@ def source_fn(cfg):
         return lambda x, y, z: S.blobs_eval(p, x, y, z, Lx=L)
     if s == "torus":
         p = S.torus_params(cfg.get("seed", 5))
-        return lambda x, y, z: S.torus_eval(p, x, y, z)
+        R, sg = cfg.get("torus_R", 0.5), cfg.get("torus_sigma", 0.03)
+        return lambda x, y, z: S.torus_eval(p, x, y, z, R=R, sigma=sg)
     if s == "tube":   # refinement score only (the solve takes the components of -∇×ω)
         # ω of a tube widened by 4 level-0 spacings: the level-0 nodes next to the
         # refined region must not reach the steep edge of the compact bump with the
@@ -133,6 +136,8 @@ CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cache")
 def _cache_path(cfg) -> str:
     keys = ("source", "seed", "base_blocks", "max_level", "target_leaves", "h0", "origin", "bc", "B", "tube_R")
     key = {k: cfg.get(k) for k in keys}
+    if cfg.get("source") == "torus" and (cfg.get("torus_R", 0.5), cfg.get("torus_sigma", 0.03)) != (0.5, 0.03):
+        key["torus"] = [cfg["torus_R"], cfg["torus_sigma"]]
     if cfg.get("source") == "tube":
         # the refinement indicator of the tube is ω of a tube widened by 4 h0 (source_fn):
         # part of the recipe, so part of the key
