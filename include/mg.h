@@ -101,6 +101,10 @@ typedef struct mg_desc {
                                 0 auto (levels with fewer blocks than SMs), 1 never, 2 always */
   int32_t fuse;              /* 0 auto: fused pencil kernels where eligible (last pre-sweep +
                                 residual + restriction; residual + restriction); 1 never fuse */
+  int32_t staging;           /* plane tiles of the RB sweep: 0 cp.async ring (default, the
+                                fastest measured), 1 TMA tensor copies (cp.async.bulk.tensor, 9
+                                boxes per field and plane) into an mbarrier ring; measured 2.5x
+                                slower on B200; same values bit for bit */
 } mg_desc;
 
 /* Validate the layout (nesting, 2:1, unbounded-face rule), build the level

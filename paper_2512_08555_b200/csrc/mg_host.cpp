@@ -99,12 +99,16 @@ struct Level {
   std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
   std::vector<uint32_t> nbr_real, nbr_ext;
+  bool has_ext_ghosts = false;  // some real block has a ghost neighbour beyond an unbounded face
   std::vector<uint8_t> covmask, c2f_ext;
   int bmap_lo[3] = {0, 0, 0}, bmap_n[3] = {1, 1, 1};
   // device
   double* u[2] = {nullptr, nullptr};
   double *f = nullptr, *r = nullptr, *uhat = nullptr;
   int cur = 0;
+  // TMA tensor maps of the RB sweep, per ping-pong parity: (u[cur], f)
+  TileMaps tmaps[2];
+  bool has_tmaps = false;
   int32_t *d_nbr = nullptr, *d_parent = nullptr, *d_bmap = nullptr, *d_c2f_dst = nullptr, *d_c2f_J = nullptr,
           *d_inj_dst = nullptr, *d_inj_src = nullptr, *d_pen_blk = nullptr, *d_pen_len = nullptr,
           *d_gbox = nullptr, *d_sw_blk = nullptr, *d_sw_len = nullptr, *d_sw_z = nullptr;
@@ -292,8 +296,8 @@ void validate_and_build(mg_handle* h) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
     if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
-    if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1))
-      throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse 0..1");
+    if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1 || d.staging < 0 || d.staging > 1))
+      throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse and staging 0..1");
     // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
     // the low face with an unbounded high face (reading S1)
     const int lo = d.bc[2 * a], hi = d.bc[2 * a + 1];
@@ -648,7 +652,10 @@ void build_ghosts(mg_handle* h) {
         if (idx < 0) throw MgError(MG_ERR_LAYOUT_GHOST, "missing neighbour block");
         l.nbr[27 * (size_t)i + o] = idx;
         if (idx < l.nreal) l.nbr_real[i] |= 1u << o;
-        else if (l.ghost_ext[idx - l.nreal]) l.nbr_ext[i] |= 1u << o;
+        else if (l.ghost_ext[idx - l.nreal]) {
+          l.nbr_ext[i] |= 1u << o;
+          l.has_ext_ghosts = true;
+        }
       }
     }
     int lo[3], hi[3];
@@ -878,6 +885,16 @@ void alloc_device(mg_handle* h) {
     l.d_sw_len = dev_upload(l.sw_len);
     l.d_sw_z = dev_upload(l.sw_z);
   }
+  // TMA tensor maps of the B = 16 levels (RB sweep plane tiles) when TMA staging is
+  // requested (mg_desc.staging = 1; cp.async otherwise, or without a tensor-map encoder)
+  for (auto& l : h->L) {
+    l.has_tmaps = false;
+    if (l.B != 16 || h->d.staging != 1) continue;
+    bool ok = true;
+    for (int c = 0; c < 2 && ok; ++c)
+      ok = encode_tile_maps(l.u[c], l.ntot(), l.tmaps[c].u) && encode_tile_maps(l.f, l.ntot(), l.tmaps[c].f);
+    l.has_tmaps = ok;
+  }
   // leaf map: leaf n -> (level, block)
   std::vector<int64_t> map(h->leaves.size());
   for (size_t n = 0; n < h->leaves.size(); ++n) {
@@ -1096,7 +1113,7 @@ void sweep(mg_handle* h, int m, bool with_res) {
   {
     Prof pr(h, ST_SMOOTH, m);
     const LevelView v = view(h, m);
-    if (mode != SM_RB || !launch_rb_pencil(v, h->order, h->omega, h->s))
+    if (mode != SM_RB || !launch_rb_pencil(v, h->order, h->omega, l.has_tmaps ? &l.tmaps[l.cur] : nullptr, h->s))
       launch_smooth(v, h->order, mode, h->omega, false, h->s);
     swap_u(l);
   }
@@ -1133,8 +1150,16 @@ void restrict_level(mg_handle* h, int m) {
   }
   refresh(h, m - 1);
   Prof pr(h, ST_RESTRICT, m);
-  if (!launch_fas_pencil(view(h, m - 1), h->order, h->s)) launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
-  CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+  if (launch_fas_pencil(view(h, m - 1), h->order, h->s)) {
+    // the pencil FAS kernel wrote û on the real blocks; the prolongation also takes ε on
+    // the exterior band (reading Z13-W, U1 / level 0), stored in the ghost blocks
+    if (C.has_ext_ghosts)
+      CUDA_OK(cudaMemcpyAsync(C.uhat + (size_t)C.nreal * C.B3, C.u[C.cur] + (size_t)C.nreal * C.B3,
+                              (size_t)C.nghost * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+  } else {
+    launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
+    CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+  }
 }
 
 // u_m += P(u - û)_{m-1} (Alg. 1).  Under U1 the exterior band of level m-1

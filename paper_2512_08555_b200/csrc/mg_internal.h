@@ -2,6 +2,7 @@
 // (mg_host.cpp) and the sm_100a kernels (mg_kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace mg {
@@ -42,6 +43,17 @@ struct LevelView {
   const int32_t* sw_pen_z;
 };
 
+// TMA tensor maps of one B = 16 level's u (current buffer) and f arrays, each viewed as a
+// 4-D tensor [ntot][16][16][16] fp64 (x fastest), one map per box shape of the plane-tile
+// pieces (mg_pencil.cu TmaTile): 0 = 16 x 16, 1 = 2 x 16, 2 = 16 x 2, 3 = 2 x 2 (x by y, one
+// plane, one block).  Passed to the kernels by value (__grid_constant__).
+struct TileMaps {
+  CUtensorMap u[4];
+  CUtensorMap f[4];
+};
+// encode the 4 maps of an array of `ntot` 16^3 blocks; false if the driver lacks TMA
+bool encode_tile_maps(const double* base, int ntot, CUtensorMap out[4]);
+
 struct C2FList {           // boundary-ghost entries of one level
   int n;
   const int32_t* dst;      // flat index into the level arrays
@@ -63,7 +75,7 @@ void launch_smooth(const LevelView& L, int order, int mode, double omega, bool w
                    cudaStream_t s);
 void launch_residual(const LevelView& L, int order, cudaStream_t s);
 // z-marching pencil kernels (B = 16 levels); return false if the level is not eligible
-bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s);
+bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMaps* tm, cudaStream_t s);
 bool launch_norm_pencil(const LevelView& L, int order, unsigned long long* out, cudaStream_t s);
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
 // FAS right-hand side f = r + Δu on the covered nodes of a coarse level (B = 16)

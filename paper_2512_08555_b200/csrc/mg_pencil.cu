@@ -18,6 +18,7 @@
 // Boundary-ghost nodes (ghost blocks: c2f at resolution jumps, exterior band) are
 // frozen during a sweep (reading Z9): halo nodes in non-real blocks keep their value.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
 #include <type_traits>
@@ -43,6 +44,58 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers (sm_90+/sm_100a PTX)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// generic-proxy accesses of shared memory ordered before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+// 4-D tiled TMA load: box at (c0, c1, c2, c3) of the tensor map into shared memory,
+// completion counted on the mbarrier in bytes
+__device__ __forceinline__ void tma_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// TMA plane tile: the 20 x 20 halo tile of one z-plane (x, y in [-2, 18)) as 9 dense
+// pieces, one per (sx, sy) in {-1, 0, 1}^2 = the neighbour block it comes from (sx =
+// -1: x in [14, 16) of the left block, ...): TMA writes boxes densely, so each piece
+// has its own row pitch (its box width) and starts 128-byte aligned.  448 doubles
+// (3584 B) per field and plane.
+struct TmaTile {
+  static constexpr int N = 448;
+  // piece p = (sx + 1) + 3 (sy + 1): offset (doubles) and row pitch
+  __host__ __device__ static constexpr int off(int p) {
+    return p == 0 ? 384 : p == 1 ? 320 : p == 2 ? 400 : p == 3 ? 256 : p == 4 ? 0 : p == 5 ? 288 : p == 6 ? 416
+                                                                                                 : p == 7 ? 352 : 432;
+  }
+  __host__ __device__ static constexpr int pitch(int p) { return (p % 3 == 1) ? 16 : 2; }
+  // tile position (x, y) in [-2, 18)^2 -> doubles from the field's piece-set base
+  __device__ static int at(int x, int y) {
+    const int sx = x < 0 ? -1 : (x >= PB ? 1 : 0), sy = y < 0 ? -1 : (y >= PB ? 1 : 0);
+    const int p = (sx + 1) + 3 * (sy + 1);
+    const int lx = sx < 0 ? x + 2 : (sx > 0 ? x - PB : x), ly = sy < 0 ? y + 2 : (sy > 0 ? y - PB : y);
+    return off(p) + ly * pitch(p) + lx;
+  }
+};
 
 // Source block / z-local index of plane z of a pencil of `len` blocks (planes
 // [-H, 16 len + H)): below the pencil -> neighbour slot dz = -1 of its first block,
@@ -74,7 +127,7 @@ __device__ __forceinline__ void plane_src(int z, int nz, int len, int& k, int& d
 // operands are old values; for a black node the faces are red (new, after the red
 // phase) and the edges and centre black (old).
 // ---------------------------------------------------------------------------------
-template <int D, int RR>
+template <int D, int RR, bool TMA = false>
 struct RBShape {
   static constexpr int T = PB + 4;                 // 20: x, y in [-2, 18)
   // row pitch 26 doubles: a warp's 3 same-parity rows (2 apart, 416 B ≡ 32 mod 128)
@@ -87,13 +140,19 @@ struct RBShape {
   static constexpr int NLD = (NPAIR + NT - 1) / NT;  // 2
   // red-phase values, one per pair: [2 planes][18 rows][pitch 13] (conflict-free)
   static constexpr int SNW = 13, SNP = 18 * SNW;
-  // [R][TP] old u | [2][SNP] red-phase values | [R][NT] f pairs
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + 2 * SNP + R * NT * 2);
+  // cp.async: [R][TP] old u | [2][SNP] red-phase values | [R][NT] f pairs
+  // TMA:      [R][u pieces | f pieces] (R x 7168 B, 128-B aligned) | [2][SNP] red-phase values
+  static constexpr int SLOT = 2 * TmaTile::N;  // TMA: doubles per ring slot
+  static constexpr size_t SMEM = TMA ? sizeof(double) * (size_t)(R * SLOT + 2 * SNP) + 128
+                                     : sizeof(double) * (size_t)(R * TP + 2 * SNP + R * NT * 2);
+  static constexpr unsigned PLANE_BYTES = 2 * 400 * sizeof(double);  // TMA bytes per plane (u and f tiles)
   static_assert(D + 2 <= R, "ring too small for the prefetch depth");
 };
 
 struct RBCtx {
   const int* snb;
+  uint64_t* bar;     // TMA: one mbarrier per ring slot
+  const TileMaps* tm;
   const uint32_t* sreal;
   double* su;
   double* sn;
@@ -107,10 +166,10 @@ struct RBCtx {
 __device__ __forceinline__ double shfl_up1(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 __device__ __forceinline__ double shfl_dn1(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
 
-template <int ORDER, int D, int RR, int RP, bool SW>
+template <int ORDER, int D, int RR, int RP, bool SW, bool TMA>
 __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int wg, int lane, double omega,
                                         double inv_h2, double inv_d) {
-  using S = RBShape<D, RR>;
+  using S = RBShape<D, RR, TMA>;
   constexpr int TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NLD = S::NLD, SNW = S::SNW, SNP = S::SNP;
   constexpr int PC = RP;  // column (0 = a = x0, 1 = b = x0+1) that is red at even planes
   const int* snb = cx.snb;
@@ -131,6 +190,12 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   const int sxy = (dxc + 1) + 3 * (dyc + 1);
   const int fxy = (cy - PB * dyc) * PB + (x0 - PB * dxc);
   const bool inner = valid && dxc == 0 && dyc == 0;
+  // TMA tile: offsets (< 448, 9 bits each) of this pair's rows cy-1, cy, cy+1 in a
+  // plane's u pieces, packed in one register (the f pair sits at the cy offset of the f
+  // pieces, which follow the u pieces in a slot)
+  const unsigned ro = TMA ? (unsigned)TmaTile::at(x0, cy - 1) | ((unsigned)TmaTile::at(x0, cy) << 9) |
+                                ((unsigned)TmaTile::at(x0, cy + 1) << 18)
+                          : 0u;
 
   // ---- plane cursors: source pointers change only at block boundaries (z % 16 == 0)
   // and at the pencil ends; between them they advance by one plane (PB^2 doubles).
@@ -150,7 +215,32 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   // stage plane z (called for z = zlo-2, zlo-1, … in order) into ring slot (z+2) & (R-1).
   // In the step loop z = 4 (zq + t) + j + D - 2 with j, D compile-time, so the slot and
   // the block-boundary test fold to constants (zlo ≡ 0 mod 4).
+  // TMA staging: lanes 0..17 of warp 0 each load one of the 9 u / 9 f pieces of plane z
+  // (lane 0 arms the slot's mbarrier with the plane's byte count first)
+  auto issue_tma = [&](int z, auto checked) {
+    if (decltype(checked)::value && z >= zhi + 2) return;
+    if (tid >= 18) return;
+    const int slot = (z + 2) & (R - 1);
+    int k, dz, zl;
+    const int len = *cx.glen;
+    plane_src(z, PB * len, len, k, dz, zl);
+    const int p = tid % 9, sx = p % 3 - 1, sy = p / 3 - 1;
+    const int mi = (sx != 0) + 2 * (sy != 0);
+    const CUtensorMap* map = tid < 9 ? &cx.tm->u[mi] : &cx.tm->f[mi];
+    const int blk = snb[k * 27 + p + 9 * (dz + 1)];
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(cx.bar + slot, S::PLANE_BYTES);
+    }
+    __syncwarp(0x3ffffu);
+    tma_load4(su + slot * S::SLOT + (tid < 9 ? 0 : TmaTile::N) + TmaTile::off(p), map, sx < 0 ? 14 : 0,
+              sy < 0 ? 14 : 0, zl, blk, cx.bar + slot);
+  };
   auto issue = [&](int z, auto checked) {
+    if constexpr (TMA) {
+      issue_tma(z, checked);
+      return;
+    }
     if (!decltype(checked)::value || z < zhi + 2) {
       if ((z & 15) == 0) seek_issue(z);
       const int slot = (z + 2) & (R - 1);
@@ -173,7 +263,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
     plane_src(z, PB * len, len, k, dz, zl);
     live = valid && ((cx.sreal[k] >> (sxy + 9 * (dz + 1))) & 1u);
   };
-  seek_issue(zlo - 2);
+  if (!TMA) seek_issue(zlo - 2);
   seek_live(zlo - 1);
 #pragma unroll
   for (int q = 0; q < D; ++q) issue(zlo - 2 + q, std::true_type{});
@@ -208,15 +298,21 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       const int s = base - 2 + j;
       const int X = (j & 1) ? PC : 1 - PC;  // red at s-1 (black at s and s-2); base even
       const int O = 1 - X;                  // red at s (and s-2)
-      cpa_wait<D - 1>();
+      if constexpr (TMA) {
+        // plane s: slot (s+2) & (R-1), used for the ((s+2) >> 2)-th time (R = 4)
+        if (!LAST || s < zhi + 2) mbar_wait(cx.bar + ((s + 2) & (R - 1)), ((s + 2 - (zlo & ~3)) >> 2) & 1);
+      } else {
+        cpa_wait<D - 1>();
+      }
       __syncthreads();
       issue(s + D, std::integral_constant<bool, LAST>{});
       double cq[2], s4q[2], d4q[2];
       {
-        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
-        const double2 m = *reinterpret_cast<const double2*>(U - TW);
+        const double* Us = su + ((s + 2) & (R - 1)) * (TMA ? S::SLOT : TP);
+        const double* U = Us + (TMA ? (ro >> 9) & 511u : i0);
+        const double2 m = *reinterpret_cast<const double2*>(TMA ? Us + (ro & 511u) : U - TW);
         const double2 cc = *reinterpret_cast<const double2*>(U);
-        const double2 p = *reinterpret_cast<const double2*>(U + TW);
+        const double2 p = *reinterpret_cast<const double2*>(TMA ? Us + (ro >> 18) : U + TW);
         const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);  // u(x0-1), u(x0+2)
         cq[0] = cc.x;
         cq[1] = cc.y;
@@ -237,7 +333,9 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
       if (!FIRST || j >= 2) {  // red half-sweep at plane r = s-1 in [zlo-1, zhi] (column X)
         if (((s - 1) & 15) == 0) seek_live(s - 1);
         fb = X ? fr.y : fr.x;                 // f at plane s-2 of column X (pair read last step)
-        fr = sfme[((s + 1) & (R - 1)) * NT];  // f pair at plane s-1
+        // f pair at plane s-1
+        fr = TMA ? *reinterpret_cast<const double2*>(su + ((s + 1) & (R - 1)) * S::SLOT + TmaTile::N + ((ro >> 9) & 511u))
+                 : sfme[((s + 1) & (R - 1)) * NT];
         double v = cR[X];
         if (live) {
           const double Lu = ORDER == 4 ? (accR[X] + alpha) * h6 : (accR[X] + alpha) * inv_h2;
@@ -273,20 +371,26 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
   group(4 * zq, std::integral_constant<int, 0>{});
   for (int t = 1; t < nt - 1; ++t) group(4 * (zq + t), std::integral_constant<int, 1>{});
   group(4 * (zq + nt - 1), std::integral_constant<int, 2>{});
-  cpa_wait<0>();
+  if (!TMA) cpa_wait<0>();
 }
 
-template <int ORDER, int D, int RR, int NREG, bool SW>
+template <int ORDER, int D, int RR, int NREG, bool SW, bool TMA>
 __global__ void __maxnreg__(NREG)
-    k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
-  using S = RBShape<D, RR>;
+    k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d, const __grid_constant__ TileMaps tm) {
+  using S = RBShape<D, RR, TMA>;
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(16) double smraw[];
   __shared__ int snb[PMAXL * 27];
   __shared__ uint32_t sreal[PMAXL];
   __shared__ int slen;
+  __shared__ __align__(8) uint64_t sbar[R];
+  // TMA destinations must be 128-byte aligned
+  double* sm = TMA ? reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127)) : smraw;
   const int tid = threadIdx.x;
   RBCtx cx;
+  cx.bar = sbar;
+  cx.tm = &tm;
+  if (TMA && tid < R) mbar_init(sbar + tid, 1);
   // sweep pencils (sw_*: may split a block into z-parts on small levels) or block pencils
   const bool sw = SW;
   cx.len = __ldg((sw ? L.sw_pen_len : L.pen_len) + blockIdx.x);
@@ -304,7 +408,7 @@ __global__ void __maxnreg__(NREG)
   cx.glen = &slen;
   if (tid == 0) slen = cx.len;
   cx.su = sm;
-  cx.sn = sm + R * TP;
+  cx.sn = sm + R * (TMA ? S::SLOT : TP);
   cx.sf = reinterpret_cast<double2*>(sm + R * TP + 2 * S::SNP);
   const int32_t* pb = sw ? L.sw_pen_blk + (size_t)blockIdx.x * L.sw_pen_lmax
                          : L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
@@ -330,11 +434,12 @@ __global__ void __maxnreg__(NREG)
     cx.ld_sxy[d] = j < NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
     cx.ld_dst[d] = py * TW + px;
   }
-  __syncthreads();  // snb / sreal
+  if (TMA && tid < R) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");  // inits -> async proxy
+  __syncthreads();  // snb / sreal / mbarriers
   // warp-uniform row parity: warps 0-2 even rows, 3-5 odd rows
   const int w = tid >> 5, lane = tid & 31;
-  if (w < 3) rb_body<ORDER, D, RR, 0, SW>(L, cx, w, lane, omega, inv_h2, inv_d);
-  else rb_body<ORDER, D, RR, 1, SW>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
+  if (w < 3) rb_body<ORDER, D, RR, 0, SW, TMA>(L, cx, w, lane, omega, inv_h2, inv_d);
+  else rb_body<ORDER, D, RR, 1, SW, TMA>(L, cx, w - 3, lane, omega, inv_h2, inv_d);
 }
 
 // ---------------------------------------------------------------------------------
@@ -596,7 +701,8 @@ struct ResShape {
 
 // MODE 0: r = f - Δ_h^M u (residual, Alg. 1) on every node of the pencil.
 // MODE 1: f = r + Δ_h^M u (FAS right-hand side on the coarse level, Alg. 1) on
-//         the nodes of octants covered by the finer level (covmask); others untouched.
+//         the nodes of octants covered by the finer level (covmask); others untouched;
+//         and û = u on every node of the pencil (the snapshot of Alg. 1).
 // MODE 2: max |f - Δ_h^M u| over the nodes of uncovered octants (the composite residual
 //         norm of the stopping test) as the bit pattern of a non-negative double
 //         (NaN -> quiet-NaN pattern, above +Inf), atomicMax-ed into *out; nothing written.
@@ -705,6 +811,7 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
         const bool cov = (scov[r >> 4] >> oct) & 1;
         if (MODE == 1) {
           if (cov) L.f[o] = f + Lu;
+          L.uhat[o] = c1;  // the û snapshot (Alg. 1) of every real node, from the staged plane
         } else if (!cov) {
           const double v = fabs(f - Lu);
           unsigned long long bits = (unsigned long long)__double_as_longlong(v);
@@ -953,7 +1060,31 @@ constexpr int RES_D = 3;
 // <2,4,80> 96.8 us, <2,4,72> 102.4 (spills, still 4 CTAs/SM), <2,4,64> 100.6 (5 CTAs/SM,
 // 88 B of spills).
 constexpr int RB_D = 2, RB_R = 4, RB_NREG = 80;
-using RBS = RBShape<RB_D, RB_R>;
+using RBS = RBShape<RB_D, RB_R, false>;
+using RBT = RBShape<RB_D, RB_R, true>;
+
+bool encode_tile_maps(const double* base, int ntot, CUtensorMap out[4]) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!enc || !base || ntot <= 0) return false;
+  const cuuint64_t dims[4] = {PB, PB, PB, (cuuint64_t)ntot};
+  const cuuint64_t strides[3] = {PB * sizeof(double), PB * PB * sizeof(double), (cuuint64_t)PB3 * sizeof(double)};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  for (int mi = 0; mi < 4; ++mi) {
+    const cuuint32_t box[4] = {(mi & 1) ? 2u : 16u, (mi & 2) ? 2u : 16u, 1u, 1u};
+    if (enc(&out[mi], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
 
 void prepare_pencil_kernels() {
   // the whole unified L1 as shared memory: several pencil CTAs per SM
@@ -961,10 +1092,14 @@ void prepare_pencil_kernels() {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   };
-  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, false>, RBS::SMEM);
-  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, false>, RBS::SMEM);
-  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, true>, RBS::SMEM);
-  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, true>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, false>, RBS::SMEM);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, true>, RBT::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, true>, RBT::SMEM);
+  setup((const void*)k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, true>, RBT::SMEM);
+  setup((const void*)k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, true>, RBT::SMEM);
   setup((const void*)k_rb6_pencil<RB6_NREG, false>, RB6Shape::SMEM);
   setup((const void*)k_rb6_pencil<RB6_NREG, true>, RB6Shape::SMEM);
   setup((const void*)k_rr2_pencil<2>, RR2Shape::SMEM);
@@ -995,7 +1130,7 @@ static bool res_pencil_launch(const LevelView& L, int order, unsigned long long*
   return true;
 }
 
-bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t s) {
+bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMaps* tm, cudaStream_t s) {
   if (L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   if (order == 6) {
     const double inv_h2 = 1.0 / (L.h * L.h);
@@ -1008,12 +1143,23 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, cudaStream_t 
   const double inv_h2 = 1.0 / (L.h * L.h);
   const double inv_d = 1.0 / ((order == 2 ? -6.0 : -4.0) * inv_h2);
   const int grid = L.sw_npen > 0 ? L.sw_npen : L.npen;
-  if (L.sw_npen > 0)
-    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true>)
-        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d);
-  else
-    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false>)
-        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d);
+  // tile staging by TMA (tensor maps given) or by cp.async
+  static const TileMaps none{};
+  const TileMaps& m = tm ? *tm : none;
+  if (tm) {
+    if (L.sw_npen > 0)
+      (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, true>)
+          <<<grid, RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+    else
+      (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, true>)
+          <<<grid, RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+  } else if (L.sw_npen > 0) {
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, false>)
+        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+  } else {
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>)
+        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+  }
   note_launch();
   return true;
 }

@@ -36,7 +36,7 @@ class MgDesc(C.Structure):
                 ("coarse_n", C.c_int32), ("smoother", C.c_int32), ("omega", C.c_double),
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
                 ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
-                ("zsplit", C.c_int32), ("fuse", C.c_int32)]
+                ("zsplit", C.c_int32), ("fuse", C.c_int32), ("staging", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -169,6 +169,7 @@ class Solver:
         d.pencil_blocks = int(cfg.get("pencil_blocks", 0))
         d.zsplit = int(cfg.get("zsplit", 0))
         d.fuse = int(cfg.get("fuse", 0))
+        d.staging = int(cfg.get("staging", 0))
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))
         self.B = int(cfg["B"])
