@@ -164,6 +164,11 @@ enum {
   MG_OP_SMOOTH_RESIDUAL = 7 /* fused last pre-sweep + residual (ghost-free levels) */
 };
 int mg_debug_apply(mg_handle* h, int op, int level);
+/* Debug (initcheck substitute): set every ghost-block node that no stencil, transfer
+ * or interpolation is designed to read (outside the needed halo) to NaN
+ * in all level fields.  Call after mg_set_rhs; a later result that reads one turns
+ * non-finite.  Synchronises. */
+int mg_debug_poison(mg_handle* h);
 /* Time one operator: runs it `reps` times between CUDA events, returns ms per rep. */
 int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out);
 

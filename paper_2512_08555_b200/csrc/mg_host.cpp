@@ -1359,7 +1359,7 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
                    h->s);
   }
-  if (!h->fwall.empty()) launch_zero_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, h->s);
+  if (!h->fwall.empty()) launch_fill_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, 0.0, h->s);
   if (!h->fm_dst.empty())
     launch_copy_signed((int)h->fm_dst.size(), h->d_fm_dst, h->d_fm_src, h->d_fm_sgn, h->L[0].f, h->L[0].f, h->s);
   for (int m = 0; m < nlev; ++m) {
@@ -1639,6 +1639,26 @@ static void apply_op(mg_handle* h, int op, int level) {
     case MG_OP_COARSE_SOLVE: coarse_solve(h); break;
     default: throw MgError(MG_ERR_ARG, "bad op");
   }
+}
+
+int mg_debug_poison(mg_handle* h) {
+  if (!h) return MG_ERR_ARG;
+  return guard(h, [&] {
+    // every ghost-block node outside the needed set (the halo the stencils may read,
+    // DESIGN.md §5) of every field := NaN; a kernel that reads one spreads it
+    const double nan = std::nan("");
+    for (auto& l : h->L) {
+      std::vector<int32_t> idx;
+      for (int gi = 0; gi < l.nghost; ++gi)
+        for (int loc = 0; loc < l.B3; ++loc)
+          if (!((l.need[gi][loc >> 6] >> (loc & 63)) & 1)) idx.push_back((l.nreal + gi) * l.B3 + loc);
+      if (idx.empty()) continue;
+      int32_t* d = dev_upload(idx);
+      for (double* p : {l.u[0], l.u[1], l.f, l.r, l.uhat}) launch_fill_list((int)idx.size(), d, p, nan, h->s);
+      CUDA_OK(cudaStreamSynchronize(h->s));
+      cudaFree(d);
+    }
+  });
 }
 
 int mg_debug_apply(mg_handle* h, int op, int level) {

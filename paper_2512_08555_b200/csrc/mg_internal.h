@@ -115,7 +115,7 @@ void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const
                           const int* off, cudaStream_t s);
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s);
-void launch_zero_list(int n, const int32_t* idx, double* d, cudaStream_t s);
+void launch_fill_list(int n, const int32_t* idx, double* d, double v, cudaStream_t s);  // d[idx[i]] = v
 void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
                         cudaStream_t s);
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s);

@@ -991,14 +991,14 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
   if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, A); ++g_nlaunch; }
 }
 
-__global__ void k_zero_list(int n, const int32_t* __restrict__ idx, double* d) {
+__global__ void k_fill_list(int n, const int32_t* __restrict__ idx, double* d, double v) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) d[idx[i]] = 0.0;
+  if (i < n) d[idx[i]] = v;
 }
 
-void launch_zero_list(int n, const int32_t* idx, double* d, cudaStream_t s) {
+void launch_fill_list(int n, const int32_t* idx, double* d, double v, cudaStream_t s) {
   if (n <= 0) return;
-  k_zero_list<<<(n + 255) / 256, 256, 0, s>>>(n, idx, d);
+  k_fill_list<<<(n + 255) / 256, 256, 0, s>>>(n, idx, d, v);
   ++g_nlaunch;
 }
 

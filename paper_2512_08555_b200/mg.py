@@ -26,7 +26,7 @@ MG_ALL_BLOCKS = 0x10000
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
            "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
-           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt"]
+           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison"]
 STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm"]
 
 
@@ -74,6 +74,7 @@ def load_library(path: str = _LIB_PATH):
     lib.mg_num_levels.argtypes = [P]
     lib.mg_debug_field.argtypes = [P, I, I, I, P]
     lib.mg_debug_apply.argtypes = [P, I, I]
+    lib.mg_debug_poison.argtypes = [P]
     lib.mg_time_op.argtypes = [P, I, I, I, C.POINTER(D)]
     lib.mg_profile.argtypes = [P, I]
     lib.mg_profile_read.argtypes = [P, C.POINTER(D), C.POINTER(C.c_int64)]
@@ -286,6 +287,10 @@ class Solver:
             self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 2 if ghosts else 0, _ptr(out)))
             return out
         self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 3 if ghosts else 1, _ptr(tensor)))
+
+    def debug_poison(self):
+        """NaN into every ghost-block node outside the needed halo (mg_debug_poison)."""
+        self._check(self.lib.mg_debug_poison(self.h))
 
     def debug_apply(self, op, m):
         self._check(self.lib.mg_debug_apply(self.h, OPS[op] if isinstance(op, str) else int(op), int(m)))
