@@ -45,12 +45,16 @@ typedef struct mg_handle mg_handle;
 
 /* boundary conditions, per face (-x,+x,-y,+y,-z,+z).  Per axis (low, high):
  * (PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), semi-unbounded (EVEN or ODD, UNBOUNDED)
- * (reading S1), or symmetric on both faces (ODD, ODD) / (EVEN, ODD) (homogeneous
- * Dirichlet / Neumann-Dirichlet; reading S2).  The low face mirrors about the node
- * plane x = 0 (EVEN: u(-k) = u(k); ODD: u(-k) = -u(k), so u(0) = 0 and f on that plane
- * is ignored); an ODD high face mirrors about the unstored node N (u(N) = 0).  Blocks
+ * (reading S1), or symmetric on both faces (ODD, ODD) / (EVEN, ODD) / (EVEN, EVEN)
+ * (homogeneous Dirichlet / Neumann-Dirichlet / Neumann; readings S2, S3).  The low
+ * face mirrors about the node plane x = 0 (EVEN: u(-k) = u(k); ODD: u(-k) = -u(k), so
+ * u(0) = 0 and f on that plane is ignored); an ODD high face mirrors about the unstored
+ * node N (u(N) = 0); an EVEN high face about the last stored node N-1 (the wall node is
+ * an unknown; u(N-1+k) = u(N-1-k)).  An (EVEN, EVEN) axis needs the other axes periodic
+ * or symmetric (else MG_ERR_BC); with no ODD face the problem is singular and the coarse
+ * solve takes the zero-average solution (f must be compatible).  Blocks
  * touching EVEN/ODD faces stay on AMR level 0, which must be the coarse-solve level
- * (coarse_n = 0, no U1).  An EVEN high face -> MG_ERR_BC (its wall node is not stored). */
+ * (coarse_n = 0, no U1). */
 enum { MG_BC_PERIODIC = 0, MG_BC_UNBOUNDED = 1, MG_BC_EVEN = 2, MG_BC_ODD = 3 };
 /* smoother ("an iteration of the Gauss-Seidel method"; readings Z10) */
 enum { MG_SMOOTHER_JACOBI = 0, MG_SMOOTHER_RBGS = 1 };

@@ -169,7 +169,7 @@ class Oracle:
         self.bcf = tuple(face_bc(b) for b in desc["bc"])
         for lo, hi in self.bcf:
             if (lo, hi) not in ((PERIODIC, PERIODIC), (UNBOUNDED, UNBOUNDED), (EVEN, UNBOUNDED), (ODD, UNBOUNDED),
-                                (ODD, ODD), (EVEN, ODD)):
+                                (ODD, ODD), (EVEN, ODD), (EVEN, EVEN)):
                 raise ValueError(f"unsupported face pair {(lo, hi)}")
         self.per = tuple(lo == PERIODIC for lo, hi in self.bcf)
         self.bc = tuple(PERIODIC if p else UNBOUNDED for p in self.per)   # per-axis kind (legacy use)
@@ -177,6 +177,11 @@ class Oracle:
         # face mirrors about the (unstored) node N: u(N) = 0, u(N+k) = -u(N-k) (reading S2)
         self.sym = tuple({EVEN: 1, ODD: -1}.get(lo, 0) for lo, hi in self.bcf)
         self.hi_odd = tuple(hi == ODD for lo, hi in self.bcf)
+        # (EVEN, EVEN): homogeneous Neumann on both faces (reading S3): the high wall
+        # is the last stored node N-1, u(N-1+k) = u(N-1-k); only with no unbounded axis
+        self.hi_even = tuple(lo == EVEN and hi == EVEN for lo, hi in self.bcf)
+        if any(self.hi_even) and any(lo == UNBOUNDED or hi == UNBOUNDED for lo, hi in self.bcf):
+            raise ValueError("(EVEN, EVEN) axes need the other axes periodic or symmetric")
         self.origin = np.asarray(desc["origin"], dtype=np.float64)
         self.leaves = np.asarray(leaves, dtype=np.int64)
         base = np.asarray(desc["base_blocks"], dtype=np.int64)
@@ -362,6 +367,10 @@ class Oracle:
                                 Gm[E + n] = 0.0
                                 for k in range(1, E):
                                     Gm[E + n + k] = -Gm[E + n - k]
+                            if self.hi_even[ax]:           # J = N - 1 + k <-> N - 1 - k (S3)
+                                n = int(L.N[ax])
+                                for k in range(1, E + 1):
+                                    Gm[E + n - 1 + k] = Gm[E + n - 1 - k]
                             G = np.moveaxis(Gm, 0, ax)
         else:
             G = self.c2f(self.source_W(m - 1, vals, exterior), self.levels[m - 1], L)
@@ -495,7 +504,7 @@ class Oracle:
         N = [2 * int(n) - 1 if semi[ax] else int(n) for ax, n in enumerate(c.N)]
         self.coff = [int(c.N[ax]) - 1 if semi[ax] else 0 for ax in range(3)]
         self.cN = N
-        if any(self.hi_odd):
+        if any(self.hi_odd) or any(self.hi_even):
             self.coarse_kind = "SS"        # a both-sided symmetric axis: _coarse_solve_ss
             return
         self.unb = [ax for ax in range(3) if not self.per[ax]]
@@ -550,14 +559,17 @@ class Oracle:
         instead of the standard discrete Fourier transform"; reading S2): ODD/ODD axes
         by the DST-I of the nodes 1..N-1 (u(0) = u(N) = 0, θ_k = πk/N), EVEN/ODD axes by
         the DCT-III of the nodes 0..N-1 (θ_k = π(2k+1)/(2N)), periodic axes by the DFT,
-        unbounded (and semi-unbounded, mirror-extended) axes by the zero-padded DFT.  No
-        mode has all-zero wavenumbers, so every mode takes 1/σ_M(θ) (reading Z22)."""
+        unbounded (and semi-unbounded, mirror-extended) axes by the zero-padded DFT,
+        EVEN/EVEN axes by the DCT-I of the nodes 0..N-1 (walls at nodes 0 and N-1,
+        θ_k = πk/(N-1); reading S3).  Every mode takes 1/σ_M(θ) (reading Z22) except the
+        one with all-zero wavenumbers (EVEN/EVEN with periodic axes only: the constant),
+        set to 0 (zero average of the coarse solution)."""
         import scipy.fft as sf
         c = self.levels[0]
         N = [int(n) for n in c.N]
         X = c.f.astype(np.float64).copy()
         for ax in range(3):               # mirror images across semi-unbounded low faces
-            if self.sym[ax] and not self.hi_odd[ax]:
+            if self.sym[ax] and not self.hi_odd[ax] and not self.hi_even[ax]:
                 fm = np.moveaxis(X, ax, 0)
                 img = self.sym[ax] * fm[:0:-1]
                 mid = fm[:1] if self.sym[ax] > 0 else 0.0 * fm[:1]
@@ -574,6 +586,10 @@ class Oracle:
                 # eigenvectors of the (non-symmetric) mirrored operator
                 X = sf.dct(X, type=3, axis=ax)
                 thetas.append(np.pi * (2 * np.arange(n) + 1) / (2 * n))
+            elif self.hi_even[ax]:                             # EVEN / EVEN
+                # DCT-I = the DFT of the even extension of period 2(N-1)
+                X = sf.dct(X, type=1, axis=ax)
+                thetas.append(np.pi * np.arange(n) / (n - 1))
             elif self.per[ax]:
                 thetas.append(None)
             else:                                              # unbounded / semi-unbounded
@@ -582,12 +598,14 @@ class Oracle:
                 shp[ax] = Pp - X.shape[ax]
                 X = np.concatenate([X, np.zeros(shp)], axis=ax)
                 thetas.append(None)
-        fft_axes = [ax for ax in range(3) if not self.hi_odd[ax]]
+        fft_axes = [ax for ax in range(3) if not self.hi_odd[ax] and not self.hi_even[ax]]
         for ax in fft_axes:
             thetas[ax] = 2 * np.pi * np.fft.fftfreq(X.shape[ax])
         Xc = np.fft.fftn(X, axes=fft_axes) if fft_axes else X
         TH = np.meshgrid(*thetas, indexing="ij")
-        Xc = Xc / symbol(self.order, TH, c.h)
+        sig = symbol(self.order, TH, c.h)
+        zero = sig == 0.0                     # the constant mode (only with EVEN/EVEN)
+        Xc = np.where(zero, 0.0, Xc / np.where(zero, 1.0, sig))
         X = np.fft.ifftn(Xc, axes=fft_axes).real if fft_axes else Xc
         for ax in range(3):
             if self.hi_odd[ax] and self.sym[ax] < 0:
@@ -597,6 +615,8 @@ class Oracle:
                 X = np.concatenate([np.zeros(shp), X], axis=ax)   # u(0) = 0
             elif self.hi_odd[ax]:
                 X = sf.idct(X, type=3, axis=ax)
+            elif self.hi_even[ax]:
+                X = sf.idct(X, type=1, axis=ax)
         # interior and exterior band: per axis a source index into X and a sign
         GEb = self.GE
         band = np.full(tuple(c.N + 2 * E), np.nan)
@@ -610,6 +630,10 @@ class Oracle:
                 i = np.where(J < 0, -J, np.where(J < n, J, 2 * n - J))
                 sg = np.where(J < 0, float(self.sym[ax]), np.where(J < n, 1.0, -1.0))
                 sg = np.where((J == n) | (J < -(n - 1)) | (J > 2 * n - 1), 0.0, sg)
+                i = np.clip(i, 0, n - 1)
+            elif self.hi_even[ax]:                 # mirrors about nodes 0 and N-1
+                i = np.where(J < 0, -J, np.where(J < n, J, 2 * (n - 1) - J))
+                sg = np.where((J < -(n - 1)) | (J > 2 * (n - 1)), np.nan, 1.0)
                 i = np.clip(i, 0, n - 1)
             else:
                 ok = (J >= -GEb) & (J < n + GEb)

@@ -130,6 +130,7 @@ struct mg_handle {
   int per[3] = {1, 1, 1};
   int sym[3] = {0, 0, 0};  // symmetric low face: mirror sign (+1 even, -1 odd), 0 none
   int hi_odd[3] = {0, 0, 0};  // odd high face (mirror about the unstored node N; reading S2)
+  int hi_even[3] = {0, 0, 0}; // (EVEN, EVEN) axis: walls at nodes 0 and N-1 (reading S3)
   int fper[3] = {1, 1, 1};    // axis periodic in the coarse-solve transform (P, or both faces symmetric)
   std::vector<int32_t> fwall;  // level-0 nodes on an odd low face: f := 0 there (u = 0)
   int32_t* d_fwall = nullptr;
@@ -302,15 +303,21 @@ void validate_and_build(mg_handle* h) {
     // the low face with an unbounded high face (reading S1)
     const int lo = d.bc[2 * a], hi = d.bc[2 * a + 1];
     const bool ok = (lo == MG_BC_PERIODIC && hi == MG_BC_PERIODIC) || (lo == MG_BC_UNBOUNDED && hi == MG_BC_UNBOUNDED) ||
-                    ((lo == MG_BC_EVEN || lo == MG_BC_ODD) && (hi == MG_BC_UNBOUNDED || hi == MG_BC_ODD));
-    if (!ok) throw MgError(MG_ERR_BC, "supported face pairs: P/P, U/U, EVEN/U, ODD/U, ODD/ODD, EVEN/ODD");
+                    ((lo == MG_BC_EVEN || lo == MG_BC_ODD) && (hi == MG_BC_UNBOUNDED || hi == MG_BC_ODD)) ||
+                    (lo == MG_BC_EVEN && hi == MG_BC_EVEN);
+    if (!ok) throw MgError(MG_ERR_BC, "supported face pairs: P/P, U/U, EVEN/U, ODD/U, ODD/ODD, EVEN/ODD, EVEN/EVEN");
     h->per[a] = lo == MG_BC_PERIODIC;
     h->sym[a] = lo == MG_BC_EVEN ? 1 : (lo == MG_BC_ODD ? -1 : 0);
     h->hi_odd[a] = hi == MG_BC_ODD;
-    h->fper[a] = h->per[a] || h->hi_odd[a];
+    h->hi_even[a] = lo == MG_BC_EVEN && hi == MG_BC_EVEN;
+    h->fper[a] = h->per[a] || h->hi_odd[a] || h->hi_even[a];
     if (h->sym[a] && (d.coarse_n > 0 || d.allow_unbounded_refined))
       throw MgError(MG_ERR_BC, "symmetric faces need AMR level 0 as the coarse-solve level and no U1");
   }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      if (h->hi_even[a] && (d.bc[2 * b] == MG_BC_UNBOUNDED || d.bc[2 * b + 1] == MG_BC_UNBOUNDED))
+        throw MgError(MG_ERR_BC, "an EVEN/EVEN axis needs the other axes periodic or symmetric");
   h->order = d.order;
   h->I = d.order + 2;
   h->GE = (d.order == 6 && d.allow_unbounded_refined) ? GE_M6U1 : GE_M4;
@@ -927,10 +934,11 @@ void setup_coarse(mg_handle* h) {
   for (int a = 0; a < 3; ++a) {
     // semi-unbounded: the mirror-extended axis of 2N-1 nodes, solved as unbounded;
     // both faces symmetric: the odd (2N) or even-odd (4N) periodic extension (S2)
-    const bool semi = h->sym[a] && !h->hi_odd[a];
+    const bool semi = h->sym[a] && !h->hi_odd[a] && !h->hi_even[a];
     const int Ne = semi ? 2 * c.N[a] - 1 : c.N[a];
     h->coff[a] = semi ? c.N[a] - 1 : 0;
     if (h->hi_odd[a]) h->P[a] = (h->sym[a] < 0 ? 2 : 4) * c.N[a];
+    else if (h->hi_even[a]) h->P[a] = 2 * (c.N[a] - 1);  // even extension about nodes 0 and N-1
     else h->P[a] = h->per[a] ? c.N[a] : smooth7(2 * Ne + 2 * h->GE - 1);
     nunb += !h->fper[a];
   }
@@ -1014,17 +1022,20 @@ void setup_coarse(mg_handle* h) {
   // level-0 exterior f ghosts beyond symmetric low faces: signed mirror copies of real
   // level-0 nodes (f := 0 beyond unbounded faces, Z16; reading S1)
   if (h->sym[0] || h->sym[1] || h->sym[2]) {
-    const Level& l = h->L[0];  // f beyond odd high faces mirrors too (hi_odd, reading S2)
+    const Level& l = h->L[0];  // f beyond odd / even high faces mirrors too (S2, S3)
     for (size_t e = 0; e < l.c2f_dst.size(); ++e) {
       int J[3] = {l.c2f_J[3 * e], l.c2f_J[3 * e + 1], l.c2f_J[3 * e + 2]};
       int sg = 1;
       bool zero = false;
       for (int a = 0; a < 3 && !zero; ++a) {
         if (h->per[a]) continue;
-        if ((J[a] >= l.N[a] && !h->hi_odd[a]) || (J[a] < 0 && !h->sym[a])) zero = true;  // beyond an unbounded face
+        if ((J[a] >= l.N[a] && !h->hi_odd[a] && !h->hi_even[a]) || (J[a] < 0 && !h->sym[a]))
+          zero = true;  // beyond an unbounded face
         else if (J[a] < 0) {
           J[a] = -J[a];
           sg *= h->sym[a];
+        } else if (J[a] >= l.N[a] && h->hi_even[a]) {  // even high face: f(N-1+k) = f(N-1-k)
+          J[a] = 2 * (l.N[a] - 1) - J[a];
         } else if (J[a] >= l.N[a]) {   // odd high face: f(N) = 0, f(N + k) = -f(N - k)
           if (J[a] == l.N[a]) zero = true;
           J[a] = 2 * l.N[a] - J[a];
@@ -1173,7 +1184,7 @@ void prolong_level(mg_handle* h, int m) {
 void coarse_solve(mg_handle* h) {
   Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
-  launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->hi_odd, h->coff, h->s);
+  launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->hi_odd, h->hi_even, h->coff, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
   if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
   else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);

@@ -112,7 +112,7 @@ void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, dou
                         unsigned long long* out, cudaStream_t s);
 // coarse solve helpers
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
-                          const int* off, cudaStream_t s);
+                          const int* hi_even, const int* off, cudaStream_t s);
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s);
 void launch_fill_list(int n, const int32_t* idx, double* d, double v, cudaStream_t s);  // d[idx[i]] = v

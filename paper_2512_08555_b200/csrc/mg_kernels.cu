@@ -899,7 +899,7 @@ void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, dou
 // (reading S1) hold the mirror-extended source on x = q - (N-1) in [-(N-1), N-1]:
 // J = |x|, times the face's sign for x < 0, and 0 at x = 0 for an odd face.
 struct CoarseAxes {
-  int P[3], sym[3], hi_odd[3], off[3];
+  int P[3], sym[3], hi_odd[3], hi_even[3], off[3];
 };
 
 __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
@@ -912,7 +912,11 @@ __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
   bool ok = true;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (A.hi_odd[a]) {
+    if (A.hi_even[a]) {
+      // walls at nodes 0 and N-1: even extension of period 2(N-1) (reading S3)
+      const int n = L.N[a], p = q[a];
+      J[a] = p < n ? p : 2 * (n - 1) - p;
+    } else if (A.hi_odd[a]) {
       // both faces symmetric: periodic extension of period 2N (odd/odd) or 4N (even/odd)
       const int n = L.N[a], p = q[a];
       if (A.sym[a] < 0) {
@@ -946,12 +950,13 @@ __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
 }
 
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
-                          const int* off, cudaStream_t s) {
+                          const int* hi_even, const int* off, cudaStream_t s) {
   CoarseAxes A;
   for (int a = 0; a < 3; ++a) {
     A.P[a] = P[a];
     A.sym[a] = sym[a];
     A.hi_odd[a] = hi_odd[a];
+    A.hi_even[a] = hi_even[a];
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)P[0] * P[1] * P[2];

@@ -33,7 +33,8 @@ def test_invalid_descriptions_return_codes():
     d = _base()
     lv = Lay.uniform_leaves(C.domain(d))
     assert _err_code(_base(order=8), lv) == MG_ERR_ORDER               # M in {2, 4, 6}
-    assert _err_code(_base(bc=(0, 2, 0)), lv) == MG_ERR_BC            # EVEN/ODD are reserved
+    assert _err_code(_base(bc=(1, 2, 1)), lv) == MG_ERR_BC            # EVEN/EVEN with unbounded axes
+    assert _err_code(_base(bc=(0, (3, 2), 0)), lv) == MG_ERR_BC       # ODD/EVEN is not a supported pair
     assert _err_code(_base(B=12), lv) == MG_ERR_ARG
     assert _err_code(d, lv[:-1]) == MG_ERR_LAYOUT_NESTING           # a hole in level 0
     # 2:1 violation: one level-0 block refined twice in a corner

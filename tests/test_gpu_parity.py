@@ -139,6 +139,14 @@ def _cfg(name):
         return _ss_adaptive((3, 3), (0, 0))
     elif name == "eo_uu":               # x Neumann / Dirichlet, y, z unbounded
         return _ss_adaptive((2, 3), (1, 1))
+    elif name == "ee_pp":               # x Neumann both faces (S3), y, z periodic: singular
+        return _ss_adaptive((2, 2), (0, 0))
+    elif name == "ee_eo_p":             # x Neumann, y Neumann / Dirichlet, z periodic
+        return _ss_adaptive((2, 2), ((2, 3), 0))
+    elif name == "ee_ee_ee_m6":         # pure Neumann box, M = 6
+        d, lv, f = _ss_adaptive((2, 2), ((2, 2), (2, 2)))
+        d["order"] = 6
+        return d, lv, f
     elif name == "oo_up_m6":
         d, lv, f = _ss_adaptive((3, 3), (1, 0))
         d["order"] = 6
@@ -179,7 +187,7 @@ def test_abi_exports_every_declared_symbol():
 # ------------------------------------------------------------------ V-cycle parity
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,cycles", [("cfg1", 10), ("cfg2_64", 3), ("per_adapt", 3), ("puu1", 3),
-                                         ("puu2", 2), ("cfg4_small", 3), ("cfg5_small", 3), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("oo_pp", 3), ("eo_uu", 3), ("oo_up_m6", 2), ("ppu", 2), ("upu", 2),
+                                         ("puu2", 2), ("cfg4_small", 3), ("cfg5_small", 3), ("cfg3_64", 3), ("cfg3_64_m6", 2), ("eu_pu", 3), ("ou_uu", 3), ("ou_up_m6", 2), ("oo_pp", 3), ("eo_uu", 3), ("oo_up_m6", 2), ("ee_pp", 3), ("ee_eo_p", 3), ("ee_ee_ee_m6", 2), ("ppu", 2), ("upu", 2),
                                          ("upp", 2), ("cfg2_64_m6", 3), ("puu1_m6", 3)])
 def test_vcycle_parity(name, cycles):
     cfg, lv, f = _cfg(name)
@@ -305,7 +313,7 @@ def test_op_prolong(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["cfg2_64", "puu1", "cfg1", "cfg3_64", "ppu", "upu", "upp", "pup", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6", "ee_pp", "ee_eo_p", "ee_ee_ee_m6"])
 def test_op_coarse_solve(name):
     p = _prepared(name)
     c = p.o.levels[0]
@@ -325,7 +333,8 @@ def test_op_coarse_solve(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu2", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6"])
+@pytest.mark.parametrize("name", ["puu2", "puu1_m6", "eu_pu", "ou_uu", "ou_up_m6", "oo_pp", "eo_uu", "oo_up_m6", "ee_pp",
+                                  "ee_eo_p", "ee_ee_ee_m6"])
 def test_set_rhs_fstar_parity(name):
     cfg, lv, f = _cfg(name)
     p = Pair(cfg, lv, f)

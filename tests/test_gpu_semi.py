@@ -74,3 +74,31 @@ def test_symmetric_both_faces_eigenmode_gpu(pair, k):
     u = s.get_solution().cpu().numpy()
     assert np.abs(u - uexp).max() <= 1e-11 * np.abs(uexp).max()
     assert s.residual_norm()[1] < 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,order", [(3, 4), (7, 6)])
+def test_even_even_eigenmode_gpu(k, order):
+    """Homogeneous Neumann on both x faces (walls at nodes 0 and N-1; reading S3) with y, z
+    periodic, uniform 64^3: cos(θ J), θ = πk/(N-1), is solved exactly through the C-ABI,
+    u = f ρ_M / σ_M (tests/test_oracle_semi.py pins the same closed form for the oracle)."""
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    n = 4
+    N = 16 * n
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / N, base_blocks=(n, n, n), B=16, bc=((EVEN, EVEN), P, P),
+               order=order, smoother=1, omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    dom = C.domain(cfg)
+    lv = Lay.uniform_leaves(dom)
+    th = np.pi * k / (N - 1)
+    f = S.sample_on_leaves(dom, lv, lambda x, y, z: np.cos(th * x * N) + 0 * y + 0 * z)
+    s = Solver(cfg, lv)
+    s.set_rhs(torch.from_numpy(f).cuda())
+    s.vcycle(1)
+    sx = 2 * np.cos(th) - 2
+    rho = 1 + sx / 12 - (sx * sx / 240 if order == 6 else 0.0)
+    uexp = f * rho / (sx * N * N)
+    u = s.get_solution().cpu().numpy()
+    assert np.abs(u - uexp).max() <= 1e-11 * np.abs(uexp).max()
+    assert s.residual_norm()[1] < 1e-11

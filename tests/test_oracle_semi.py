@@ -114,3 +114,64 @@ def test_symmetric_both_faces_with_unbounded_axes():
     assert o.residual_norm()[1] < 1e-11
     u0 = o.levels[0].u
     assert np.abs(u0[0]).max() <= 1e-13 * np.abs(u0).max()
+
+
+# ------------------------------------------------------------- EVEN / EVEN (reading S3)
+def _ee_case(others, n=2, order=4):
+    cfg = dict(origin=(0.0, 0.0, 0.0), h0=1.0 / (16 * n), base_blocks=(n, n, n), B=16,
+               bc=((EVEN, EVEN), others[0], others[1]), order=order, smoother=1, omega=1.0, eta1=2, eta2=2,
+               coarse_n=0)
+    dom = C.domain(cfg)
+    return cfg, dom, Lay.uniform_leaves(dom)
+
+
+@pytest.mark.parametrize("order", [2, 4, 6])
+@pytest.mark.parametrize("k", [1, 4, 9])
+def test_even_even_eigenmode_exact(order, k):
+    """Homogeneous Neumann on both x faces, walls at nodes 0 and N-1 (reading S3):
+    cos(θ J), θ = πk/(N-1), is a lattice eigenfunction of every Mehrstellen operator with
+    the mirrored ghosts, eigenvalue σ_M(θ, θ_y, 0) from the stencil symbol (A1); f* =
+    R_h^M f scales it by ρ_M, so u = f ρ_M / σ_M exactly, walls included."""
+    cfg, dom, lv = _ee_case((P, P), order=order)
+    N = 32
+    h = 1.0 / N
+    th, ky = np.pi * k / (N - 1), 2 * np.pi * 3 / N
+    fn = lambda x, y, z: np.cos(th * x * N) * np.cos(ky * y * N) + 0 * z   # noqa: E731
+    f = S.sample_on_leaves(dom, lv, fn)
+    o = _solve(cfg, lv, f)
+    sx, sy = 2 * np.cos(th) - 2, 2 * np.cos(ky) - 2
+    # symbols typed from fig:stencils (M = 2, 4, 6) and the right-hand sides E10-E13
+    sig = {2: sx + sy, 4: sx + sy + sx * sy / 6, 6: sx + sy + sx * sy / 6}[order] / h ** 2
+    rho = {2: 1.0, 4: 1 + (sx + sy) / 12, 6: 1 + (sx + sy) / 12 + sx * sy / 90 - (sx * sx + sy * sy) / 240}[order]
+    uexp = f * rho / sig
+    assert np.abs(o.get_solution() - uexp).max() <= 1e-11 * np.abs(uexp).max()
+
+
+def test_even_even_singular_zero_mean_and_neumann_convergence():
+    """Pure Neumann box (EVEN/EVEN on all axes): the constant is in the null space, the
+    coarse solve returns the zero-(weighted-)mean solution; with the compatible
+    manufactured u = cos(πx/Lx) cos(πy/Ly) + cos(2πz/Lz), L = (N-1)h (walls at 0 and L),
+    the discrete solution converges to u at 4th order (M = 4) mod the constant."""
+    errs = []
+    for n in (2, 4):
+        cfg, dom, lv = _ee_case(((EVEN, EVEN), (EVEN, EVEN)), n=n)
+        N = 16 * n
+        L = (N - 1) / N
+        ue = lambda x, y, z: np.cos(np.pi * x / L) * np.cos(np.pi * y / L) + np.cos(2 * np.pi * z / L)  # noqa: E731
+        fe = lambda x, y, z: (-2 * (np.pi / L) ** 2 * np.cos(np.pi * x / L) * np.cos(np.pi * y / L)  # noqa: E731
+                              - (2 * np.pi / L) ** 2 * np.cos(2 * np.pi * z / L))
+        f = S.sample_on_leaves(dom, lv, fe)
+        o = _solve(cfg, lv, f)
+        assert o.residual_norm()[1] < 1e-10        # the discrete equation, walls included
+        u = o.get_solution()
+        ua = S.sample_on_leaves(dom, lv, ue)
+        d = u - ua
+        errs.append(np.abs(d - d.mean()).max())
+    rate = np.log2(errs[0] / errs[1])
+    assert 3.6 < rate < 4.6, (errs, rate)
+
+
+def test_even_even_rejects_unbounded_axes():
+    cfg, dom, lv = _ee_case((U, P))
+    with pytest.raises(ValueError):
+        MO.Oracle(cfg, lv)
