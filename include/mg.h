@@ -105,6 +105,11 @@ typedef struct mg_desc {
                                 0 auto (levels with fewer blocks than SMs), 1 never, 2 always */
   int32_t fuse;              /* 0 auto: fused pencil kernels where eligible (last pre-sweep +
                                 residual + restriction; residual + restriction); 1 never fuse */
+  int32_t ncomp;             /* right-hand sides solved together (0 or 1 = scalar; up to 8, e.g. 3 for
+                                the Biot-Savart velocity): every call then takes and
+                                returns leaf arrays [ncomp][n_leaf][B][B][B], one V-cycle and every
+                                kernel launch cover all components (gridDim.y = ncomp), the norms
+                                are the max over components, the coarse solve is one batched FFT */
   int32_t staging;           /* plane tiles of the RB sweep: 0 cp.async ring (default, the
                                 fastest measured), 1 TMA tensor copies (cp.async.bulk.tensor, 9
                                 boxes per field and plane) into an mbarrier ring; measured 2.5x
@@ -155,7 +160,8 @@ int mg_num_levels(mg_handle* h);
 
 enum { MG_FIELD_U = 0, MG_FIELD_F = 1, MG_FIELD_R = 2, MG_FIELD_UHAT = 3 };
 /* dir 0: export the level's real blocks [n_real][B^3] into dev; 1: import from dev;
- * 2 / 3: export / import real then ghost blocks [n_real + n_ghost][B^3] (ghost checks) */
+ * 2 / 3: export / import real then ghost blocks [n_real + n_ghost][B^3] (ghost checks).
+ * field | (c << 8) selects component c (ncomp > 1). */
 int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev);
 enum {
   MG_OP_REFRESH = 0,        /* ghost fill of `level` (f2c injection + c2f / band) */
@@ -218,6 +224,17 @@ int mg_adapt(const int32_t base_blocks[3], const int32_t bc[6], int32_t allow_un
              const int32_t* leaves, int32_t n_leaf, const double* gamma, double eps_r, double eps_c,
              int32_t max_level, int32_t* out_leaves, int32_t out_capacity, int32_t* n_out,
              int32_t* n_suppressed);
+
+/* mg_transfer: u of `dst` (an adapted grid of the same domain: same origin, h0,
+ * base_blocks, B, bc, coarse_n, ncomp) from the composite solution of `src` (
+ * reading A3): a dst leaf that is a block of src at the same level copies it (a leaf kept,
+ * or coarsened into a parent, which holds the injected fine values, E7); a dst leaf one
+ * level finer than src (refined) takes the trilinear interpolation of its src
+ * parent, ghost nodes included; then inject-up.  Call after mg_set_rhs(dst) (which
+ * resets u).  Device-to-device on dst's stream; synchronises both streams.  Returns
+ * MG_OK, MG_ERR_ARG (different domains), MG_ERR_STATE, MG_ERR_LAYOUT_NESTING (a leaf
+ * more than one level finer than src). */
+int mg_transfer(mg_handle* dst, mg_handle* src);
 
 #ifdef __cplusplus
 }

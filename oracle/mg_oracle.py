@@ -746,6 +746,39 @@ class Oracle:
             out[n] = self.levels[self.nsub + lev].u[i:i + B, j:j + B, k:k + B].transpose(2, 1, 0)
         return out
 
+    def transfer_from(self, old):
+        """u on this (adapted) grid from the composite solution of `old`, the same domain
+        on another leaf set ("refined into 8 finer blocks" / "revert
+        back to a single grid block"; reading A3): a level-k block of this grid that is
+        also a level-k block of `old` takes its values (a coarsened leaf: the old parent,
+        which holds the injected fine values, E7); a block new at level k (a refined leaf)
+        takes the trilinear interpolation (the prolongation rule applied to u) of
+        the old level k-1, ghosts included (lookup O2 after inject-up).  Then inject-up."""
+        old.inject_up()
+        B = self.B
+        for lev, bi, bj, bk in self.leaves.tolist():
+            m = self.nsub + lev
+            L, Lo = self.levels[m], old.levels[m] if m < len(old.levels) else None
+            i, j, k = self._local(lev, bi, bj, bk)
+            J0 = np.array([bi, bj, bk]) * B
+            if Lo is not None:
+                io = J0 - Lo.lo
+                if (io >= 0).all() and (io + B <= Lo.n).all() and Lo.mask[io[0], io[1], io[2]]:
+                    L.u[i:i + B, j:j + B, k:k + B] = Lo.u[io[0]:io[0] + B, io[1]:io[1] + B, io[2]:io[2] + B]
+                    continue
+            C = old.levels[m - 1]
+            X = old.lookup(m - 1, old.uvals())            # extended: stored + ghosts
+            c0 = J0 // 2 - C.lo + E                          # extended index of coarse node J0/2
+            sub = X[c0[0]:c0[0] + B // 2 + 1, c0[1]:c0[1] + B // 2 + 1, c0[2]:c0[2] + B // 2 + 1]
+            for ax in range(3):                              # per axis: even -> copy, odd -> mean
+                sm = np.moveaxis(sub, ax, 0)
+                out = np.empty((B,) + sm.shape[1:])
+                out[0::2] = sm[:B // 2]
+                out[1::2] = 0.5 * (sm[:B // 2] + sm[1:B // 2 + 1])
+                sub = np.moveaxis(out, 0, ax)
+            L.u[i:i + B, j:j + B, k:k + B] = sub
+        self.inject_up()
+
     def vcycle(self, n=1):
         """Alg. 1 with readings Z9-Z15, then inject-up."""
         top = len(self.levels) - 1

@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
                                                    double* __restrict__ ff, const double* __restrict__ cf,
                                                    bool ext_zero, int t1_off) {
   extern __shared__ double sm[];
+  ff += (int64_t)blockIdx.y * F.cs;  // component blockIdx.y
+  cf += (int64_t)blockIdx.y * C.cs;
   const int32_t* bx = boxes + GBOX_REC * blockIdx.x;
   const int blk = bx[0];
   const int lo[3] = {bx[1], bx[2], bx[3]}, hi[3] = {bx[4], bx[5], bx[6]};
@@ -203,11 +205,11 @@ void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_
   if (nbox <= 0) return;
   const size_t smem = sizeof(double) * (size_t)(szA + szB);
   if (I == 4)
-    k_c2f_box<4><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<4><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else if (I == 6)
-    k_c2f_box<6><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<6><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else
-    k_c2f_box<8><<<nbox, GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<8><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   note_launch();
 }
 

@@ -170,6 +170,8 @@ struct mg_handle {
   std::vector<double> prof_ms;      // [stage][level]
   std::vector<int64_t> prof_n;
   int nsm = 148;  // SMs of the device (grid sizing of the pencil kernels)
+  int nc = 1;     // components solved together (mg_desc.ncomp): fields [nc][ntot][B^3]
+  int64_t* d_lvl_cs = nullptr;  // per level: component stride (doubles) of its fields
   // graph
   bool use_graph = false;
   cudaGraphExec_t gexec = nullptr;
@@ -262,6 +264,8 @@ LevelView view(mg_handle* h, int m) {
   v.sw_pen_blk = l.d_sw_blk;
   v.sw_pen_len = l.d_sw_len;
   v.sw_pen_z = l.d_sw_z;
+  v.nc = h->nc;
+  v.cs = (int64_t)l.ntot() * l.B3;
   return v;
 }
 
@@ -297,6 +301,7 @@ void validate_and_build(mg_handle* h) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
     if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
+    if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
     if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1 || d.staging < 0 || d.staging > 1))
       throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse and staging 0..1");
     // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
@@ -318,6 +323,7 @@ void validate_and_build(mg_handle* h) {
     for (int b = 0; b < 3; ++b)
       if (h->hi_even[a] && (d.bc[2 * b] == MG_BC_UNBOUNDED || d.bc[2 * b + 1] == MG_BC_UNBOUNDED))
         throw MgError(MG_ERR_BC, "an EVEN/EVEN axis needs the other axes periodic or symmetric");
+  h->nc = d.ncomp > 0 ? d.ncomp : 1;
   h->order = d.order;
   h->I = d.order + 2;
   h->GE = (d.order == 6 && d.allow_unbounded_refined) ? GE_M6U1 : GE_M4;
@@ -866,7 +872,7 @@ void build_pencils(mg_handle* h) {
 
 void alloc_device(mg_handle* h) {
   for (auto& l : h->L) {
-    const size_t n = (size_t)l.ntot() * l.B3;
+    const size_t n = (size_t)h->nc * l.ntot() * l.B3;
     for (double** p : {&l.u[0], &l.u[1], &l.f, &l.r, &l.uhat}) {
       CUDA_OK(cudaMalloc(p, n * sizeof(double)));
       CUDA_OK(cudaMemsetAsync(*p, 0, n * sizeof(double), h->s));
@@ -899,7 +905,7 @@ void alloc_device(mg_handle* h) {
     if (l.B != 16 || h->d.staging != 1) continue;
     bool ok = true;
     for (int c = 0; c < 2 && ok; ++c)
-      ok = encode_tile_maps(l.u[c], l.ntot(), l.tmaps[c].u) && encode_tile_maps(l.f, l.ntot(), l.tmaps[c].f);
+      ok = encode_tile_maps(l.u[c], h->nc * l.ntot(), l.tmaps[c].u) && encode_tile_maps(l.f, h->nc * l.ntot(), l.tmaps[c].f);
     l.has_tmaps = ok;
   }
   // leaf map: leaf n -> (level, block)
@@ -914,9 +920,12 @@ void alloc_device(mg_handle* h) {
   h->h_lvl_ptrs.assign(h->L.size(), nullptr);
   CUDA_OK(cudaMalloc(&h->d_lvl_ptrs, h->L.size() * sizeof(double*)));
   CUDA_OK(cudaMalloc(&h->d_norm, 2 * sizeof(unsigned long long)));
-  const size_t nl = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
+  const size_t nl = (size_t)h->nc * h->leaves.size() * h->d.block_size * h->d.block_size * h->d.block_size;
   CUDA_OK(cudaMalloc(&h->d_leafbuf, nl * sizeof(double)));
   CUDA_OK(cudaMalloc(&h->d_leafbuf2, nl * sizeof(double)));
+  std::vector<int64_t> lcs;
+  for (auto& l : h->L) lcs.push_back((int64_t)l.ntot() * l.B3);
+  h->d_lvl_cs = dev_upload(lcs);
 }
 
 int smooth7(int n) {
@@ -948,10 +957,14 @@ void setup_coarse(mg_handle* h) {
   h->coarse_kind = nunb == 0 ? 0 : (nunb == 3 ? 1 : 2);
   const int Px = h->P[0], Py = h->P[1], Pz = h->P[2];
   const int64_t nd = (int64_t)Px * Py * Pz, nc = (int64_t)(Px / 2 + 1) * Py * Pz;
-  CUDA_OK(cudaMalloc(&h->d_dense, nd * sizeof(double)));
-  CUDA_OK(cudaMalloc(&h->d_spec, nc * sizeof(cufftDoubleComplex)));
-  CUFFT_OK(cufftPlan3d(&h->plan_f, Pz, Py, Px, CUFFT_D2Z));
-  CUFFT_OK(cufftPlan3d(&h->plan_b, Pz, Py, Px, CUFFT_Z2D));
+  // one batched transform over the components (dense [ncomp][Pz][Py][Px])
+  CUDA_OK(cudaMalloc(&h->d_dense, (size_t)h->nc * nd * sizeof(double)));
+  CUDA_OK(cudaMalloc(&h->d_spec, (size_t)h->nc * nc * sizeof(cufftDoubleComplex)));
+  {
+    int dims[3] = {Pz, Py, Px};
+    CUFFT_OK(cufftPlanMany(&h->plan_f, 3, dims, nullptr, 1, (int)nd, nullptr, 1, (int)nc, CUFFT_D2Z, h->nc));
+    CUFFT_OK(cufftPlanMany(&h->plan_b, 3, dims, nullptr, 1, (int)nc, nullptr, 1, (int)nd, CUFFT_Z2D, h->nc));
+  }
   CUFFT_OK(cufftSetStream(h->plan_f, h->s));
   CUFFT_OK(cufftSetStream(h->plan_b, h->s));
   const double sc = c.h * c.h / (double)nd;
@@ -967,7 +980,14 @@ void setup_coarse(mg_handle* h) {
           T[((size_t)z * Py + y) * Px + x] = G[((size_t)(nz + R) * n + (ny + R)) * n + (nx + R)];
         }
     CUDA_OK(cudaMemcpy(h->d_dense, T.data(), nd * sizeof(double), cudaMemcpyHostToDevice));
-    CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
+    {  // one (unbatched) transform of the LGF table
+      cufftHandle p1;
+      CUFFT_OK(cufftPlan3d(&p1, Pz, Py, Px, CUFFT_D2Z));
+      CUFFT_OK(cufftSetStream(p1, h->s));
+      CUFFT_OK(cufftExecD2Z(p1, h->d_dense, (cufftDoubleComplex*)h->d_spec));
+      CUDA_OK(cudaStreamSynchronize(h->s));
+      cufftDestroy(p1);
+    }
     CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
     launch_real_part_scale(h->d_spec, h->d_mult, nc, sc, h->s);
   } else if (h->coarse_kind == 2) {
@@ -1081,13 +1101,19 @@ void refresh(mg_handle* h, int m) {
   Prof pr(h, ST_GHOST, m);
   if (lo < m && m < MAX_CHAIN_LEVELS && !h->L[m].chain_dst.empty()) {
     double* fields[MAX_CHAIN_LEVELS] = {};
-    for (int j = 0; j <= m && j < MAX_CHAIN_LEVELS; ++j) fields[j] = h->L[j].u[h->L[j].cur];
+    int64_t cs[MAX_CHAIN_LEVELS] = {};
+    for (int j = 0; j <= m && j < MAX_CHAIN_LEVELS; ++j) {
+      fields[j] = h->L[j].u[h->L[j].cur];
+      cs[j] = (int64_t)h->L[j].ntot() * h->L[j].B3;
+    }
     const Level& T = h->L[m];
-    launch_inject_chain((int)T.chain_dst.size(), T.d_chain_lev, T.d_chain_dst, T.d_chain_src, fields, h->s);
+    launch_inject_chain((int)T.chain_dst.size(), T.d_chain_lev, T.d_chain_dst, T.d_chain_src, fields, cs, h->nc, h->s);
   } else {
     for (int j = m; j >= lo; --j) {
       Level &F = h->L[j], &C = h->L[j - 1];
-      if (!F.inj_dst.empty()) launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->s);
+      if (!F.inj_dst.empty())
+        launch_inject_list(inj_list(F), C.u[C.cur], F.u[F.cur], h->nc, (int64_t)C.ntot() * C.B3, (int64_t)F.ntot() * F.B3,
+                           h->s);
     }
   }
   for (int j = lo; j <= m; ++j) {
@@ -1164,12 +1190,15 @@ void restrict_level(mg_handle* h, int m) {
   if (launch_fas_pencil(view(h, m - 1), h->order, h->s)) {
     // the pencil FAS kernel wrote û on the real blocks; the prolongation also takes ε on
     // the exterior band (reading Z13-W, U1 / level 0), stored in the ghost blocks
-    if (C.has_ext_ghosts)
-      CUDA_OK(cudaMemcpyAsync(C.uhat + (size_t)C.nreal * C.B3, C.u[C.cur] + (size_t)C.nreal * C.B3,
-                              (size_t)C.nghost * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+    if (C.has_ext_ghosts) {  // the ghost part of every component
+      const size_t pitch = (size_t)C.ntot() * C.B3 * sizeof(double);
+      CUDA_OK(cudaMemcpy2DAsync(C.uhat + (size_t)C.nreal * C.B3, pitch, C.u[C.cur] + (size_t)C.nreal * C.B3, pitch,
+                                (size_t)C.nghost * C.B3 * sizeof(double), h->nc, cudaMemcpyDeviceToDevice, h->s));
+    }
   } else {
     launch_fas_rhs(view(h, m), view(h, m - 1), h->order, h->s);
-    CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)C.ntot() * C.B3 * sizeof(double), cudaMemcpyDeviceToDevice, h->s));
+    CUDA_OK(cudaMemcpyAsync(C.uhat, C.u[C.cur], (size_t)h->nc * C.ntot() * C.B3 * sizeof(double),
+                            cudaMemcpyDeviceToDevice, h->s));
   }
 }
 
@@ -1186,8 +1215,8 @@ void coarse_solve(mg_handle* h) {
   LevelView c = view(h, 0);
   launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->hi_odd, h->hi_even, h->coff, h->s);
   CUFFT_OK(cufftExecD2Z(h->plan_f, h->d_dense, (cufftDoubleComplex*)h->d_spec));
-  if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->s);
-  else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->s);
+  if (h->coarse_kind == 0) launch_coarse_mul_periodic(h->d_spec, h->P, h->order, h->L[0].h, h->nc, h->s);
+  else launch_coarse_mul_table(h->d_spec, h->d_mult, (int64_t)(h->P[0] / 2 + 1) * h->P[1] * h->P[2], h->nc, h->s);
   CUFFT_OK(cufftExecZ2D(h->plan_b, (cufftDoubleComplex*)h->d_spec, h->d_dense));
   launch_coarse_scatter(c, h->d_dense, h->P, h->coff, c2f_list(h->L[0]), h->s);
 }
@@ -1219,7 +1248,7 @@ void vcycle_body(mg_handle* h) {
     // keep the buffer parity fixed per cycle (so one captured graph can be replayed)
     for (int m = 1; m <= top; ++m) {
       Level& l = h->L[m];
-      CUDA_OK(cudaMemcpyAsync(l.u[1 - l.cur], l.u[l.cur], (size_t)l.ntot() * l.B3 * sizeof(double),
+      CUDA_OK(cudaMemcpyAsync(l.u[1 - l.cur], l.u[l.cur], (size_t)h->nc * l.ntot() * l.B3 * sizeof(double),
                               cudaMemcpyDeviceToDevice, h->s));
       swap_u(l);
     }
@@ -1325,7 +1354,7 @@ double cauchy_increment(mg_handle* h) {
   set_level_ptrs(h, MG_FIELD_U);
   CUDA_OK(cudaMemsetAsync(h->d_norm, 0, 2 * sizeof(unsigned long long), h->s));
   launch_leaf_cauchy((int)h->leaves.size(), h->d.block_size * h->d.block_size * h->d.block_size, h->d_leafmap,
-                     h->d_leafbuf2, h->d_lvl_ptrs, h->d_norm, h->s);
+                     h->d_leafbuf2, h->d_lvl_ptrs, h->d_lvl_cs, h->nc, h->d_norm, h->s);
   unsigned long long bits[2];
   CUDA_OK(cudaMemcpyAsync(bits, h->d_norm, sizeof(bits), cudaMemcpyDeviceToHost, h->s));
   CUDA_OK(cudaStreamSynchronize(h->s));
@@ -1339,7 +1368,7 @@ double cauchy_increment(mg_handle* h) {
 void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
   set_level_ptrs(h, field);
   launch_leaf_scatter((int)h->leaves.size(), h->d.block_size * h->d.block_size * h->d.block_size, h->d_leafmap,
-                      leafbuf, h->d_lvl_ptrs, (int)h->L.size(), to_levels, h->s);
+                      leafbuf, h->d_lvl_ptrs, h->d_lvl_cs, h->nc, to_levels, h->s);
   // the pointer table is reused by the next call: order it on the stream
   CUDA_OK(cudaStreamSynchronize(h->s));
 }
@@ -1347,7 +1376,7 @@ void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
 void set_rhs(mg_handle* h, const double* f_dev) {
   const int nlev = (int)h->L.size();
   for (auto& l : h->L) {
-    const size_t n = (size_t)l.ntot() * l.B3;
+    const size_t n = (size_t)h->nc * l.ntot() * l.B3;
     CUDA_OK(cudaMemsetAsync(l.f, 0, n * sizeof(double), h->s));
     CUDA_OK(cudaMemsetAsync(l.u[0], 0, n * sizeof(double), h->s));
     CUDA_OK(cudaMemsetAsync(l.u[1], 0, n * sizeof(double), h->s));
@@ -1370,15 +1399,17 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
                    h->s);
   }
-  if (!h->fwall.empty()) launch_fill_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, 0.0, h->s);
+  const int64_t cs0 = (int64_t)h->L[0].ntot() * h->L[0].B3;
+  if (!h->fwall.empty()) launch_fill_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, 0.0, h->nc, cs0, h->s);
   if (!h->fm_dst.empty())
-    launch_copy_signed((int)h->fm_dst.size(), h->d_fm_dst, h->d_fm_src, h->d_fm_sgn, h->L[0].f, h->L[0].f, h->s);
+    launch_copy_signed((int)h->fm_dst.size(), h->d_fm_dst, h->d_fm_src, h->d_fm_sgn, h->L[0].f, h->L[0].f, h->nc, cs0,
+                       h->s);
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
     launch_correct_rhs(view(h, m), h->order, l.r, h->s);
   }
   for (auto& l : h->L)
-    CUDA_OK(cudaMemsetAsync(l.r, 0, (size_t)l.ntot() * l.B3 * sizeof(double), h->s));
+    CUDA_OK(cudaMemsetAsync(l.r, 0, (size_t)h->nc * l.ntot() * l.B3 * sizeof(double), h->s));
   CUDA_OK(cudaMemsetAsync(h->d_norm, 0, sizeof(unsigned long long), h->s));
   for (int m = 0; m < nlev; ++m) launch_norm(view(h, m), h->order, false, h->d_norm, h->s);
   h->fstar_norm = read_norm(h);
@@ -1400,7 +1431,7 @@ void destroy(mg_handle* h) {
   }
   for (void* p : {(void*)h->d_fm_dst, (void*)h->d_fm_src, (void*)h->d_fm_sgn, (void*)h->d_fwall})
     if (p) cudaFree(p);
-  for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_norm, (void*)h->d_leafbuf,
+  for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_lvl_cs, (void*)h->d_norm, (void*)h->d_leafbuf,
                   (void*)h->d_leafbuf2, (void*)h->d_dense, h->d_spec, (void*)h->d_mult})
     if (p) cudaFree(p);
   if (h->plan_f) cufftDestroy(h->plan_f);
@@ -1547,7 +1578,7 @@ int mg_solve(mg_handle* h, double tol, int max_cycles, int criterion, int* cycle
 int mg_run_host(mg_handle* h, const double* f_host, double* u_host, int ncycles, double* rel_out) {
   if (!h || !f_host || !u_host || ncycles < 0) return MG_ERR_ARG;
   return guard(h, [&] {
-    const size_t n = h->leaves.size() * (size_t)h->d.block_size * h->d.block_size * h->d.block_size;
+    const size_t n = (size_t)h->nc * h->leaves.size() * h->d.block_size * h->d.block_size * h->d.block_size;
     CUDA_OK(cudaMemcpyAsync(h->d_leafbuf, f_host, n * sizeof(double), cudaMemcpyHostToDevice, h->s));
     set_rhs(h, h->d_leafbuf);
     run_vcycles(h, ncycles);
@@ -1616,9 +1647,13 @@ int mg_level_blocks(mg_handle* h, int level, int32_t* coords) {
 
 int mg_debug_field(mg_handle* h, int field, int level, int dir, double* dev) {
   if (!h || !dev || level < 0 || level >= (int)h->L.size()) return MG_ERR_ARG;
+  const int comp = (field >> 8) & 0xff;
+  field &= 0xff;
+  if (comp >= h->nc) return MG_ERR_ARG;
   return guard(h, [&] {
     Level& l = h->L[level];
     double* p = field == MG_FIELD_U ? l.u[l.cur] : field == MG_FIELD_F ? l.f : field == MG_FIELD_R ? l.r : l.uhat;
+    p += (size_t)comp * l.ntot() * l.B3;
     const size_t n = (size_t)(dir >= 2 ? l.ntot() : l.nreal) * l.B3 * sizeof(double);
     if (dir == 0 || dir == 2) CUDA_OK(cudaMemcpyAsync(dev, p, n, cudaMemcpyDeviceToDevice, h->s));
     else CUDA_OK(cudaMemcpyAsync(p, dev, n, cudaMemcpyDeviceToDevice, h->s));
@@ -1652,6 +1687,67 @@ static void apply_op(mg_handle* h, int op, int level) {
   }
 }
 
+int mg_transfer(mg_handle* dst, mg_handle* src) {
+  if (!dst || !src || dst == src) return MG_ERR_ARG;
+  if (!dst->rhs_set) {
+    dst->err = "mg_transfer before mg_set_rhs on the destination";
+    return MG_ERR_STATE;
+  }
+  return guard(dst, [&] {
+    const mg_desc &a = dst->d, &b = src->d;
+    bool same = a.block_size == b.block_size && a.coarse_n == b.coarse_n && dst->nc == src->nc && a.h0 == b.h0;
+    for (int i = 0; i < 3; ++i) same = same && a.base_blocks[i] == b.base_blocks[i] && a.origin[i] == b.origin[i];
+    for (int i = 0; i < 6; ++i) same = same && a.bc[i] == b.bc[i];
+    if (!same) throw MgError(MG_ERR_ARG, "mg_transfer: the grids must share domain, base blocks, B, BC, coarse_n, ncomp");
+    // the source's composite solution: canonical coarse values and refreshed ghosts
+    CUDA_OK(cudaStreamSynchronize(dst->s));
+    if (!src->canonical) {
+      inject_up_all(src);
+      src->canonical = true;
+    }
+    for (int m = 1; m < (int)src->L.size(); ++m) refresh(src, m);
+    CUDA_OK(cudaStreamSynchronize(src->s));
+    const int B = a.block_size;
+    std::vector<std::vector<int32_t>> rec(dst->L.size());
+    for (const auto& lf : dst->leaves) {
+      const int m = dst->nsub + lf[0];
+      const int di = dst->L[m].find(lf[1], lf[2], lf[3]);
+      const int si = m < (int)src->L.size() ? src->L[m].find(lf[1], lf[2], lf[3]) : -1;
+      if (si >= 0 && si < src->L[m].nreal) {
+        rec[m].insert(rec[m].end(), {di, si, -1, 0, 0});
+        continue;
+      }
+      const int pi = m >= 1 && m - 1 < (int)src->L.size() ? src->L[m - 1].find(lf[1] >> 1, lf[2] >> 1, lf[3] >> 1) : -1;
+      if (pi < 0 || pi >= src->L[m - 1].nreal)
+        throw MgError(MG_ERR_LAYOUT_NESTING, "mg_transfer: a leaf more than one level finer than the source grid");
+      rec[m].insert(rec[m].end(), {di, pi, (lf[1] & 1) * B / 2, (lf[2] & 1) * B / 2, (lf[3] & 1) * B / 2});
+    }
+    for (size_t m = 0; m < dst->L.size(); ++m) {
+      if (rec[m].empty()) continue;
+      Level& D = dst->L[m];
+      // copies read the source level m, interpolations level m - 1: one launch each
+      std::vector<int32_t> cp, ip;
+      for (size_t e = 0; e < rec[m].size(); e += 5) {
+        auto& v = rec[m][e + 2] < 0 ? cp : ip;
+        v.insert(v.end(), rec[m].begin() + e, rec[m].begin() + e + 5);
+      }
+      for (int kind = 0; kind < 2; ++kind) {
+        const auto& v = kind == 0 ? cp : ip;
+        if (v.empty()) continue;
+        const Level& S = src->L[kind == 0 ? m : m - 1];
+        int32_t* dv = dev_upload(v);
+        launch_transfer((int)v.size() / 5, dv, D.u[D.cur], (int64_t)D.ntot() * D.B3, S.u[S.cur], (int64_t)S.ntot() * S.B3,
+                        S.d_nbr, B, dst->nc, dst->s);
+        CUDA_OK(cudaStreamSynchronize(dst->s));
+        cudaFree(dv);
+      }
+    }
+    inject_up_all(dst);
+    dst->canonical = true;
+    CUDA_OK(cudaStreamSynchronize(dst->s));
+  });
+}
+
 int mg_debug_poison(mg_handle* h) {
   if (!h) return MG_ERR_ARG;
   return guard(h, [&] {
@@ -1665,7 +1761,8 @@ int mg_debug_poison(mg_handle* h) {
           if (!((l.need[gi][loc >> 6] >> (loc & 63)) & 1)) idx.push_back((l.nreal + gi) * l.B3 + loc);
       if (idx.empty()) continue;
       int32_t* d = dev_upload(idx);
-      for (double* p : {l.u[0], l.u[1], l.f, l.r, l.uhat}) launch_fill_list((int)idx.size(), d, p, nan, h->s);
+      for (double* p : {l.u[0], l.u[1], l.f, l.r, l.uhat})
+        launch_fill_list((int)idx.size(), d, p, nan, h->nc, (int64_t)l.ntot() * l.B3, h->s);
       CUDA_OK(cudaStreamSynchronize(h->s));
       cudaFree(d);
     }

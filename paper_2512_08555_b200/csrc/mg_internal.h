@@ -15,6 +15,10 @@ enum SmoothMode { SM_JACOBI = 0, SM_RB = 1 };
 // values (resolution-jump c2f, exterior band).  See DESIGN.md §Layout.
 struct LevelView {
   int B, B3, nreal, ntot;
+  // components (right-hand sides solved together, mg_desc.ncomp): every field array holds
+  // nc copies [nc][ntot][B^3]; component c of a batched launch is blockIdx.y (comp_view)
+  int nc;
+  int64_t cs;           // component stride (doubles) = ntot * B3
   int N[3];             // nodes per axis of the level lattice
   double h;
   double* u;            // current solution buffer (ping-pong, see mg_host.cpp)
@@ -53,6 +57,18 @@ struct TileMaps {
 };
 // encode the 4 maps of an array of `ntot` 16^3 blocks; false if the driver lacks TMA
 bool encode_tile_maps(const double* base, int ntot, CUtensorMap out[4]);
+
+#ifdef __CUDACC__
+// the field pointers of component blockIdx.y (batched launches: gridDim.y = nc)
+__device__ __forceinline__ void comp_view(LevelView& L) {
+  const int64_t o = (int64_t)blockIdx.y * L.cs;
+  L.u += o;
+  L.u_out += o;
+  L.f += o;
+  L.r += o;
+  L.uhat += o;
+}
+#endif
 
 struct C2FList {           // boundary-ghost entries of one level
   int n;
@@ -93,33 +109,41 @@ size_t c2f_box_smem_max(int I);
 void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, int szA,
                     int szB, double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void prepare_ghost_kernels();
-void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s);
+void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, int nc, int64_t cs_coarse,
+                        int64_t cs_fine, cudaStream_t s);
 // composed exterior-chain injections: fields[lev] = current u of level lev; entry e copies
 // fields[lev_e >> 4][src_e] to fields[lev_e & 15][dst_e]
 constexpr int MAX_CHAIN_LEVELS = 16;
 void launch_inject_chain(int n, const int32_t* lev, const int32_t* dst, const int32_t* src,
-                         double* const fields[MAX_CHAIN_LEVELS], cudaStream_t s);
+                         double* const fields[MAX_CHAIN_LEVELS], const int64_t cs[MAX_CHAIN_LEVELS], int nc,
+                         cudaStream_t s);
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s);
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s);
 void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s);
 void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s);
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s);
+// leaf arrays [nc][nleaf][B3]; lev_cs[level] = component stride of that level's fields
 void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
-                         int nlev, bool to_levels, cudaStream_t s);
+                         const int64_t* lev_cs, int nc, bool to_levels, cudaStream_t s);
 // E20 Cauchy increment on leaf nodes: out[0] max|u - prev|, out[1] max|u|; prev <- u
 void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, double* const* lev_u,
-                        unsigned long long* out, cudaStream_t s);
+                        const int64_t* lev_cs, int nc, unsigned long long* out, cudaStream_t s);
+// field transfer (mg_transfer): n records (dst block, src block, ox, oy, oz), ox < 0 = copy
+void launch_transfer(int n, const int32_t* rec, double* dst, int64_t dcs, const double* src, int64_t scs,
+                     const int32_t* snbr, int B, int nc, cudaStream_t s);
 // coarse solve helpers
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
                           const int* hi_even, const int* off, cudaStream_t s);
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s);
-void launch_fill_list(int n, const int32_t* idx, double* d, double v, cudaStream_t s);  // d[idx[i]] = v
+// d[c cs + idx[i]] = v for every component c < nc
+void launch_fill_list(int n, const int32_t* idx, double* d, double v, int nc, int64_t cs, cudaStream_t s);
 void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
-                        cudaStream_t s);
-void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s);
-void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s);
+                        int nc, int64_t cs, cudaStream_t s);
+// spectra of the nc components stored one after the other, (P0/2+1) P1 P2 each
+void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, int nc, cudaStream_t s);
+void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, cudaStream_t s);
 // full multiplier table of a mixed periodic / unbounded coarse solve (R2C layout)
 void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
                        double h2, double scale, cudaStream_t s);

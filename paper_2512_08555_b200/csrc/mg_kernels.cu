@@ -81,6 +81,7 @@ __device__ __forceinline__ double lap_fetch(const double* __restrict__ u, const 
 // ---------------------------------------------------------------------------------
 template <int B, int ORDER, int MODE, bool RES, int NT>
 __global__ void __launch_bounds__(NT) k_smooth(LevelView L, double omega, double inv_h2, double inv_d) {
+  comp_view(L);
   constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
   constexpr int H = NS + (RES ? 1 : 0);
   constexpr int T = B + 2 * H;
@@ -292,6 +293,7 @@ static const uint32_t* smooth_table() {
 template <int B, int ORDER, int MODE, bool RES, int NT>
 __global__ void __launch_bounds__(NT, (MODE == SM_RB && RES) ? 2 : (MODE < 0 ? 4 : 3))
     k_smooth2(LevelView L, const uint32_t* __restrict__ tab, double omega, double inv_h2, double inv_d) {
+  comp_view(L);
   using SH = SmoothShape<B, MODE, RES>;
   constexpr int NS = SH::NS, T = SH::T, B3 = SH::B3;
   constexpr int MAXU = (SH::CNT(0) + NT - 1) / NT;  // pass 0 is the largest
@@ -408,7 +410,7 @@ static void smooth_inst(const LevelView& L, double omega, double inv_h2, double 
       return;
     }
     const uint32_t* tab = smooth_table<B, MODE, RES>();
-    if (L.nreal > 0) { k<<<L.nreal, NT, smem, s>>>(L, tab, omega, inv_h2, inv_d); ++g_nlaunch; }
+    if (L.nreal > 0) { k<<<dim3(L.nreal, L.nc), NT, smem, s>>>(L, tab, omega, inv_h2, inv_d); ++g_nlaunch; }
     return;
   }
   smooth_inst_v1<B, ORDER, MODE, RES>(L, omega, inv_h2, inv_d, s, prepare_only);
@@ -427,7 +429,7 @@ static void smooth_inst_v1(const LevelView& L, double omega, double inv_h2, doub
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return;
   }
-  if (L.nreal > 0) { k<<<L.nreal, NT, smem, s>>>(L, omega, inv_h2, inv_d); ++g_nlaunch; }
+  if (L.nreal > 0) { k<<<dim3(L.nreal, L.nc), NT, smem, s>>>(L, omega, inv_h2, inv_d); ++g_nlaunch; }
 }
 
 template <int B, int ORDER>
@@ -488,13 +490,16 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s) {
 }
 
 __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
-                            double* __restrict__ d, const double* __restrict__ sv) {
+                            double* __restrict__ d, const double* __restrict__ sv, int64_t csd, int64_t css) {
+  d += (int64_t)blockIdx.y * csd;
+  sv += (int64_t)blockIdx.y * css;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) d[dst[i]] = sv[src[i]];
 }
 
 struct ChainFields {
   double* f[MAX_CHAIN_LEVELS];
+  int64_t cs[MAX_CHAIN_LEVELS];
 };
 
 __global__ void k_copy_chain(int n, const int32_t* __restrict__ lev, const int32_t* __restrict__ dst,
@@ -502,22 +507,29 @@ __global__ void k_copy_chain(int n, const int32_t* __restrict__ lev, const int32
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const int l = lev[i];
-    F.f[l & 15][dst[i]] = F.f[l >> 4][src[i]];
+    const int c = blockIdx.y;
+    F.f[l & 15][c * F.cs[l & 15] + dst[i]] = F.f[l >> 4][c * F.cs[l >> 4] + src[i]];
   }
 }
 
 void launch_inject_chain(int n, const int32_t* lev, const int32_t* dst, const int32_t* src,
-                         double* const fields[MAX_CHAIN_LEVELS], cudaStream_t s) {
+                         double* const fields[MAX_CHAIN_LEVELS], const int64_t cs[MAX_CHAIN_LEVELS], int nc,
+                         cudaStream_t s) {
   if (n <= 0) return;
   ChainFields F;
-  for (int j = 0; j < MAX_CHAIN_LEVELS; ++j) F.f[j] = fields[j];
-  k_copy_chain<<<(n + 255) / 256, 256, 0, s>>>(n, lev, dst, src, F);
+  for (int j = 0; j < MAX_CHAIN_LEVELS; ++j) {
+    F.f[j] = fields[j];
+    F.cs[j] = cs[j];
+  }
+  k_copy_chain<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, lev, dst, src, F);
   ++g_nlaunch;
 }
 
-void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, cudaStream_t s) {
+void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, int nc, int64_t cs_coarse,
+                        int64_t cs_fine, cudaStream_t s) {
   if (l.n == 0) return;
-  { k_copy_list<<<(l.n + 255) / 256, 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field); ++g_nlaunch; }
+  k_copy_list<<<dim3((l.n + 255) / 256, nc), 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field, cs_coarse, cs_fine);
+  ++g_nlaunch;
 }
 
 // ---------------------------------------------------------------------------------
@@ -526,6 +538,8 @@ void launch_inject_list(const InjList& l, double* coarse_field, const double* fi
 // is never written and stays 0 (reading Z14).
 // ---------------------------------------------------------------------------------
 __global__ void k_restrict(LevelView F, LevelView C) {
+  comp_view(F);
+  comp_view(C);
   const int b = blockIdx.x;
   const int B = F.B, Bh = B / 2;
   const int32_t* nb = F.nbr + (size_t)b * 27;
@@ -553,6 +567,8 @@ __global__ void k_restrict(LevelView F, LevelView C) {
 // memory by cp.async; FW evaluated with the same nesting/rounding as k_restrict.
 template <int B>
 __global__ void __launch_bounds__(256) k_restrict2(LevelView F, LevelView C) {
+  comp_view(F);
+  comp_view(C);
   constexpr int T = B + 2, Bh = B / 2, B3 = B * B * B;
   __shared__ double rt[T * T * T];
   __shared__ int snb[27];
@@ -604,13 +620,15 @@ __global__ void __launch_bounds__(256) k_restrict2(LevelView F, LevelView C) {
 
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (fine.B == 16) { k_restrict2<16><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
-  else { k_restrict<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  if (fine.B == 16) { k_restrict2<16><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_restrict<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // FAS right-hand side on the covered coarse nodes (Alg. 1): f = r + Δ u.
 template <int ORDER>
 __global__ void k_fas_rhs(LevelView F, LevelView C) {
+  comp_view(F);
+  comp_view(C);
   const int b = blockIdx.x;
   const int Bh = F.B / 2;
   const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
@@ -625,13 +643,15 @@ __global__ void k_fas_rhs(LevelView F, LevelView C) {
 
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (order == 2) { k_fas_rhs<2><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
-  else if (order == 4) { k_fas_rhs<4><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
-  else { k_fas_rhs<6><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  if (order == 2) { k_fas_rhs<2><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else if (order == 4) { k_fas_rhs<4><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_fas_rhs<6><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // Prolongation of the correction (Alg. 1): u_f += trilinear(u_c - û_c).
 __global__ void k_prolong(LevelView F, LevelView C) {
+  comp_view(F);
+  comp_view(C);
   const int b = blockIdx.x;
   const int B = F.B;
   const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
@@ -666,6 +686,8 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 // block staged once in shared memory; same nesting/rounding as k_prolong.
 template <int B>
 __global__ void __launch_bounds__(256, 5) k_prolong2(LevelView F, LevelView C) {
+  comp_view(F);
+  comp_view(C);
   constexpr int E = B / 2 + 1, B3 = B * B * B;
   __shared__ double eps[E * E * E];
   __shared__ int snb[27];
@@ -711,11 +733,13 @@ __global__ void __launch_bounds__(256, 5) k_prolong2(LevelView F, LevelView C) {
 
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (fine.B == 16) { k_prolong2<16><<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
-  else { k_prolong<<<fine.nreal, 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  if (fine.B == 16) { k_prolong2<16><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_prolong<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
+  comp_view(F);
+  cu += (int64_t)blockIdx.y * C.cs;
   const int b = blockIdx.x;
   const int B = F.B, Bh = B / 2;
   const int p = F.parent[4 * b], ox = F.parent[4 * b + 1], oy = F.parent[4 * b + 2], oz = F.parent[4 * b + 3];
@@ -727,7 +751,7 @@ __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
 }
 
 void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s) {
-  if (fine.nreal) { k_inject_up<<<fine.nreal, 256, 0, s>>>(fine, coarse, coarse_u); ++g_nlaunch; }
+  if (fine.nreal) { k_inject_up<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse, coarse_u); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -737,6 +761,7 @@ void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* co
 // ---------------------------------------------------------------------------------
 template <int ORDER>
 __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
+  comp_view(L);
   const int b = blockIdx.x;
   const int B = L.B, Bh = B / 2;
   const int32_t* nb = L.nbr + (size_t)b * 27;
@@ -770,15 +795,17 @@ __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
 
 void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s) {
   if (!L.nreal) return;
-  if (order == 2) { k_norm<2><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
-  else if (order == 4) { k_norm<4><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
-  else { k_norm<6><<<L.nreal, 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  if (order == 2) { k_norm<2><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else if (order == 4) { k_norm<4><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else { k_norm<6><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
 }
 
 // R_h^M f on all real nodes into tmp (M=4: f + (1/12)Σδ²f, right side of E12), then
 // f <- tmp on leaf nodes only (reading Z16).
 template <int ORDER>
 __global__ void k_rhs_apply(LevelView L, double* tmp) {
+  comp_view(L);
+  tmp += (int64_t)blockIdx.y * L.cs;
   const int b = blockIdx.x;
   const int B = L.B;
   const int32_t* nb = L.nbr + (size_t)b * 27;
@@ -808,6 +835,8 @@ __global__ void k_rhs_apply(LevelView L, double* tmp) {
 }
 
 __global__ void k_rhs_commit(LevelView L, const double* tmp) {
+  comp_view(L);
+  tmp += (int64_t)blockIdx.y * L.cs;
   const int b = blockIdx.x;
   const int B = L.B, Bh = B / 2;
   const uint8_t cov = L.covmask[b];
@@ -820,19 +849,19 @@ __global__ void k_rhs_commit(LevelView L, const double* tmp) {
 
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s) {
   if (!L.nreal || order == 2) return;
-  if (order == 4) { k_rhs_apply<4><<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
-  else { k_rhs_apply<6><<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
-  { k_rhs_commit<<<L.nreal, 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  if (order == 4) { k_rhs_apply<4><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  else { k_rhs_apply<6><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  { k_rhs_commit<<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
 }
 
 // leaf-ordered [n_leaf][B^3] <-> level block storage
 __global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const double* __restrict__ src,
-                               double* const* __restrict__ dst, bool to_levels) {
-  const int n = blockIdx.x;
+                               double* const* __restrict__ dst, const int64_t* __restrict__ lev_cs, bool to_levels) {
+  const int n = blockIdx.x, c = blockIdx.y;
   const int64_t m = map[n];
   const int lev = (int)(m >> 32), blk = (int)(m & 0xffffffff);
-  double* d = dst[lev] + (size_t)blk * B3;
-  const double* sl = src + (size_t)n * B3;
+  double* d = dst[lev] + c * lev_cs[lev] + (size_t)blk * B3;
+  const double* sl = src + ((size_t)c * gridDim.x + n) * B3;
   if (to_levels) {
     for (int i = threadIdx.x; i < B3; i += blockDim.x) d[i] = sl[i];
   } else {
@@ -842,20 +871,70 @@ __global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const do
 }
 
 void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
-                         int nlev, bool to_levels, cudaStream_t s) {
-  (void)nlev;
-  if (nleaf) { k_leaf_scatter<<<nleaf, 256, 0, s>>>(B3, map, src, dst_by_level, to_levels); ++g_nlaunch; }
+                         const int64_t* lev_cs, int nc, bool to_levels, cudaStream_t s) {
+  if (nleaf) { k_leaf_scatter<<<dim3(nleaf, nc), 256, 0, s>>>(B3, map, src, dst_by_level, lev_cs, to_levels); ++g_nlaunch; }
+}
+
+// Field transfer onto an adapted grid (reading A3): one CTA per destination block.
+// rec = (dst block, src block, ox, oy, oz): ox < 0 -> copy the source block (same level
+// and position); else trilinear interpolation of the source level's u on the
+// octant (ox, oy, oz) of source block `src` and the next coarse node beyond it (real or
+// ghost block, refreshed), per axis even -> copy, odd -> mean (the oracle's order).
+__global__ void k_transfer(const int32_t* __restrict__ rec, double* __restrict__ dst, int64_t dcs,
+                           const double* __restrict__ src, int64_t scs, const int32_t* __restrict__ snbr, int B) {
+  const int32_t* r = rec + 5 * blockIdx.x;
+  const int B3 = B * B * B, Bh = B / 2, E = Bh + 1;
+  dst += (int64_t)blockIdx.y * dcs + (size_t)r[0] * B3;
+  src += (int64_t)blockIdx.y * scs;
+  if (r[2] < 0) {
+    const double* s = src + (size_t)r[1] * B3;
+    for (int i = threadIdx.x; i < B3; i += blockDim.x) dst[i] = s[i];
+    return;
+  }
+  extern __shared__ double cw[];  // [E][E][E] coarse window
+  const int32_t* nb = snbr + (size_t)r[1] * 27;
+  for (int i = threadIdx.x; i < E * E * E; i += blockDim.x) {
+    const int x = r[2] + i % E, y = r[3] + (i / E) % E, z = r[4] + i / (E * E);
+    cw[i] = fetch(src, nb, B, x, y, z);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < B3; i += blockDim.x) {
+    const int x = i % B, y = (i / B) % B, z = i / (B * B);
+    const int cx = x >> 1, cy = y >> 1, cz = z >> 1;
+    const int nx = (x & 1) ? 2 : 1, ny = (y & 1) ? 2 : 1, nz = (z & 1) ? 2 : 1;
+    double vz[2];
+    for (int tz = 0; tz < nz; ++tz) {
+      double vy[2];
+      for (int ty = 0; ty < ny; ++ty) {
+        const double* row = cw + ((cz + tz) * E + (cy + ty)) * E + cx;
+        vy[ty] = nx == 2 ? 0.5 * (row[0] + row[1]) : row[0];
+      }
+      vz[tz] = ny == 2 ? 0.5 * (vy[0] + vy[1]) : vy[0];
+    }
+    dst[i] = nz == 2 ? 0.5 * (vz[0] + vz[1]) : vz[0];
+    (void)Bh;
+  }
+}
+
+void launch_transfer(int n, const int32_t* rec, double* dst, int64_t dcs, const double* src, int64_t scs,
+                     const int32_t* snbr, int B, int nc, cudaStream_t s) {
+  if (n <= 0) return;
+  const int E = B / 2 + 1;
+  k_transfer<<<dim3(n, nc), 256, sizeof(double) * E * E * E, s>>>(rec, dst, dcs, src, scs, snbr, B);
+  ++g_nlaunch;
 }
 
 // Cauchy increment of one V-cycle (E20) over the leaf nodes, on the device:
 // out[0] <- max |u_new - u_old|, out[1] <- max |u_new| (bit patterns of non-negative
 // doubles, atomicMax; NaN -> the quiet-NaN pattern), and prev <- u_new for the next cycle.
 __global__ void k_leaf_cauchy(int B3, const int64_t* __restrict__ map, double* __restrict__ prev,
-                              double* const* __restrict__ lev_u, unsigned long long* out) {
-  const int n = blockIdx.x;
+                              double* const* __restrict__ lev_u, const int64_t* __restrict__ lev_cs,
+                              unsigned long long* out) {
+  const int n = blockIdx.x, c = blockIdx.y;
   const int64_t m = map[n];
-  const double* u = lev_u[(int)(m >> 32)] + (size_t)(m & 0xffffffff) * B3;
-  double* p = prev + (size_t)n * B3;
+  const int lev = (int)(m >> 32);
+  const double* u = lev_u[lev] + c * lev_cs[lev] + (size_t)(m & 0xffffffff) * B3;
+  double* p = prev + ((size_t)c * gridDim.x + n) * B3;
   unsigned long long dm = 0ull, um = 0ull;
   for (int i = threadIdx.x; i < B3; i += blockDim.x) {
     const double v = u[i], d = fabs(v - p[i]), a = fabs(v);
@@ -887,8 +966,8 @@ __global__ void k_leaf_cauchy(int B3, const int64_t* __restrict__ map, double* _
 }
 
 void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, double* const* lev_u,
-                        unsigned long long* out, cudaStream_t s) {
-  if (nleaf) { k_leaf_cauchy<<<nleaf, 256, 0, s>>>(B3, map, prev, lev_u, out); ++g_nlaunch; }
+                        const int64_t* lev_cs, int nc, unsigned long long* out, cudaStream_t s) {
+  if (nleaf) { k_leaf_cauchy<<<dim3(nleaf, nc), 256, 0, s>>>(B3, map, prev, lev_u, lev_cs, out); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -903,6 +982,8 @@ struct CoarseAxes {
 };
 
 __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
+  comp_view(L);
+  dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)A.P[0] * A.P[1] * A.P[2];
   if (i >= n) return;
@@ -960,10 +1041,12 @@ void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)P[0] * P[1] * P[2];
-  { k_coarse_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
+  { k_coarse_gather<<<dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
 }
 
 __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, CoarseAxes A) {
+  comp_view(L);
+  dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
   if (i >= n) return;
@@ -974,7 +1057,9 @@ __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ d
       dense[((int64_t)(z + A.off[2]) * A.P[1] + (y + A.off[1])) * A.P[0] + (x + A.off[0])];
 }
 
-__global__ void k_coarse_band(C2FList g, double* u, const double* __restrict__ dense, CoarseAxes A) {
+__global__ void k_coarse_band(C2FList g, double* u, int64_t cs, const double* __restrict__ dense, CoarseAxes A) {
+  u += (int64_t)blockIdx.y * cs;
+  dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   int q[3];
@@ -992,31 +1077,34 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
-  { k_coarse_scatter_nodes<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
-  if (band.n) { k_coarse_band<<<(band.n + 127) / 128, 128, 0, s>>>(band, L.u, dense, A); ++g_nlaunch; }
+  { k_coarse_scatter_nodes<<<dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
+  if (band.n) { k_coarse_band<<<dim3((band.n + 127) / 128, L.nc), 128, 0, s>>>(band, L.u, L.cs, dense, A); ++g_nlaunch; }
 }
 
-__global__ void k_fill_list(int n, const int32_t* __restrict__ idx, double* d, double v) {
+__global__ void k_fill_list(int n, const int32_t* __restrict__ idx, double* d, double v, int64_t cs) {
+  d += (int64_t)blockIdx.y * cs;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) d[idx[i]] = v;
 }
 
-void launch_fill_list(int n, const int32_t* idx, double* d, double v, cudaStream_t s) {
+void launch_fill_list(int n, const int32_t* idx, double* d, double v, int nc, int64_t cs, cudaStream_t s) {
   if (n <= 0) return;
-  k_fill_list<<<(n + 255) / 256, 256, 0, s>>>(n, idx, d, v);
+  k_fill_list<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, idx, d, v, cs);
   ++g_nlaunch;
 }
 
 __global__ void k_copy_signed(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
-                              const int8_t* __restrict__ sgn, double* d, const double* sv) {
+                              const int8_t* __restrict__ sgn, double* d, const double* sv, int64_t cs) {
+  d += (int64_t)blockIdx.y * cs;
+  sv += (int64_t)blockIdx.y * cs;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) d[dst[i]] = (double)sgn[i] * sv[src[i]];
 }
 
 void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
-                        cudaStream_t s) {
+                        int nc, int64_t cs, cudaStream_t s) {
   if (n <= 0) return;
-  k_copy_signed<<<(n + 255) / 256, 256, 0, s>>>(n, dst, src, sgn, d, sv);
+  k_copy_signed<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, dst, src, sgn, d, sv, cs);
   ++g_nlaunch;
 }
 
@@ -1034,6 +1122,7 @@ __global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, in
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)Hx * Py * Pz;
   if (i >= n) return;
+  spec += (int64_t)blockIdx.y * n;
   const int kx = (int)(i % Hx), ky = (int)((i / Hx) % Py), kz = (int)(i / ((int64_t)Hx * Py));
   const double tw = 6.283185307179586476925286766559;
   const double sx = 2.0 * cos(tw * kx / Px) - 2.0, sy = 2.0 * cos(tw * ky / Py) - 2.0, sz = 2.0 * cos(tw * kz / Pz) - 2.0;
@@ -1043,20 +1132,21 @@ __global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, in
   spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
 }
 
-void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, cudaStream_t s) {
+void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, int nc, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  { k_mul_periodic<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h); ++g_nlaunch; }
+  { k_mul_periodic<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h); ++g_nlaunch; }
 }
 
 __global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mult, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  spec += (int64_t)blockIdx.y * n;
   const double m = mult[i];
   spec[i] = make_cuDoubleComplex(cuCreal(spec[i]) * m, cuCimag(spec[i]) * m);
 }
 
-void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, cudaStream_t s) {
-  { k_mul_table<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
+void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, cudaStream_t s) {
+  { k_mul_table<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
 }
 
 // Multiplier of a mixed periodic / unbounded coarse solve on the R2C spectrum (x halved):

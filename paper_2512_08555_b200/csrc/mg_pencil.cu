@@ -227,7 +227,7 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
     const int p = tid % 9, sx = p % 3 - 1, sy = p / 3 - 1;
     const int mi = (sx != 0) + 2 * (sy != 0);
     const CUtensorMap* map = tid < 9 ? &cx.tm->u[mi] : &cx.tm->f[mi];
-    const int blk = snb[k * 27 + p + 9 * (dz + 1)];
+    const int blk = snb[k * 27 + p + 9 * (dz + 1)] + (int)blockIdx.y * L.ntot;  // component c: blocks c ntot + .
     if (tid == 0) {
       fence_proxy_async();
       mbar_expect_tx(cx.bar + slot, S::PLANE_BYTES);
@@ -378,6 +378,7 @@ template <int ORDER, int D, int RR, int NREG, bool SW, bool TMA>
 __global__ void __maxnreg__(NREG)
     k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d, const __grid_constant__ TileMaps tm) {
   using S = RBShape<D, RR, TMA>;
+  comp_view(L);
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
   extern __shared__ __align__(16) double smraw[];
   __shared__ int snb[PMAXL * 27];
@@ -633,6 +634,7 @@ __device__ __forceinline__ void rb6_body(const LevelView& L, const RBCtx& cx, in
 template <int NREG, bool SW>
 __global__ void __maxnreg__(NREG) k_rb6_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
   using S = RB6Shape;
+  comp_view(L);
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
   extern __shared__ __align__(16) double sm[];
   __shared__ int snb[PMAXL * 27];
@@ -710,6 +712,7 @@ template <int ORDER, int D, int MODE = 0>
 __global__ void __launch_bounds__(ResShape<D>::NT, 4)
     k_res_pencil(LevelView L, double inv_h2, unsigned long long* out = nullptr) {
   using S = ResShape<D>;
+  comp_view(L);
   constexpr int T = S::T, TP = S::TP, FP = S::FP, R = S::R, NT = S::NT;
   extern __shared__ __align__(16) double sm[];
   double* su = sm;           // [R][TP]
@@ -867,6 +870,8 @@ template <int ORDER>
 __global__ void __maxnreg__(80)
     k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
   using S = RR2Shape;
+  comp_view(L);
+  comp_view(C);
   constexpr int T = S::T, TW = S::TW, TP = S::TP, D = S::D, R = S::R, NR = S::NR, NT = S::NT;
   constexpr int SXW = S::SXW, SXP = S::SXP;
   extern __shared__ __align__(16) double sm[];
@@ -1043,9 +1048,9 @@ __global__ void __maxnreg__(80)
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (fine.B != PB || fine.npen <= 0 || fine.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (fine.h * fine.h);
-  if (order == 2) k_rr2_pencil<2><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
-  else if (order == 4) k_rr2_pencil<4><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
-  else k_rr2_pencil<6><<<fine.npen, RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  if (order == 2) k_rr2_pencil<2><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else if (order == 4) k_rr2_pencil<4><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else k_rr2_pencil<6><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
   note_launch();
   return true;
 }
@@ -1123,9 +1128,9 @@ static bool res_pencil_launch(const LevelView& L, int order, unsigned long long*
   const double inv_h2 = 1.0 / (L.h * L.h);
   constexpr int NT = ResShape<RES_D>::NT;
   constexpr size_t SM = ResShape<RES_D>::SMEM;
-  if (order == 2) k_res_pencil<2, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
-  else if (order == 4) k_res_pencil<4, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
-  else k_res_pencil<6, RES_D, MODE><<<L.npen, NT, SM, s>>>(L, inv_h2, out);
+  if (order == 2) k_res_pencil<2, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
+  else if (order == 4) k_res_pencil<4, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
+  else k_res_pencil<6, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
   note_launch();
   return true;
 }
@@ -1135,8 +1140,8 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
   if (order == 6) {
     const double inv_h2 = 1.0 / (L.h * L.h);
     const double inv_d = 1.0 / ((-128.0 / 30.0) * inv_h2);
-    if (L.sw_npen > 0) k_rb6_pencil<RB6_NREG, true><<<L.sw_npen, 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
-    else k_rb6_pencil<RB6_NREG, false><<<L.npen, 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
+    if (L.sw_npen > 0) k_rb6_pencil<RB6_NREG, true><<<dim3(L.sw_npen, L.nc), 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
+    else k_rb6_pencil<RB6_NREG, false><<<dim3(L.npen, L.nc), 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
     note_launch();
     return true;
   }
@@ -1149,16 +1154,16 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
   if (tm) {
     if (L.sw_npen > 0)
       (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, true>)
-          <<<grid, RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+          <<<dim3(grid, L.nc), RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
     else
       (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, true>)
-          <<<grid, RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+          <<<dim3(grid, L.nc), RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   } else if (L.sw_npen > 0) {
     (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, false>)
-        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+        <<<dim3(grid, L.nc), RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   } else {
     (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>)
-        <<<grid, RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
+        <<<dim3(grid, L.nc), RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   }
   note_launch();
   return true;

@@ -26,7 +26,7 @@ MG_ALL_BLOCKS = 0x10000
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
            "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
-           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison"]
+           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison", "mg_transfer"]
 STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm"]
 
 
@@ -36,7 +36,7 @@ class MgDesc(C.Structure):
                 ("coarse_n", C.c_int32), ("smoother", C.c_int32), ("omega", C.c_double),
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
                 ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
-                ("zsplit", C.c_int32), ("fuse", C.c_int32), ("staging", C.c_int32)]
+                ("zsplit", C.c_int32), ("fuse", C.c_int32), ("ncomp", C.c_int32), ("staging", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -75,6 +75,7 @@ def load_library(path: str = _LIB_PATH):
     lib.mg_debug_field.argtypes = [P, I, I, I, P]
     lib.mg_debug_apply.argtypes = [P, I, I]
     lib.mg_debug_poison.argtypes = [P]
+    lib.mg_transfer.argtypes = [P, P]
     lib.mg_time_op.argtypes = [P, I, I, I, C.POINTER(D)]
     lib.mg_profile.argtypes = [P, I]
     lib.mg_profile_read.argtypes = [P, C.POINTER(D), C.POINTER(C.c_int64)]
@@ -171,6 +172,8 @@ class Solver:
         d.zsplit = int(cfg.get("zsplit", 0))
         d.fuse = int(cfg.get("fuse", 0))
         d.staging = int(cfg.get("staging", 0))
+        d.ncomp = int(cfg.get("ncomp", 1))
+        self.nc = max(1, d.ncomp)
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))
         self.B = int(cfg["B"])
@@ -201,7 +204,9 @@ class Solver:
             pass
 
     def leaf_shape(self):
-        return (self.n_leaf, self.B, self.B, self.B)
+        """[n_leaf, B, B, B], or [ncomp, n_leaf, B, B, B] for a batched handle."""
+        s = (self.n_leaf, self.B, self.B, self.B)
+        return (self.nc,) + s if self.nc > 1 else s
 
     # ---------------------------------------------------------------- API
     def set_rhs(self, f):
@@ -232,12 +237,24 @@ class Solver:
         return c.value, v.value, rc == MG_OK
 
     def solve_vector(self, f_components, tol, max_cycles=50, criterion=MG_CRIT_RESIDUAL):
-        """Vector Poisson problem, one scalar solve per component on this handle (the
-        Biot–Savart law ∇²u = -∇×ω of P:627-631: layout, tables, LGF multipliers and
-        CUDA graphs are shared by the components).  f_components: sequence of
-        leaf-ordered device tensors; returns ([u_c], [(cycles, rel, converged)]).
-        A zero component is solved exactly by u = 0 without cycling."""
+        """Vector Poisson problem (the Biot–Savart law ∇²u = -∇×ω of P:627-631).
+        On a handle created with ncomp = len(f_components) all components go through ONE
+        batched solve: every V-cycle kernel launch covers all components, the tables,
+        ghost boxes and the coarse-solve FFT plan are shared, the stopping test is the
+        max over components (returns one stats tuple per component, all equal).
+        Otherwise one scalar solve per component on this handle (a zero component is
+        solved exactly by u = 0 without cycling).  f_components: sequence of leaf-ordered
+        device tensors; returns ([u_c], [(cycles, rel, converged)])."""
         import torch
+        if self.nc > 1:
+            if len(f_components) != self.nc:
+                raise ValueError(f"handle has ncomp={self.nc}, got {len(f_components)} components")
+            f = torch.stack([t.contiguous() for t in f_components]).contiguous()
+            self.set_rhs(f)
+            self.set_solution(torch.zeros_like(f))
+            st = self.solve(tol, max_cycles, criterion)
+            u = self.get_solution()
+            return [u[c] for c in range(self.nc)], [st] * self.nc
         us, stats = [], []
         for f in f_components:
             if not bool(torch.any(f != 0)):
@@ -287,6 +304,11 @@ class Solver:
             self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 2 if ghosts else 0, _ptr(out)))
             return out
         self._check(self.lib.mg_debug_field(self.h, int(field), int(m), 3 if ghosts else 1, _ptr(tensor)))
+
+    def transfer_from(self, other):
+        """mg_transfer: u on this (adapted) grid from the solution of `other` (call after
+        set_rhs)."""
+        self._check(self.lib.mg_transfer(self.h, other.h))
 
     def debug_poison(self):
         """NaN into every ghost-block node outside the needed halo (mg_debug_poison)."""

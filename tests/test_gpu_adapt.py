@@ -74,3 +74,38 @@ def test_adaptation_pipeline_matches_oracle_and_solves():
     s.set_rhs(torch.from_numpy(S.sample_on_leaves(dom, lv, blob)).cuda())
     cyc, rel, ok = s.solve(1e-9, 30)
     assert ok, (cyc, rel)
+
+
+@pytest.mark.gpu
+def test_transfer_onto_adapted_grid_matches_oracle():
+    """mg_transfer (reading A3): after 3 V-cycles on the old grid, u moves onto an adapted
+    grid (one x-block coarsened, one refined; x periodic, y, z unbounded) exactly as the
+    oracle's transfer_from (copies bit for bit, trilinear within round-off), and the
+    adapted grid solves from that warm start."""
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    from tests.test_oracle_adapt import _transfer_pair
+    from workloads import sources as S
+    MO, d, old_lv, new_lv = _transfer_pair()
+    dom = C.domain(d)
+    src = lambda x, y, z: S.gaussian_charge(x, y, z, sigma=0.06, c=(0.35, 0.5, 0.5))  # noqa: E731
+    f_old = S.sample_on_leaves(dom, old_lv, src)
+    f_new = S.sample_on_leaves(dom, new_lv, src)
+    o_old = MO.Oracle(d, old_lv)
+    o_old.set_rhs(f_old)
+    o_old.vcycle(3)
+    g_old = Solver(d, old_lv)
+    g_old.set_rhs(torch.from_numpy(f_old).cuda())
+    g_old.vcycle(3)
+    o_new = MO.Oracle(d, new_lv)
+    o_new.set_rhs(f_new)
+    o_new.transfer_from(o_old)
+    g_new = Solver(d, new_lv)
+    g_new.set_rhs(torch.from_numpy(f_new).cuda())
+    g_new.transfer_from(g_old)
+    ug, uo = g_new.get_solution().cpu().numpy(), o_new.get_solution()
+    assert np.abs(ug - uo).max() <= 1e-9 * np.abs(uo).max()
+    r0 = g_new.residual_norm()[1]
+    cyc, rel, ok = g_new.solve(1e-10, 30)
+    assert ok and r0 < 0.5

@@ -40,3 +40,58 @@ def test_tube_fullsize_vector_solve_vs_analytic():
         # 1/128 outside): 4.24e-7 on the B200 and in the oracle on the same x-y layout
         # (the uniform 1/256 grid: 4.1e-7); a wrong sign, component or scaling is O(1)
         assert err < 1e-6, (comp, err)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["puu2", "cfg3_64", "per_adapt", "cfg5_small"])
+def test_batched_components_bitwise_equal_scalar(name):
+    """ncomp = 3 (mg_desc.ncomp): one V-cycle carries three right-hand sides through the
+    same launches (gridDim.y = component).  Each component equals, bit for bit, the
+    scalar solve of that right-hand side, and the oracle within the V-cycle tolerance."""
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    from oracle.mg_oracle import Oracle
+    from tests.test_gpu_parity import _cfg
+    cfg, lv, f = _cfg(name)
+    rng = np.random.default_rng(7)
+    fs = [f, -0.5 * f[::-1].copy(), f * rng.uniform(0.5, 2.0)]   # three different fields on the layout
+    cb = dict(cfg)
+    cb["ncomp"] = 3
+    sb = Solver(cb, lv)
+    sb.set_rhs(torch.from_numpy(np.stack(fs)).cuda())
+    sb.vcycle(2)
+    ub = sb.get_solution().cpu().numpy()
+    a, r = sb.residual_norm()
+    norms = []
+    for c in range(3):
+        s = Solver(cfg, lv)
+        s.set_rhs(torch.from_numpy(fs[c]).cuda())
+        s.vcycle(2)
+        assert np.array_equal(ub[c], s.get_solution().cpu().numpy()), c
+        norms.append(s.residual_norm()[0])
+        if c == 0:
+            o = Oracle(cfg, lv)
+            o.set_rhs(fs[c])
+            o.vcycle(2)
+            assert rel_err(ub[c], o.get_solution()) < 1e-9
+    assert a == max(norms)
+
+
+@pytest.mark.gpu
+def test_tube_batched_vector_solve_vs_analytic():
+    """The vortex-tube velocity as ONE 3-component solve (ncomp = 3)."""
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    cfg = dict(C.tube())
+    dom, lv, f3, u3 = C.build_vector(cfg)
+    cfg["ncomp"] = 3
+    s = Solver(cfg, lv)
+    s.use_graph(True)
+    us, stats = s.solve_vector([torch.from_numpy(f).cuda() for f in f3], cfg["tol"], 30)
+    assert stats[0][2], stats
+    assert float(us[2].abs().max()) == 0.0        # f_z = 0 -> u_z = 0 exactly
+    for comp in (0, 1):
+        err = np.abs(us[comp].cpu().numpy() - u3[comp]).max()
+        assert err < 1e-6, (comp, err)

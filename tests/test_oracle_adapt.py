@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import adapt as OA
+from workloads import sources as S
 from workloads import configs as C
 from workloads import layouts as Lay
 
@@ -166,3 +167,41 @@ def test_host_abi_adapt_rejects_invalid_input():
                           g.ctypes.data_as(Cc.POINTER(Cc.c_double)), 1.0, 0.1, 3,
                           out.ctypes.data_as(Cc.POINTER(I32)), 4096, Cc.byref(n_out), None)
         assert rc == code, (rc, code)
+
+
+# ------------------------------------------------------------- field transfer (A3)
+def _transfer_pair(poly=None):
+    from oracle import mg_oracle as MO
+    dom = Lay.Domain((0.0, 0.0, 0.0), 1 / 64, (4, 4, 4), 16, (0, 1, 1))
+    d = dict(origin=(0.0, 0.0, 0.0), h0=1 / 64, base_blocks=(4, 4, 4), B=16, bc=(0, 1, 1), order=4, smoother=1,
+             omega=1.0, eta1=2, eta2=2, coarse_n=0)
+    t = Lay.Tree(dom)
+    for b in sorted(t.nodes[0]):
+        if all(1 <= b[a] <= 2 for a in (1, 2)) and b[0] in (0, 1):
+            t.refine(0, b)
+    old_lv = t.leaves()
+    t2 = Lay.Tree(dom)                      # adapted: x-block 0 coarsened, x-block 2 refined
+    for b in sorted(t2.nodes[0]):
+        if all(1 <= b[a] <= 2 for a in (1, 2)) and b[0] in (1, 2):
+            t2.refine(0, b)
+    new_lv = t2.leaves()
+    return MO, d, old_lv, new_lv
+
+
+def test_transfer_trilinear_exact_and_identity():
+    """The transfer reproduces a trilinear field exactly on refined, kept and coarsened
+    blocks (prolongation exactness + injection), and is the identity when the layout is
+    unchanged.  (x is periodic: the refined region stays clear of the wrap, where a
+    polynomial is not periodic.)"""
+    MO, d, old_lv, new_lv = _transfer_pair()
+    o_old = MO.Oracle(d, old_lv)
+    fn = lambda x, y, z: 1.0 + 2.0 * x - y + 0.5 * z + 0.3 * x * y - 0.7 * y * z + 0.2 * x * y * z  # noqa: E731
+    dom = Lay.Domain((0.0, 0.0, 0.0), 1 / 64, (4, 4, 4), 16, (0, 1, 1))
+    o_old.set_solution(S.sample_on_leaves(dom, old_lv, fn))
+    o_new = MO.Oracle(d, new_lv)
+    o_new.transfer_from(o_old)
+    want = S.sample_on_leaves(dom, new_lv, fn)
+    assert np.abs(o_new.get_solution() - want).max() < 1e-13
+    o_same = MO.Oracle(d, old_lv)
+    o_same.transfer_from(o_old)
+    assert np.array_equal(o_same.get_solution(), o_old.get_solution())
