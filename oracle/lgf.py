@@ -17,6 +17,7 @@ elsewhere 1/σ_ℒ(k) of the 3D operator.  Here the periodic axis is x (reading 
 """
 from __future__ import annotations
 
+import functools
 import math
 
 import numpy as np
@@ -90,7 +91,13 @@ def _apply_op(G, order):
 
 
 def box_lgf(dim: int, order: int, R: int) -> np.ndarray:
-    """G on the box [-R, R]^dim (index n+R), solving ℒG = δ exactly inside."""
+    """G on the box [-R, R]^dim (index n+R), solving ℒG = δ exactly inside.  (A read-only
+    table, memoised per (dim, order, R): the tests build many oracles on one domain.)"""
+    return _box_lgf(dim, order, R)
+
+
+@functools.lru_cache(maxsize=8)
+def _box_lgf(dim: int, order: int, R: int) -> np.ndarray:
     n = 2 * R + 1
     idx = np.arange(-R, R + 1, dtype=np.float64)
     grids = np.meshgrid(*([idx] * dim), indexing="ij")
@@ -123,6 +130,7 @@ def box_lgf(dim: int, order: int, R: int) -> np.ndarray:
     G[inner] = Gi
     if dim == 2:
         G = G - G[R, R]
+    G.setflags(write=False)
     return G
 
 
