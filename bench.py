@@ -374,17 +374,28 @@ def measure(S, cfg, args, dist, dev, ws, local, with_clocks=True):
 
 
 def smoother_residual(S, levels):
-    """The fused smoother+residual kernel (K4: the last pre-sweep and
-    r = f - Δu in one pass, 32 B per unknown) on the finest level, 20 launches alone."""
+    """The smoother + residual of the last pre-smoothing step on the
+    finest level, kernels only (no ghost refresh), 20 launches each: the production pair
+    (RB pencil sweep 24 B + residual pencil kernel 24 B per unknown; in the V-cycle the
+    residual is fused with the restriction instead) and the single-pass fused tile kernel
+    (32 B per unknown); fractions of the measured HBM peak on each one's bytes, and of
+    the pair against the 32 B a single pass needs."""
     top = len(levels) - 1
     Nf = levels[top]["nreal"] * levels[top]["B"] ** 3
     peak = peak_hbm()[0]
-    S.time_op("smooth_residual", top, 3)
-    ms = S.time_op("smooth_residual", top, 20)
-    gbs = 32 * Nf / (ms * 1e-3) / 1e9
-    return {"kernel": "MG_OP_SMOOTH_RESIDUAL on the finest level (refresh + fused RB sweep + residual)",
-            "avg_ms": ms, "unknowns": Nf, "alg_bytes_per_unknown": 32, "gbs": gbs, "frac": gbs / peak,
-            "unknowns_per_s": Nf / (ms * 1e-3)}
+    out = {}
+    for name, op, bpu in (("pair", "smooth_residual_pair", 48), ("fused_tile", "smooth_residual_fused_tile", 32)):
+        S.time_op(op, top, 3)
+        ms = S.time_op(op, top, 20)
+        gbs = bpu * Nf / (ms * 1e-3) / 1e9
+        out[name] = {"avg_ms": ms, "alg_bytes_per_unknown": bpu, "gbs": gbs, "frac": gbs / peak,
+                     "frac_vs_single_pass_32B": 32 * Nf / (ms * 1e-3) / 1e9 / peak,
+                     "unknowns_per_s": Nf / (ms * 1e-3)}
+    out["what"] = ("finest level, kernels only: 'pair' = k_rb_pencil then k_res_pencil (production; in the "
+                   "V-cycle the residual is fused with the restriction, k_rr2_pencil); 'fused_tile' = one "
+                   "k_smooth2 pass (halo-3 tile: red, black and r = f - Lu)")
+    out["unknowns"] = Nf
+    return out
 
 
 def run_mine(args, ws, rank, local, dist):

@@ -179,7 +179,10 @@ int mg_debug_apply(mg_handle* h, int op, int level);
  * in all level fields.  Call after mg_set_rhs; a later result that reads one turns
  * non-finite.  Synchronises. */
 int mg_debug_poison(mg_handle* h);
-/* Time one operator: runs it `reps` times between CUDA events, returns ms per rep. */
+/* Time one operator: runs it `reps` times between CUDA events, returns ms per rep.
+ * op: an MG_OP_*, 100 = one V-cycle, -1 = the bare fused RB sweep + residual tile kernel
+ * of the level, -2 = the bare production pair (RB pencil sweep, then residual pencil
+ * kernel); no ghost refresh for -1 / -2. */
 int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out);
 
 /* Per-stage CUDA-event profiling of non-graph launches.  mg_profile(h, 1) clears

@@ -1785,10 +1785,21 @@ int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out) {
     CUDA_OK(cudaEventCreate(&b));
     CUDA_OK(cudaEventRecord(a, h->s));
     for (int i = 0; i < reps; ++i) {
-      if (op < 0) {
-        // op -1: the bare smoother kernel (fused RB+residual if `level` is ghost-free)
+      if (op == -1) {
+        // the bare fused smoother + residual tile kernel (k_smooth2 with the residual),
+        // no ghost refresh (boundary ghosts as they are)
         const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
         launch_smooth(view(h, level), h->order, mode, h->omega, true, h->s);
+      } else if (op == -2) {
+        // the bare production pair: RB pencil sweep, then the residual pencil kernel
+        Level& l = h->L[level];
+        const LevelView v = view(h, level);
+        if (h->smoother != MG_SMOOTHER_RBGS || !launch_rb_pencil(v, h->order, h->omega, nullptr, h->s))
+          launch_smooth(v, h->order, h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI, h->omega, false, h->s);
+        swap_u(l);
+        residual_kernel(h, level);
+      } else if (op < 0) {
+        throw MgError(MG_ERR_ARG, "bad op");
       } else if (op == 100) {
         run_vcycles(h, 1);
       } else {

@@ -334,6 +334,7 @@ class Solver:
 
     def time_op(self, op, m, reps):
         ms = C.c_double()
-        code = {"smooth_kernel": -1, "vcycle": 100}.get(op, OPS.get(op, op)) if isinstance(op, str) else op
+        code = {"smooth_residual_fused_tile": -1, "smooth_residual_pair": -2, "vcycle": 100}.get(
+            op, OPS.get(op, op)) if isinstance(op, str) else op
         self._check(self.lib.mg_time_op(self.h, int(code), int(m), int(reps), C.byref(ms)))
         return ms.value
