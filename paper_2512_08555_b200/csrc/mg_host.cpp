@@ -499,8 +499,14 @@ bool is_real_node(const mg_handle* h, const Level& l, int Jx, int Jy, int Jz, in
 
 void build_ghosts(mg_handle* h) {
   const int nlev = (int)h->L.size();
-  // halo read by one sweep (RB: 2), and by the radius-2 right-hand side of M = 6
-  const int g = (h->smoother == MG_SMOOTHER_RBGS || h->order == 6) ? 2 : 1;
+  // needed halo: every stencil, sweep, residual, transfer and norm evaluates live nodes
+  // only, whose operands lie within Chebyshev distance 1 of a real block (the sweeps stage
+  // a halo-2 tile, but a ring node at distance 1 is updated only when it is itself real,
+  // and then its operands are within distance 1 of its own block); the radius-2 right-hand
+  // side of M = 6 needs f at distance 2 (round 1 filled distance 2 for every RB level).
+  // tests/test_gpu_edge.py poisons every ghost node outside this set with NaN and checks
+  // that nothing reads one.
+  const int g = h->order == 6 ? 2 : 1;
   for (int m = nlev - 1; m >= 0; --m) {
     Level& l = h->L[m];
     // halo ghosts: nodes within Chebyshev distance g of a real block, not in one
