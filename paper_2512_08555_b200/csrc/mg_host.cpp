@@ -6,6 +6,7 @@
 // schedule of sm_100a kernel launches (optionally one CUDA graph per V-cycle).
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -159,6 +160,17 @@ struct mg_handle {
   int coarse_kind = 0;  // 0 all periodic, 1 all unbounded, 2 any mix (see setup_coarse)
   int P[3] = {0, 0, 0};
   cufftHandle plan_f = 0, plan_b = 0;
+  // pruned coarse solve (x periodic, y and z unbounded, the cfg4 / cfg5 / tube-like mixes):
+  // 1-D transforms that skip the zero half of the padded source and the outputs outside
+  // the [-GE, N + GE) window (see coarse_solve_pruned)
+  bool pruned = false;
+  cufftHandle pr_xf = 0, pr_y = 0, pr_z = 0, pr_y1 = 0, pr_y2 = 0, pr_xb = 0;
+  double *pr_X = nullptr, *pr_R = nullptr, *pr_mult = nullptr;
+  void *pr_C1 = nullptr, *pr_C2 = nullptr, *pr_C3 = nullptr;
+  int pr_W[3] = {0, 0, 0};  // window (x periodic: N; y, z: N + 2 GE)
+  std::vector<cufftHandle*> plans() {
+    return {&plan_f, &plan_b, &pr_xf, &pr_y, &pr_z, &pr_y1, &pr_y2, &pr_xb};
+  }
   double* d_dense = nullptr;
   void* d_spec = nullptr;
   double* d_mult = nullptr;  // kinds 1, 2: full multiplier table on the R2C spectrum
@@ -195,19 +207,26 @@ cudaEvent_t get_ev(mg_handle* h) {
   return e;
 }
 
-// RAII event pair around one stage on the handle's stream (only when profiling).
+const char* const kStageName[ST_COUNT] = {"mg smooth", "mg smooth+residual", "mg residual", "mg ghost fill",
+                                          "mg restrict", "mg prolong", "mg coarse solve", "mg inject-up",
+                                          "mg norm"};
+
+// RAII around one stage: an NVTX range (host timeline, for nsys / ncu --nvtx filters)
+// and, when profiling, a CUDA event pair on the handle's stream.
 struct Prof {
   mg_handle* h;
   int st, lv;
   cudaEvent_t a = nullptr;
   bool on;
   Prof(mg_handle* hh, int stage, int level) : h(hh), st(stage), lv(level), on(hh->prof_on) {
+    nvtxRangePushA(kStageName[stage]);
     if (on) {
       a = get_ev(h);
       cudaEventRecord(a, h->s);
     }
   }
   ~Prof() {
+    nvtxRangePop();
     if (!on) return;
     cudaEvent_t b = get_ev(h);
     cudaEventRecord(b, h->s);
@@ -302,6 +321,7 @@ void validate_and_build(mg_handle* h) {
     if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
     if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
+    if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 1)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..1");
     if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1 || d.staging < 0 || d.staging > 1))
       throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse and staging 0..1");
     // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
@@ -963,6 +983,8 @@ void setup_coarse(mg_handle* h) {
   h->coarse_kind = nunb == 0 ? 0 : (nunb == 3 ? 1 : 2);
   const int Px = h->P[0], Py = h->P[1], Pz = h->P[2];
   const int64_t nd = (int64_t)Px * Py * Pz, nc = (int64_t)(Px / 2 + 1) * Py * Pz;
+  h->pruned = h->coarse_kind == 2 && h->per[0] && !h->per[1] && !h->per[2] && !h->sym[0] && !h->sym[1] &&
+               !h->sym[2] && !h->hi_odd[0] && !h->hi_even[0] && h->d.coarse_pruning != 1;
   // one batched transform over the components (dense [ncomp][Pz][Py][Px])
   CUDA_OK(cudaMalloc(&h->d_dense, (size_t)h->nc * nd * sizeof(double)));
   CUDA_OK(cudaMalloc(&h->d_spec, (size_t)h->nc * nc * sizeof(cufftDoubleComplex)));
@@ -1040,11 +1062,39 @@ void setup_coarse(mg_handle* h) {
       dLow = dev_upload(T1);
     }
     CUDA_OK(cudaMalloc(&h->d_mult, nc * sizeof(double)));
-    launch_build_mult(h->d_mult, h->P, h->fper, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, h->s);
+    launch_build_mult(h->d_mult, h->P, h->fper, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, 0, h->s);
+    if (h->pruned) {
+      // the same multipliers in the [kz][kx][ky] layout of the pruned transforms
+      CUDA_OK(cudaMalloc(&h->pr_mult, nc * sizeof(double)));
+      launch_build_mult(h->pr_mult, h->P, h->fper, ua, ub, dLow, h->order, c.h * c.h, 1.0 / (double)nd, 1, h->s);
+    }
     CUDA_OK(cudaStreamSynchronize(h->s));
     cudaFree(dLow);
   }
   CUDA_OK(cudaStreamSynchronize(h->s));
+  if (h->pruned) {
+    const int Nx = c.N[0], Ny = c.N[1], Nz = c.N[2], Hx = Nx / 2 + 1, Py = h->P[1], Pz = h->P[2], GE = h->GE;
+    const int Wy = Ny + 2 * GE, Wz = Nz + 2 * GE, nc = h->nc;
+    h->pr_W[0] = Nx;
+    h->pr_W[1] = Wy;
+    h->pr_W[2] = Wz;
+    const size_t cz = sizeof(cufftDoubleComplex);
+    CUDA_OK(cudaMalloc(&h->pr_X, (size_t)nc * Nz * Ny * Nx * sizeof(double)));
+    CUDA_OK(cudaMalloc(&h->pr_C1, (size_t)nc * Nz * Ny * Hx * cz));
+    CUDA_OK(cudaMalloc(&h->pr_C2, (size_t)nc * Pz * Hx * Py * cz));
+    CUDA_OK(cudaMalloc(&h->pr_C3, (size_t)nc * Wz * Wy * Hx * cz));
+    CUDA_OK(cudaMalloc(&h->pr_R, (size_t)nc * Wz * Wy * Nx * sizeof(double)));
+    int n1 = Nx;
+    CUFFT_OK(cufftPlanMany(&h->pr_xf, 1, &n1, nullptr, 1, Nx, nullptr, 1, Hx, CUFFT_D2Z, nc * Nz * Ny));
+    CUFFT_OK(cufftPlanMany(&h->pr_xb, 1, &n1, nullptr, 1, Hx, nullptr, 1, Nx, CUFFT_Z2D, nc * Wz * Wy));
+    int ny = Py, nz = Pz, emb = Pz;
+    CUFFT_OK(cufftPlanMany(&h->pr_y, 1, &ny, nullptr, 1, Py, nullptr, 1, Py, CUFFT_Z2Z, Nz * Hx));
+    CUFFT_OK(cufftPlanMany(&h->pr_y1, 1, &ny, nullptr, 1, Py, nullptr, 1, Py, CUFFT_Z2Z, (Nz + GE) * Hx));
+    CUFFT_OK(cufftPlanMany(&h->pr_y2, 1, &ny, nullptr, 1, Py, nullptr, 1, Py, CUFFT_Z2Z, GE * Hx));
+    CUFFT_OK(cufftPlanMany(&h->pr_z, 1, &nz, &emb, Hx * Py, 1, &emb, Hx * Py, 1, CUFFT_Z2Z, Hx * Py));
+    for (cufftHandle* p : {&h->pr_xf, &h->pr_xb, &h->pr_y, &h->pr_y1, &h->pr_y2, &h->pr_z})
+      CUFFT_OK(cufftSetStream(*p, h->s));
+  }
   // level-0 exterior f ghosts beyond symmetric low faces: signed mirror copies of real
   // level-0 nodes (f := 0 beyond unbounded faces, Z16; reading S1)
   if (h->sym[0] || h->sym[1] || h->sym[2]) {
@@ -1216,7 +1266,45 @@ void prolong_level(mg_handle* h, int m) {
   launch_prolong(view(h, m), view(h, m - 1), h->s);
 }
 
+// The x-periodic, y/z-unbounded solve with 1-D transforms (the 3-D R2C factorised, so the
+// multiplier and the values are those of the 3-D path up to rounding): R2C along x of
+// the N^3 source only; along y (zero-padded to Py) only the Nz source planes; along z
+// every line; the multiplier; back along z every line, along y only the planes of the
+// output window z in [-GE, N + GE); C2R along x only the (z, y) window lines.  The zero
+// half of the padded source and the outputs nobody reads are never transformed.
+void coarse_solve_pruned(mg_handle* h) {
+  Prof pr(h, ST_COARSE, 0);
+  LevelView c = view(h, 0);
+  const Level& l0 = h->L[0];
+  const int Nx = l0.N[0], Ny = l0.N[1], Nz = l0.N[2], Hx = Nx / 2 + 1, Py = h->P[1], Pz = h->P[2], GE = h->GE;
+  const int N[3] = {Nx, Ny, Nz}, zero[3] = {0, 0, 0};
+  launch_coarse_gather(c, h->pr_X, N, zero, zero, zero, zero, h->s);
+  CUFFT_OK(cufftExecD2Z(h->pr_xf, h->pr_X, (cufftDoubleComplex*)h->pr_C1));
+  launch_spec_pad_y(h->pr_C1, h->pr_C2, Nz, Ny, Hx, Py, Pz, h->nc, h->s);
+  const size_t plane = (size_t)Hx * Py, comp = (size_t)Pz * plane;
+  auto C2 = [&](int cc, int z) { return (cufftDoubleComplex*)h->pr_C2 + cc * comp + (size_t)z * plane; };
+  for (int cc = 0; cc < h->nc; ++cc) {
+    CUDA_OK(cudaMemsetAsync(C2(cc, Nz), 0, (size_t)(Pz - Nz) * plane * sizeof(cufftDoubleComplex), h->s));
+    CUFFT_OK(cufftExecZ2Z(h->pr_y, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
+    CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
+  }
+  launch_coarse_mul_table(h->pr_C2, h->pr_mult, (int64_t)comp, h->nc, h->s);
+  for (int cc = 0; cc < h->nc; ++cc) {
+    CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
+    CUFFT_OK(cufftExecZ2Z(h->pr_y1, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
+    CUFFT_OK(cufftExecZ2Z(h->pr_y2, C2(cc, Pz - GE), C2(cc, Pz - GE), CUFFT_INVERSE));
+  }
+  launch_spec_window(h->pr_C2, h->pr_C3, h->pr_W[2], h->pr_W[1], Hx, Py, Pz, GE, h->nc, h->s);
+  CUFFT_OK(cufftExecZ2D(h->pr_xb, (cufftDoubleComplex*)h->pr_C3, h->pr_R));
+  const int off[3] = {0, GE, GE};
+  launch_coarse_scatter(c, h->pr_R, h->pr_W, off, c2f_list(h->L[0]), h->s);
+}
+
 void coarse_solve(mg_handle* h) {
+  if (h->pruned) {
+    coarse_solve_pruned(h);
+    return;
+  }
   Prof pr(h, ST_COARSE, 0);
   LevelView c = view(h, 0);
   launch_coarse_gather(c, h->d_dense, h->P, h->sym, h->hi_odd, h->hi_even, h->coff, h->s);
@@ -1287,8 +1375,8 @@ void run_vcycles(mg_handle* h, int n) {
     auto restore = [&] {
       h->s = orig;
       h->prof_on = prof;
-      cufftSetStream(h->plan_f, orig);
-      cufftSetStream(h->plan_b, orig);
+      for (cufftHandle* p : h->plans())
+        if (*p) cufftSetStream(*p, orig);
       if (g) cudaGraphDestroy(g);
       g = nullptr;
       if (cap) cudaStreamDestroy(cap);
@@ -1298,8 +1386,8 @@ void run_vcycles(mg_handle* h, int n) {
       CUDA_OK(cudaStreamSynchronize(orig));
       h->s = cap;
       h->prof_on = false;
-      CUFFT_OK(cufftSetStream(h->plan_f, cap));
-      CUFFT_OK(cufftSetStream(h->plan_b, cap));
+      for (cufftHandle* p : h->plans())
+        if (*p) CUFFT_OK(cufftSetStream(*p, cap));
       CUDA_OK(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
       try {
         vcycle_body(h);
@@ -1440,8 +1528,10 @@ void destroy(mg_handle* h) {
   for (void* p : {(void*)h->d_leafmap, (void*)h->d_lvl_ptrs, (void*)h->d_lvl_cs, (void*)h->d_norm, (void*)h->d_leafbuf,
                   (void*)h->d_leafbuf2, (void*)h->d_dense, h->d_spec, (void*)h->d_mult})
     if (p) cudaFree(p);
-  if (h->plan_f) cufftDestroy(h->plan_f);
-  if (h->plan_b) cufftDestroy(h->plan_b);
+  for (cufftHandle* p : h->plans())
+    if (*p) cufftDestroy(*p);
+  for (void* p : {(void*)h->pr_X, (void*)h->pr_R, (void*)h->pr_mult, h->pr_C1, h->pr_C2, h->pr_C3})
+    if (p) cudaFree(p);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   delete h;
 }

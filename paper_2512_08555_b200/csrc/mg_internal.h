@@ -145,8 +145,13 @@ void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, int nc, cudaStream_t s);
 void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, cudaStream_t s);
 // full multiplier table of a mixed periodic / unbounded coarse solve (R2C layout)
+// layout 0: [kz][ky][kx] (3-D R2C spectrum), 1: [kz][kx][ky] (pruned solve)
 void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
-                       double h2, double scale, cudaStream_t s);
+                       double h2, double scale, int layout, cudaStream_t s);
+// pruned coarse solve (x periodic, y, z unbounded): transposes around the 1-D transforms
+void launch_spec_pad_y(const void* c1, void* c2, int Nz, int Ny, int Hx, int Py, int Pz, int nc, cudaStream_t s);
+void launch_spec_window(const void* c2, void* c3, int Wz, int Wy, int Hx, int Py, int Pz, int ge, int nc,
+                        cudaStream_t s);
 void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s);
 
 }  // namespace mg

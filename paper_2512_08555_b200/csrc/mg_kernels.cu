@@ -1032,7 +1032,7 @@ __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
 
 void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const int* sym, const int* hi_odd,
                           const int* hi_even, const int* off, cudaStream_t s) {
-  CoarseAxes A;
+  CoarseAxes A{};
   for (int a = 0; a < 3; ++a) {
     A.P[a] = P[a];
     A.sym[a] = sym[a];
@@ -1069,11 +1069,9 @@ __global__ void k_coarse_band(C2FList g, double* u, int64_t cs, const double* __
 
 void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P, const int* off, const C2FList& band,
                            cudaStream_t s) {
-  CoarseAxes A;
+  CoarseAxes A{};
   for (int a = 0; a < 3; ++a) {
     A.P[a] = P[a];
-    A.sym[a] = 0;
-    A.hi_odd[a] = 0;
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
@@ -1154,12 +1152,22 @@ void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, 
 // operator restricted to the unbounded axes (`low`, already x h^2 / (Px Py Pz)); all
 // others h^2 / σ_M(k) / (Px Py Pz) (generalised E14, reading Z22).
 __global__ void k_build_mult(double* __restrict__ mult, int Px, int Py, int Pz, int perx, int pery, int perz,
-                             int ua, int ub, const double* __restrict__ low, int order, double h2, double scale) {
+                             int ua, int ub, const double* __restrict__ low, int order, double h2, double scale,
+                             int layout) {
   const int Hx = Px / 2 + 1;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)Hx * Py * Pz;
   if (i >= n) return;
-  const int k[3] = {(int)(i % Hx), (int)((i / Hx) % Py), (int)(i / ((int64_t)Hx * Py))};
+  // layout 0: [kz][ky][kx] (the 3-D R2C spectrum); 1: [kz][kx][ky] (the pruned solve)
+  int k[3];
+  if (layout == 0) {
+    k[0] = (int)(i % Hx);
+    k[1] = (int)((i / Hx) % Py);
+  } else {
+    k[1] = (int)(i % Py);
+    k[0] = (int)((i / Py) % Hx);
+  }
+  k[2] = (int)(i / ((int64_t)Hx * Py));
   const int P[3] = {Px, Py, Pz}, per[3] = {perx, pery, perz};
   bool zero_per = true;
   for (int a = 0; a < 3; ++a)
@@ -1177,10 +1185,52 @@ __global__ void k_build_mult(double* __restrict__ mult, int Px, int Py, int Pz, 
 }
 
 void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
-                       double h2, double scale, cudaStream_t s) {
+                       double h2, double scale, int layout, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
   k_build_mult<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mult, P[0], P[1], P[2], per[0], per[1], per[2], ua, ub,
-                                                             low, order, h2, scale);
+                                                             low, order, h2, scale, layout);
+  ++g_nlaunch;
+}
+
+// Pruned coarse solve (x periodic, y and z unbounded): the y-transform input
+// [c][z < Nz][kx][y < Py] from the x-spectrum [c][z][y < Ny][kx], zero for y >= Ny
+__global__ void k_spec_pad_y(const cuDoubleComplex* __restrict__ c1, cuDoubleComplex* __restrict__ c2, int Nz, int Ny,
+                             int Hx, int Py, int Pz) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // over z < Nz, kx, y < Py
+  const int64_t n = (int64_t)Nz * Hx * Py;
+  if (i >= n) return;
+  const int y = (int)(i % Py), kx = (int)((i / Py) % Hx), z = (int)(i / ((int64_t)Py * Hx));
+  const int c = blockIdx.y;
+  c2 += (int64_t)c * Pz * Hx * Py;
+  c1 += (int64_t)c * Nz * Ny * Hx;
+  c2[((int64_t)z * Hx + kx) * Py + y] = y < Ny ? c1[((int64_t)z * Ny + y) * Hx + kx] : make_cuDoubleComplex(0.0, 0.0);
+}
+
+// the output window (z, y in [-GE, N + GE), periodic images in the padded lattice) of the
+// inverse-transformed [c][z][kx][y] as x-spectra [c][zw][yw][kx] for the final C2R along x
+__global__ void k_spec_window(const cuDoubleComplex* __restrict__ c2, cuDoubleComplex* __restrict__ c3, int Wz, int Wy,
+                              int Hx, int Py, int Pz, int ge) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // over zw, yw, kx
+  const int64_t n = (int64_t)Wz * Wy * Hx;
+  if (i >= n) return;
+  const int kx = (int)(i % Hx), yw = (int)((i / Hx) % Wy), zw = (int)(i / ((int64_t)Hx * Wy));
+  const int c = blockIdx.y;
+  const int z = (zw - ge + Pz) % Pz, y = (yw - ge + Py) % Py;
+  c3[(int64_t)c * Wz * Wy * Hx + i] = c2[(int64_t)c * Pz * Hx * Py + ((int64_t)z * Hx + kx) * Py + y];
+}
+
+void launch_spec_pad_y(const void* c1, void* c2, int Nz, int Ny, int Hx, int Py, int Pz, int nc, cudaStream_t s) {
+  const int64_t n = (int64_t)Nz * Hx * Py;
+  k_spec_pad_y<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((const cuDoubleComplex*)c1, (cuDoubleComplex*)c2, Nz,
+                                                                    Ny, Hx, Py, Pz);
+  ++g_nlaunch;
+}
+
+void launch_spec_window(const void* c2, void* c3, int Wz, int Wy, int Hx, int Py, int Pz, int ge, int nc,
+                        cudaStream_t s) {
+  const int64_t n = (int64_t)Wz * Wy * Hx;
+  k_spec_window<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((const cuDoubleComplex*)c2, (cuDoubleComplex*)c3, Wz,
+                                                                     Wy, Hx, Py, Pz, ge);
   ++g_nlaunch;
 }
 

@@ -36,7 +36,8 @@ class MgDesc(C.Structure):
                 ("coarse_n", C.c_int32), ("smoother", C.c_int32), ("omega", C.c_double),
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
                 ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
-                ("zsplit", C.c_int32), ("fuse", C.c_int32), ("ncomp", C.c_int32), ("staging", C.c_int32)]
+                ("zsplit", C.c_int32), ("fuse", C.c_int32), ("ncomp", C.c_int32), ("coarse_pruning", C.c_int32),
+                ("staging", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -173,6 +174,7 @@ class Solver:
         d.fuse = int(cfg.get("fuse", 0))
         d.staging = int(cfg.get("staging", 0))
         d.ncomp = int(cfg.get("ncomp", 1))
+        d.coarse_pruning = int(cfg.get("coarse_pruning", 0))
         self.nc = max(1, d.ncomp)
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))
