@@ -21,7 +21,10 @@ namespace mg {
 
 namespace {
 
-constexpr int GB_NT = 256;
+#ifndef MG_GB_NT
+#define MG_GB_NT 128
+#endif
+constexpr int GB_NT = MG_GB_NT;  // threads per ghost box (a 16-wide tile of GB_NT/16 rows)
 // coarse extent per axis of a 16-wide box: 7 + I (13 for I = 6, 15 for I = 8)
 template <int I> struct GB {
   static constexpr int MAXC = 7 + I;
@@ -69,22 +72,26 @@ __device__ __forceinline__ double apply_taps(const double* p, int stride, bool o
 }  // namespace
 
 // box record: GBOX_REC int32 (mg_internal.h).
-// Every stage iterates a 3-D index box with the 256 threads laid out as a 16 x 16 tile
+// Every stage iterates a 3-D index box with the GB_NT threads laid out as a 16-wide tile
 // over its two largest axes and a loop over the smallest one (ghost boxes are thin
 // slabs: 2 x 16 x 16 faces, 2 x 2 x 16 edges), so that the index arithmetic is adds
 // and every thread has work.
 template <typename Fn>
 __device__ __forceinline__ void box_for(const int D[3], Fn&& fn) {
-  const int ta = threadIdx.x & 15, tb = threadIdx.x >> 4;
+  constexpr int TB = GB_NT / 16;  // rows of the 16-wide thread tile
+  const int ta = threadIdx.x & 15;
   if (D[0] <= D[1] && D[0] <= D[2]) {         // loop over x
-    if (ta >= D[1] || tb >= D[2]) return;
-    for (int l = 0; l < D[0]; ++l) fn(l, ta, tb);
+    if (ta >= D[1]) return;
+    for (int tb = threadIdx.x >> 4; tb < D[2]; tb += TB)
+      for (int l = 0; l < D[0]; ++l) fn(l, ta, tb);
   } else if (D[1] <= D[2]) {                  // loop over y
-    if (ta >= D[0] || tb >= D[2]) return;
-    for (int l = 0; l < D[1]; ++l) fn(ta, l, tb);
+    if (ta >= D[0]) return;
+    for (int tb = threadIdx.x >> 4; tb < D[2]; tb += TB)
+      for (int l = 0; l < D[1]; ++l) fn(ta, l, tb);
   } else {                                    // loop over z
-    if (ta >= D[0] || tb >= D[1]) return;
-    for (int l = 0; l < D[2]; ++l) fn(ta, tb, l);
+    if (ta >= D[0]) return;
+    for (int tb = threadIdx.x >> 4; tb < D[1]; tb += TB)
+      for (int l = 0; l < D[2]; ++l) fn(ta, tb, l);
   }
 }
 
