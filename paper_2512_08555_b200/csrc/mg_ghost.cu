@@ -22,7 +22,7 @@ namespace mg {
 namespace {
 
 #ifndef MG_GB_NT
-#define MG_GB_NT 128
+#define MG_GB_NT 256
 #endif
 constexpr int GB_NT = MG_GB_NT;  // threads per ghost box (a 16-wide tile of GB_NT/16 rows)
 // coarse extent per axis of a 16-wide box: 7 + I (13 for I = 6, 15 for I = 8)
