@@ -18,6 +18,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="cfg2")
     ap.add_argument("--cycles", type=int, default=5)
+    ap.add_argument("--extra", default="{}", help="extra cfg keys (json), e.g. fuse, pencil_blocks")
     a = ap.parse_args()
     import torch
 
@@ -28,6 +29,7 @@ def main():
     if a.cfg.endswith("_m6"):  # the 6th-order variant
         cfg = dict(cfg, order=6, name=a.cfg)
     dom, leaves, f = C.build(cfg)
+    cfg = dict(cfg, **json.loads(a.extra))
     S = Solver(cfg, leaves)
     S.set_rhs(torch.from_numpy(f).cuda())
     S.vcycle(2)
@@ -43,7 +45,7 @@ def main():
             if cnt[m]:
                 rows.setdefault(st, {})[m] = (round(ms[m] / a.cycles * 1e3, 1), round(cnt[m] / a.cycles, 2))
     info = [S.level_info(m) for m in range(nlev)]
-    print(json.dumps({"cfg": a.cfg, "blocks": [i["nreal"] for i in info], "ghosts": [i["nghost"] for i in info],
+    print(json.dumps({"cfg": a.cfg, "extra": a.extra, "blocks": [i["nreal"] for i in info], "ghosts": [i["nghost"] for i in info],
                       "us_per_cycle[stage][level]=(us, launches)": rows}), flush=True)
     S.use_graph(True)
     ms = S.time_op("vcycle", 0, 10)
