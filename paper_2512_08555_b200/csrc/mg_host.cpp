@@ -1469,13 +1469,14 @@ void leaf_io(mg_handle* h, double* leafbuf, bool to_levels, int field) {
 
 void set_rhs(mg_handle* h, const double* f_dev) {
   const int nlev = (int)h->L.size();
+  // u := 0 (initial solution, Z28), f := 0 (ghost nodes beyond unbounded faces); r is
+  // zeroed after the right-hand-side correction, û is written by every restriction
+  // before a prolongation reads it
   for (auto& l : h->L) {
     const size_t n = (size_t)h->nc * l.ntot() * l.B3;
     CUDA_OK(cudaMemsetAsync(l.f, 0, n * sizeof(double), h->s));
     CUDA_OK(cudaMemsetAsync(l.u[0], 0, n * sizeof(double), h->s));
     CUDA_OK(cudaMemsetAsync(l.u[1], 0, n * sizeof(double), h->s));
-    CUDA_OK(cudaMemsetAsync(l.uhat, 0, n * sizeof(double), h->s));
-    CUDA_OK(cudaMemsetAsync(l.r, 0, n * sizeof(double), h->s));
     l.cur = 0;
   }
   leaf_io(h, const_cast<double*>(f_dev), true, MG_FIELD_F);
@@ -1500,7 +1501,14 @@ void set_rhs(mg_handle* h, const double* f_dev) {
                        h->s);
   for (int m = 0; m < nlev; ++m) {
     Level& l = h->L[m];
-    launch_correct_rhs(view(h, m), h->order, l.r, h->s);
+    if (launch_rhs_pencil(view(h, m), h->order, h->s)) {
+      // r holds f* (leaves) / f (covered) on the real blocks: copy into f, per component
+      const size_t pitch = (size_t)l.ntot() * l.B3 * sizeof(double);
+      CUDA_OK(cudaMemcpy2DAsync(l.f, pitch, l.r, pitch, (size_t)l.nreal * l.B3 * sizeof(double), h->nc,
+                                cudaMemcpyDeviceToDevice, h->s));
+    } else {
+      launch_correct_rhs(view(h, m), h->order, l.r, h->s);
+    }
   }
   for (auto& l : h->L)
     CUDA_OK(cudaMemsetAsync(l.r, 0, (size_t)h->nc * l.ntot() * l.B3 * sizeof(double), h->s));

@@ -94,6 +94,8 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s);
 bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMaps* tm, cudaStream_t s);
 bool launch_norm_pencil(const LevelView& L, int order, unsigned long long* out, cudaStream_t s);
 bool launch_res_pencil(const LevelView& L, int order, cudaStream_t s);
+// f* = R_h^4 f into L.r on the leaf nodes (raw f on covered nodes) (B = 16, M = 4)
+bool launch_rhs_pencil(const LevelView& L, int order, cudaStream_t s);
 // FAS right-hand side f = r + Δu on the covered nodes of a coarse level (B = 16)
 bool launch_fas_pencil(const LevelView& L, int order, cudaStream_t s);
 // fused fine residual + full-weighting restriction + u injection into the coarse level

@@ -705,6 +705,9 @@ struct ResShape {
 // MODE 1: f = r + Δ_h^M u (FAS right-hand side on the coarse level, Alg. 1) on
 //         the nodes of octants covered by the finer level (covmask); others untouched;
 //         and û = u on every node of the pencil (the snapshot of Alg. 1).
+// MODE 3: r = R_h^4 f = f + (1/12) Σ δ² f (the right-hand side of E12; M = 4)
+//         on leaf nodes and r = f on covered nodes, from the plane tiles of f (its ghosts
+//         filled); the caller copies r into f (f* stored once).
 // MODE 2: max |f - Δ_h^M u| over the nodes of uncovered octants (the composite residual
 //         norm of the stopping test) as the bit pattern of a non-negative double
 //         (NaN -> quiet-NaN pattern, above +Inf), atomicMax-ed into *out; nothing written.
@@ -726,6 +729,7 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
   if (MODE != 0 && tid < len) scov[tid] = __ldg(L.covmask + __ldg(pb + tid));
   const int nz = PB * len;
   const double* __restrict__ fin = MODE == 1 ? L.r : L.f;  // the right-hand operand staged per plane
+  const double* __restrict__ tsrc = MODE == 3 ? L.f : L.u;  // the field of the plane tiles
   unsigned long long nmax = 0ull;                            // MODE 2
 
   int ld_xy[2], ld_sxy[2], ld_dst[2];
@@ -757,9 +761,9 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
       const int slot = (z + 1) % R;
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        if (!ld_on[d] || (ld_f[d] && dz != 0)) continue;
+        if (!ld_on[d] || (ld_f[d] && (dz != 0 || MODE == 3))) continue;
         const int blk = snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)];
-        const double* src = (ld_f[d] ? fin : L.u) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
+        const double* src = (ld_f[d] ? fin : tsrc) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
         cpa16(sm + ld_dst[d] + slot * (ld_f[d] ? FP : TP), src);
       }
     }
@@ -786,7 +790,16 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
       a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
       if (ORDER == 6) d0 = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
     }
-    if (s >= 1) {
+    if (MODE == 3 && s >= 1) {
+      // f* at plane r = s-1: δ² along x, y from the tile, along z from the carried centres,
+      // summed as ((δ²x + δ²y) + δ²z) / 12 (the generic kernel's order)
+      const int r = s - 1;
+      const double* U = su + ((r + 1) % R) * TP + ci;
+      const double dx = (U[-1] - 2.0 * c1) + U[1], dy = (U[-T] - 2.0 * c1) + U[T], dz = (c2 - 2.0 * c1) + c0;
+      const size_t o = (size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid;
+      const int oct = (cx >= PB / 2) | ((cy >= PB / 2) << 1) | (((r & 15) >= PB / 2) << 2);
+      L.r[o] = ((scov[r >> 4] >> oct) & 1) ? c1 : c1 + ((dx + dy) + dz) / 12.0;
+    } else if (s >= 1) {
       const int r = s - 1;
       const int sl = (r + 1) % R;
       const double f = sf[sl * FP + tid];
@@ -1119,6 +1132,7 @@ void prepare_pencil_kernels() {
   setup((const void*)k_res_pencil<6, RES_D, 0>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<6, RES_D, 1>, ResShape<RES_D>::SMEM);
   setup((const void*)k_res_pencil<6, RES_D, 2>, ResShape<RES_D>::SMEM);
+  setup((const void*)k_res_pencil<4, RES_D, 3>, ResShape<RES_D>::SMEM);
 }
 
 // residual-type pencil launch (MODE 0 residual, 1 FAS right-hand side, 2 norm)
@@ -1165,6 +1179,14 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
     (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>)
         <<<dim3(grid, L.nc), RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   }
+  note_launch();
+  return true;
+}
+
+bool launch_rhs_pencil(const LevelView& L, int order, cudaStream_t s) {
+  if (order != 4 || L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  k_res_pencil<4, RES_D, 3><<<dim3(L.npen, L.nc), ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, nullptr);
   note_launch();
   return true;
 }
