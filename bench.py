@@ -275,6 +275,8 @@ def run_reference(args, ws, rank, dist):
     name = args.workload
     cores, model = host_cores()
     P = min(cores, MAX_ORACLE_PROCS)
+    if args.ref_sample == "auto":
+        args.ref_sample = "full" if (args.steps + args.warmup) * 13.0 <= 180.0 else "tiny"
     cfg = oracle_sample_cfg(name, args.ref_sample)
     from workloads import configs as C
     C.leaves_for(cfg)
@@ -507,8 +509,9 @@ def main():
     ap.add_argument("--workload", choices=["cfg5", "cfg2"], default="cfg5")
     ap.add_argument("--no-secondary", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-sample", choices=["full", "tiny"], default="full",
-                    help="--impl reference: the oracle sample per step (tiny: for tests)")
+    ap.add_argument("--ref-sample", choices=["auto", "full", "tiny"], default="auto",
+                    help="--impl reference: the oracle sample per step; auto = full (5 levels, ~13 s per step "
+                         "with all cores busy) when the whole run stays under ~3 minutes, else tiny (2 levels)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
