@@ -206,12 +206,17 @@ def test_vcycle_parity(name, cycles):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["puu1", "cfg3_64", "puu1_m6"])
-def test_vcycle_parity_graph_and_determinism(name):
+@pytest.mark.parametrize("name,variant", [("puu1", {}), ("cfg3_64", {}), ("puu1_m6", {}),
+                                          ("puu2", {"pencil_blocks": 2}), ("cfg3_64", {"pencil_blocks": 4}),
+                                          ("cfg5_small", {"pencil_blocks": 2})])
+def test_vcycle_parity_graph_and_determinism(name, variant):
     """CUDA-graph launched V-cycles (the bench configuration) vs the oracle, and bitwise
     determinism of two fresh runs; cfg3_64 exercises the composed exterior-chain
-    injections, puu1_m6 the M = 6 pencil sweep."""
+    injections, puu1_m6 the M = 6 pencil sweep, the forced pencil lengths the
+    production (multi-block pencil, no z-split) variants."""
     cfg, lv, f = _cfg(name)
+    cfg = dict(cfg)
+    cfg.update(variant)
     p = Pair(cfg, lv, f)
     p.g.use_graph(True)
     for _ in range(2):
