@@ -99,7 +99,6 @@ template <int I>
 __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ boxes, LevelView F, LevelView C,
                                                    double* __restrict__ ff, const double* __restrict__ cf,
                                                    bool ext_zero, int t1_off) {
-  pdl_enter();
   extern __shared__ double sm[];
   ff += (int64_t)blockIdx.y * F.cs;  // component blockIdx.y
   cf += (int64_t)blockIdx.y * C.cs;
@@ -213,11 +212,11 @@ void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_
   if (nbox <= 0) return;
   const size_t smem = sizeof(double) * (size_t)(szA + szB);
   if (I == 4)
-    pdl_launch(k_c2f_box<4>, dim3(nbox, fine.nc), GB_NT, smem, s, boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<4><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else if (I == 6)
-    pdl_launch(k_c2f_box<6>, dim3(nbox, fine.nc), GB_NT, smem, s, boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<6><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   else
-    pdl_launch(k_c2f_box<8>, dim3(nbox, fine.nc), GB_NT, smem, s, boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
+    k_c2f_box<8><<<dim3(nbox, fine.nc), GB_NT, smem, s>>>(boxes, fine, coarse, fine_field, coarse_field, ext_zero, szA);
   note_launch();
 }
 

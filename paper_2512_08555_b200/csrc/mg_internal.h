@@ -2,7 +2,6 @@
 // (mg_host.cpp) and the sm_100a kernels (mg_kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
-#include <utility>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -60,32 +59,6 @@ struct TileMaps {
 bool encode_tile_maps(const double* base, int ntot, CUtensorMap out[4]);
 
 #ifdef __CUDACC__
-// Programmatic dependent launch (sm_90+): every kernel of the library lets the next one
-// launch as soon as all its CTAs have started, and waits for its predecessor to complete
-// (memory visible) before it reads anything, so kernel boundaries in a V-cycle graph
-// overlap the next kernel's launch with the previous one's tail.  Without the launch
-// attribute both instructions are no-ops.
-__device__ __forceinline__ void pdl_enter() {
-  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-  asm volatile("griddepcontrol.wait;\n" ::: "memory");
-}
-
-// kernel launch with the programmatic-stream-serialisation attribute (see pdl_enter)
-template <typename... KArgs, typename... Args>
-inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
-}
-
 // the field pointers of component blockIdx.y (batched launches: gridDim.y = nc)
 __device__ __forceinline__ void comp_view(LevelView& L) {
   const int64_t o = (int64_t)blockIdx.y * L.cs;

@@ -81,7 +81,6 @@ __device__ __forceinline__ double lap_fetch(const double* __restrict__ u, const 
 // ---------------------------------------------------------------------------------
 template <int B, int ORDER, int MODE, bool RES, int NT>
 __global__ void __launch_bounds__(NT) k_smooth(LevelView L, double omega, double inv_h2, double inv_d) {
-  pdl_enter();
   comp_view(L);
   constexpr int NS = MODE == SM_RB ? 2 : (MODE == SM_JACOBI ? 1 : 0);
   constexpr int H = NS + (RES ? 1 : 0);
@@ -294,7 +293,6 @@ static const uint32_t* smooth_table() {
 template <int B, int ORDER, int MODE, bool RES, int NT>
 __global__ void __launch_bounds__(NT, (MODE == SM_RB && RES) ? 2 : (MODE < 0 ? 4 : 3))
     k_smooth2(LevelView L, const uint32_t* __restrict__ tab, double omega, double inv_h2, double inv_d) {
-  pdl_enter();
   comp_view(L);
   using SH = SmoothShape<B, MODE, RES>;
   constexpr int NS = SH::NS, T = SH::T, B3 = SH::B3;
@@ -412,7 +410,7 @@ static void smooth_inst(const LevelView& L, double omega, double inv_h2, double 
       return;
     }
     const uint32_t* tab = smooth_table<B, MODE, RES>();
-    if (L.nreal > 0) { pdl_launch(k, dim3(L.nreal, L.nc), NT, smem, s, L, tab, omega, inv_h2, inv_d); ++g_nlaunch; }
+    if (L.nreal > 0) { k<<<dim3(L.nreal, L.nc), NT, smem, s>>>(L, tab, omega, inv_h2, inv_d); ++g_nlaunch; }
     return;
   }
   smooth_inst_v1<B, ORDER, MODE, RES>(L, omega, inv_h2, inv_d, s, prepare_only);
@@ -431,7 +429,7 @@ static void smooth_inst_v1(const LevelView& L, double omega, double inv_h2, doub
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return;
   }
-  if (L.nreal > 0) { pdl_launch(k, dim3(L.nreal, L.nc), NT, smem, s, L, omega, inv_h2, inv_d); ++g_nlaunch; }
+  if (L.nreal > 0) { k<<<dim3(L.nreal, L.nc), NT, smem, s>>>(L, omega, inv_h2, inv_d); ++g_nlaunch; }
 }
 
 template <int B, int ORDER>
@@ -493,7 +491,6 @@ void launch_residual(const LevelView& L, int order, cudaStream_t s) {
 
 __global__ void k_copy_list(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                             double* __restrict__ d, const double* __restrict__ sv, int64_t csd, int64_t css) {
-  pdl_enter();
   d += (int64_t)blockIdx.y * csd;
   sv += (int64_t)blockIdx.y * css;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -507,7 +504,6 @@ struct ChainFields {
 
 __global__ void k_copy_chain(int n, const int32_t* __restrict__ lev, const int32_t* __restrict__ dst,
                              const int32_t* __restrict__ src, ChainFields F) {
-  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const int l = lev[i];
@@ -525,14 +521,14 @@ void launch_inject_chain(int n, const int32_t* lev, const int32_t* dst, const in
     F.f[j] = fields[j];
     F.cs[j] = cs[j];
   }
-  pdl_launch(k_copy_chain, dim3((n + 255) / 256, nc), 256, 0, s, n, lev, dst, src, F);
+  k_copy_chain<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, lev, dst, src, F);
   ++g_nlaunch;
 }
 
 void launch_inject_list(const InjList& l, double* coarse_field, const double* fine_field, int nc, int64_t cs_coarse,
                         int64_t cs_fine, cudaStream_t s) {
   if (l.n == 0) return;
-  pdl_launch(k_copy_list, dim3((l.n + 255) / 256, nc), 256, 0, s, l.n, l.dst, l.src, coarse_field, fine_field, cs_coarse, cs_fine);
+  k_copy_list<<<dim3((l.n + 255) / 256, nc), 256, 0, s>>>(l.n, l.dst, l.src, coarse_field, fine_field, cs_coarse, cs_fine);
   ++g_nlaunch;
 }
 
@@ -542,7 +538,6 @@ void launch_inject_list(const InjList& l, double* coarse_field, const double* fi
 // is never written and stays 0 (reading Z14).
 // ---------------------------------------------------------------------------------
 __global__ void k_restrict(LevelView F, LevelView C) {
-  pdl_enter();
   comp_view(F);
   comp_view(C);
   const int b = blockIdx.x;
@@ -572,7 +567,6 @@ __global__ void k_restrict(LevelView F, LevelView C) {
 // memory by cp.async; FW evaluated with the same nesting/rounding as k_restrict.
 template <int B>
 __global__ void __launch_bounds__(256) k_restrict2(LevelView F, LevelView C) {
-  pdl_enter();
   comp_view(F);
   comp_view(C);
   constexpr int T = B + 2, Bh = B / 2, B3 = B * B * B;
@@ -626,14 +620,13 @@ __global__ void __launch_bounds__(256) k_restrict2(LevelView F, LevelView C) {
 
 void launch_restrict(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (fine.B == 16) { pdl_launch(k_restrict2<16>, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
-  else { pdl_launch(k_restrict, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
+  if (fine.B == 16) { k_restrict2<16><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_restrict<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // FAS right-hand side on the covered coarse nodes (Alg. 1): f = r + Δ u.
 template <int ORDER>
 __global__ void k_fas_rhs(LevelView F, LevelView C) {
-  pdl_enter();
   comp_view(F);
   comp_view(C);
   const int b = blockIdx.x;
@@ -650,14 +643,13 @@ __global__ void k_fas_rhs(LevelView F, LevelView C) {
 
 void launch_fas_rhs(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (order == 2) { pdl_launch(k_fas_rhs<2>, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
-  else if (order == 4) { pdl_launch(k_fas_rhs<4>, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
-  else { pdl_launch(k_fas_rhs<6>, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
+  if (order == 2) { k_fas_rhs<2><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else if (order == 4) { k_fas_rhs<4><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_fas_rhs<6><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 // Prolongation of the correction (Alg. 1): u_f += trilinear(u_c - û_c).
 __global__ void k_prolong(LevelView F, LevelView C) {
-  pdl_enter();
   comp_view(F);
   comp_view(C);
   const int b = blockIdx.x;
@@ -694,7 +686,6 @@ __global__ void k_prolong(LevelView F, LevelView C) {
 // block staged once in shared memory; same nesting/rounding as k_prolong.
 template <int B>
 __global__ void __launch_bounds__(256, 5) k_prolong2(LevelView F, LevelView C) {
-  pdl_enter();
   comp_view(F);
   comp_view(C);
   constexpr int E = B / 2 + 1, B3 = B * B * B;
@@ -742,12 +733,11 @@ __global__ void __launch_bounds__(256, 5) k_prolong2(LevelView F, LevelView C) {
 
 void launch_prolong(const LevelView& fine, const LevelView& coarse, cudaStream_t s) {
   if (!fine.nreal) return;
-  if (fine.B == 16) { pdl_launch(k_prolong2<16>, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
-  else { pdl_launch(k_prolong, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse); ++g_nlaunch; }
+  if (fine.B == 16) { k_prolong2<16><<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
+  else { k_prolong<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse); ++g_nlaunch; }
 }
 
 __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
-  pdl_enter();
   comp_view(F);
   cu += (int64_t)blockIdx.y * C.cs;
   const int b = blockIdx.x;
@@ -761,7 +751,7 @@ __global__ void k_inject_up(LevelView F, LevelView C, double* cu) {
 }
 
 void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* coarse_u, cudaStream_t s) {
-  if (fine.nreal) { pdl_launch(k_inject_up, dim3(fine.nreal, fine.nc), 256, 0, s, fine, coarse, coarse_u); ++g_nlaunch; }
+  if (fine.nreal) { k_inject_up<<<dim3(fine.nreal, fine.nc), 256, 0, s>>>(fine, coarse, coarse_u); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -771,7 +761,6 @@ void launch_inject_up(const LevelView& fine, const LevelView& coarse, double* co
 // ---------------------------------------------------------------------------------
 template <int ORDER>
 __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
-  pdl_enter();
   comp_view(L);
   const int b = blockIdx.x;
   const int B = L.B, Bh = B / 2;
@@ -806,16 +795,15 @@ __global__ void k_norm(LevelView L, bool residual, unsigned long long* out) {
 
 void launch_norm(const LevelView& L, int order, bool residual, unsigned long long* out, cudaStream_t s) {
   if (!L.nreal) return;
-  if (order == 2) { pdl_launch(k_norm<2>, dim3(L.nreal, L.nc), 256, 0, s, L, residual, out); ++g_nlaunch; }
-  else if (order == 4) { pdl_launch(k_norm<4>, dim3(L.nreal, L.nc), 256, 0, s, L, residual, out); ++g_nlaunch; }
-  else { pdl_launch(k_norm<6>, dim3(L.nreal, L.nc), 256, 0, s, L, residual, out); ++g_nlaunch; }
+  if (order == 2) { k_norm<2><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else if (order == 4) { k_norm<4><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
+  else { k_norm<6><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, residual, out); ++g_nlaunch; }
 }
 
 // R_h^M f on all real nodes into tmp (M=4: f + (1/12)Σδ²f, right side of E12), then
 // f <- tmp on leaf nodes only (reading Z16).
 template <int ORDER>
 __global__ void k_rhs_apply(LevelView L, double* tmp) {
-  pdl_enter();
   comp_view(L);
   tmp += (int64_t)blockIdx.y * L.cs;
   const int b = blockIdx.x;
@@ -847,7 +835,6 @@ __global__ void k_rhs_apply(LevelView L, double* tmp) {
 }
 
 __global__ void k_rhs_commit(LevelView L, const double* tmp) {
-  pdl_enter();
   comp_view(L);
   tmp += (int64_t)blockIdx.y * L.cs;
   const int b = blockIdx.x;
@@ -862,15 +849,14 @@ __global__ void k_rhs_commit(LevelView L, const double* tmp) {
 
 void launch_correct_rhs(const LevelView& L, int order, double* tmp, cudaStream_t s) {
   if (!L.nreal || order == 2) return;
-  if (order == 4) { pdl_launch(k_rhs_apply<4>, dim3(L.nreal, L.nc), 256, 0, s, L, tmp); ++g_nlaunch; }
-  else { pdl_launch(k_rhs_apply<6>, dim3(L.nreal, L.nc), 256, 0, s, L, tmp); ++g_nlaunch; }
-  { pdl_launch(k_rhs_commit, dim3(L.nreal, L.nc), 256, 0, s, L, tmp); ++g_nlaunch; }
+  if (order == 4) { k_rhs_apply<4><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  else { k_rhs_apply<6><<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
+  { k_rhs_commit<<<dim3(L.nreal, L.nc), 256, 0, s>>>(L, tmp); ++g_nlaunch; }
 }
 
 // leaf-ordered [n_leaf][B^3] <-> level block storage
 __global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const double* __restrict__ src,
                                double* const* __restrict__ dst, const int64_t* __restrict__ lev_cs, bool to_levels) {
-  pdl_enter();
   const int n = blockIdx.x, c = blockIdx.y;
   const int64_t m = map[n];
   const int lev = (int)(m >> 32), blk = (int)(m & 0xffffffff);
@@ -886,7 +872,7 @@ __global__ void k_leaf_scatter(int B3, const int64_t* __restrict__ map, const do
 
 void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* src, double* const* dst_by_level,
                          const int64_t* lev_cs, int nc, bool to_levels, cudaStream_t s) {
-  if (nleaf) { pdl_launch(k_leaf_scatter, dim3(nleaf, nc), 256, 0, s, B3, map, src, dst_by_level, lev_cs, to_levels); ++g_nlaunch; }
+  if (nleaf) { k_leaf_scatter<<<dim3(nleaf, nc), 256, 0, s>>>(B3, map, src, dst_by_level, lev_cs, to_levels); ++g_nlaunch; }
 }
 
 // Field transfer onto an adapted grid (reading A3): one CTA per destination block.
@@ -896,7 +882,6 @@ void launch_leaf_scatter(int nleaf, int B3, const int64_t* map, const double* sr
 // ghost block, refreshed), per axis even -> copy, odd -> mean (the oracle's order).
 __global__ void k_transfer(const int32_t* __restrict__ rec, double* __restrict__ dst, int64_t dcs,
                            const double* __restrict__ src, int64_t scs, const int32_t* __restrict__ snbr, int B) {
-  pdl_enter();
   const int32_t* r = rec + 5 * blockIdx.x;
   const int B3 = B * B * B, Bh = B / 2, E = Bh + 1;
   dst += (int64_t)blockIdx.y * dcs + (size_t)r[0] * B3;
@@ -935,7 +920,7 @@ void launch_transfer(int n, const int32_t* rec, double* dst, int64_t dcs, const 
                      const int32_t* snbr, int B, int nc, cudaStream_t s) {
   if (n <= 0) return;
   const int E = B / 2 + 1;
-  pdl_launch(k_transfer, dim3(n, nc), 256, sizeof(double) * E * E * E, s, rec, dst, dcs, src, scs, snbr, B);
+  k_transfer<<<dim3(n, nc), 256, sizeof(double) * E * E * E, s>>>(rec, dst, dcs, src, scs, snbr, B);
   ++g_nlaunch;
 }
 
@@ -945,7 +930,6 @@ void launch_transfer(int n, const int32_t* rec, double* dst, int64_t dcs, const 
 __global__ void k_leaf_cauchy(int B3, const int64_t* __restrict__ map, double* __restrict__ prev,
                               double* const* __restrict__ lev_u, const int64_t* __restrict__ lev_cs,
                               unsigned long long* out) {
-  pdl_enter();
   const int n = blockIdx.x, c = blockIdx.y;
   const int64_t m = map[n];
   const int lev = (int)(m >> 32);
@@ -983,7 +967,7 @@ __global__ void k_leaf_cauchy(int B3, const int64_t* __restrict__ map, double* _
 
 void launch_leaf_cauchy(int nleaf, int B3, const int64_t* map, double* prev, double* const* lev_u,
                         const int64_t* lev_cs, int nc, unsigned long long* out, cudaStream_t s) {
-  if (nleaf) { pdl_launch(k_leaf_cauchy, dim3(nleaf, nc), 256, 0, s, B3, map, prev, lev_u, lev_cs, out); ++g_nlaunch; }
+  if (nleaf) { k_leaf_cauchy<<<dim3(nleaf, nc), 256, 0, s>>>(B3, map, prev, lev_u, lev_cs, out); ++g_nlaunch; }
 }
 
 // ---------------------------------------------------------------------------------
@@ -998,7 +982,6 @@ struct CoarseAxes {
 };
 
 __global__ void k_coarse_gather(LevelView L, double* dense, CoarseAxes A) {
-  pdl_enter();
   comp_view(L);
   dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1058,11 +1041,10 @@ void launch_coarse_gather(const LevelView& L, double* dense, const int* P, const
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)P[0] * P[1] * P[2];
-  { pdl_launch(k_coarse_gather, dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s, L, dense, A); ++g_nlaunch; }
+  { k_coarse_gather<<<dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
 }
 
 __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ dense, CoarseAxes A) {
-  pdl_enter();
   comp_view(L);
   dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1076,7 +1058,6 @@ __global__ void k_coarse_scatter_nodes(LevelView L, const double* __restrict__ d
 }
 
 __global__ void k_coarse_band(C2FList g, double* u, int64_t cs, const double* __restrict__ dense, CoarseAxes A) {
-  pdl_enter();
   u += (int64_t)blockIdx.y * cs;
   dense += (int64_t)blockIdx.y * A.P[0] * A.P[1] * A.P[2];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1094,12 +1075,11 @@ void launch_coarse_scatter(const LevelView& L, const double* dense, const int* P
     A.off[a] = off[a];
   }
   const int64_t n = (int64_t)L.N[0] * L.N[1] * L.N[2];
-  { pdl_launch(k_coarse_scatter_nodes, dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s, L, dense, A); ++g_nlaunch; }
-  if (band.n) { pdl_launch(k_coarse_band, dim3((band.n + 127) / 128, L.nc), 128, 0, s, band, L.u, L.cs, dense, A); ++g_nlaunch; }
+  { k_coarse_scatter_nodes<<<dim3((unsigned)((n + 255) / 256), L.nc), 256, 0, s>>>(L, dense, A); ++g_nlaunch; }
+  if (band.n) { k_coarse_band<<<dim3((band.n + 127) / 128, L.nc), 128, 0, s>>>(band, L.u, L.cs, dense, A); ++g_nlaunch; }
 }
 
 __global__ void k_fill_list(int n, const int32_t* __restrict__ idx, double* d, double v, int64_t cs) {
-  pdl_enter();
   d += (int64_t)blockIdx.y * cs;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) d[idx[i]] = v;
@@ -1107,13 +1087,12 @@ __global__ void k_fill_list(int n, const int32_t* __restrict__ idx, double* d, d
 
 void launch_fill_list(int n, const int32_t* idx, double* d, double v, int nc, int64_t cs, cudaStream_t s) {
   if (n <= 0) return;
-  pdl_launch(k_fill_list, dim3((n + 255) / 256, nc), 256, 0, s, n, idx, d, v, cs);
+  k_fill_list<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, idx, d, v, cs);
   ++g_nlaunch;
 }
 
 __global__ void k_copy_signed(int n, const int32_t* __restrict__ dst, const int32_t* __restrict__ src,
                               const int8_t* __restrict__ sgn, double* d, const double* sv, int64_t cs) {
-  pdl_enter();
   d += (int64_t)blockIdx.y * cs;
   sv += (int64_t)blockIdx.y * cs;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1123,7 +1102,7 @@ __global__ void k_copy_signed(int n, const int32_t* __restrict__ dst, const int3
 void launch_copy_signed(int n, const int32_t* dst, const int32_t* src, const int8_t* sgn, double* d, const double* sv,
                         int nc, int64_t cs, cudaStream_t s) {
   if (n <= 0) return;
-  pdl_launch(k_copy_signed, dim3((n + 255) / 256, nc), 256, 0, s, n, dst, src, sgn, d, sv, cs);
+  k_copy_signed<<<dim3((n + 255) / 256, nc), 256, 0, s>>>(n, dst, src, sgn, d, sv, cs);
   ++g_nlaunch;
 }
 
@@ -1137,7 +1116,6 @@ __device__ __forceinline__ double symbol_h2(int order, double sx, double sy, dou
 
 // periodic: û /= σ, zero mode -> 0; includes the 1/(PxPyPz) inverse scale
 __global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, int order, double h2) {
-  pdl_enter();
   const int Hx = Px / 2 + 1;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)Hx * Py * Pz;
@@ -1154,11 +1132,10 @@ __global__ void k_mul_periodic(cuDoubleComplex* spec, int Px, int Py, int Pz, in
 
 void launch_coarse_mul_periodic(void* spec, const int* P, int order, double h, int nc, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  { pdl_launch(k_mul_periodic, dim3((unsigned)((n + 255) / 256), nc), 256, 0, s, (cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h); ++g_nlaunch; }
+  { k_mul_periodic<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((cuDoubleComplex*)spec, P[0], P[1], P[2], order, h * h); ++g_nlaunch; }
 }
 
 __global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mult, int64_t n) {
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   spec += (int64_t)blockIdx.y * n;
@@ -1167,7 +1144,7 @@ __global__ void k_mul_table(cuDoubleComplex* spec, const double* __restrict__ mu
 }
 
 void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, cudaStream_t s) {
-  { pdl_launch(k_mul_table, dim3((unsigned)((n + 255) / 256), nc), 256, 0, s, (cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
+  { k_mul_table<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((cuDoubleComplex*)spec, mult, n); ++g_nlaunch; }
 }
 
 // Multiplier of a mixed periodic / unbounded coarse solve on the R2C spectrum (x halved):
@@ -1177,7 +1154,6 @@ void launch_coarse_mul_table(void* spec, const double* mult, int64_t n, int nc, 
 __global__ void k_build_mult(double* __restrict__ mult, int Px, int Py, int Pz, int perx, int pery, int perz,
                              int ua, int ub, const double* __restrict__ low, int order, double h2, double scale,
                              int layout) {
-  pdl_enter();
   const int Hx = Px / 2 + 1;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)Hx * Py * Pz;
@@ -1211,7 +1187,7 @@ __global__ void k_build_mult(double* __restrict__ mult, int Px, int Py, int Pz, 
 void launch_build_mult(double* mult, const int* P, const int* per, int ua, int ub, const double* low, int order,
                        double h2, double scale, int layout, cudaStream_t s) {
   const int64_t n = (int64_t)(P[0] / 2 + 1) * P[1] * P[2];
-  pdl_launch(k_build_mult, (unsigned)((n + 255) / 256), 256, 0, s, mult, P[0], P[1], P[2], per[0], per[1], per[2], ua, ub,
+  k_build_mult<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(mult, P[0], P[1], P[2], per[0], per[1], per[2], ua, ub,
                                                              low, order, h2, scale, layout);
   ++g_nlaunch;
 }
@@ -1220,7 +1196,6 @@ void launch_build_mult(double* mult, const int* P, const int* per, int ua, int u
 // [c][z < Nz][kx][y < Py] from the x-spectrum [c][z][y < Ny][kx], zero for y >= Ny
 __global__ void k_spec_pad_y(const cuDoubleComplex* __restrict__ c1, cuDoubleComplex* __restrict__ c2, int Nz, int Ny,
                              int Hx, int Py, int Pz) {
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // over z < Nz, kx, y < Py
   const int64_t n = (int64_t)Nz * Hx * Py;
   if (i >= n) return;
@@ -1235,7 +1210,6 @@ __global__ void k_spec_pad_y(const cuDoubleComplex* __restrict__ c1, cuDoubleCom
 // inverse-transformed [c][z][kx][y] as x-spectra [c][zw][yw][kx] for the final C2R along x
 __global__ void k_spec_window(const cuDoubleComplex* __restrict__ c2, cuDoubleComplex* __restrict__ c3, int Wz, int Wy,
                               int Hx, int Py, int Pz, int ge) {
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // over zw, yw, kx
   const int64_t n = (int64_t)Wz * Wy * Hx;
   if (i >= n) return;
@@ -1247,7 +1221,7 @@ __global__ void k_spec_window(const cuDoubleComplex* __restrict__ c2, cuDoubleCo
 
 void launch_spec_pad_y(const void* c1, void* c2, int Nz, int Ny, int Hx, int Py, int Pz, int nc, cudaStream_t s) {
   const int64_t n = (int64_t)Nz * Hx * Py;
-  pdl_launch(k_spec_pad_y, dim3((unsigned)((n + 255) / 256), nc), 256, 0, s, (const cuDoubleComplex*)c1, (cuDoubleComplex*)c2, Nz,
+  k_spec_pad_y<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((const cuDoubleComplex*)c1, (cuDoubleComplex*)c2, Nz,
                                                                     Ny, Hx, Py, Pz);
   ++g_nlaunch;
 }
@@ -1255,19 +1229,18 @@ void launch_spec_pad_y(const void* c1, void* c2, int Nz, int Ny, int Hx, int Py,
 void launch_spec_window(const void* c2, void* c3, int Wz, int Wy, int Hx, int Py, int Pz, int ge, int nc,
                         cudaStream_t s) {
   const int64_t n = (int64_t)Wz * Wy * Hx;
-  pdl_launch(k_spec_window, dim3((unsigned)((n + 255) / 256), nc), 256, 0, s, (const cuDoubleComplex*)c2, (cuDoubleComplex*)c3, Wz,
+  k_spec_window<<<dim3((unsigned)((n + 255) / 256), nc), 256, 0, s>>>((const cuDoubleComplex*)c2, (cuDoubleComplex*)c3, Wz,
                                                                      Wy, Hx, Py, Pz, ge);
   ++g_nlaunch;
 }
 
 __global__ void k_real_part_scale(const cuDoubleComplex* c, double* out, int64_t n, double a) {
-  pdl_enter();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = cuCreal(c[i]) * a;
 }
 
 void launch_real_part_scale(const void* cplx, double* out, int64_t n, double a, cudaStream_t s) {
-  if (n) { pdl_launch(k_real_part_scale, (unsigned)((n + 255) / 256), 256, 0, s, (const cuDoubleComplex*)cplx, out, n, a); ++g_nlaunch; }
+  if (n) { k_real_part_scale<<<(unsigned)((n + 255) / 256), 256, 0, s>>>((const cuDoubleComplex*)cplx, out, n, a); ++g_nlaunch; }
 }
 
 }  // namespace mg

@@ -377,7 +377,6 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
 template <int ORDER, int D, int RR, int NREG, bool SW, bool TMA>
 __global__ void __maxnreg__(NREG)
     k_rb_pencil(LevelView L, double omega, double inv_h2, double inv_d, const __grid_constant__ TileMaps tm) {
-  pdl_enter();
   using S = RBShape<D, RR, TMA>;
   comp_view(L);
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
@@ -634,7 +633,6 @@ __device__ __forceinline__ void rb6_body(const LevelView& L, const RBCtx& cx, in
 
 template <int NREG, bool SW>
 __global__ void __maxnreg__(NREG) k_rb6_pencil(LevelView L, double omega, double inv_h2, double inv_d) {
-  pdl_enter();
   using S = RB6Shape;
   comp_view(L);
   constexpr int T = S::T, TW = S::TW, TP = S::TP, R = S::R, NT = S::NT, NPAIR = S::NPAIR, NLD = S::NLD;
@@ -716,7 +714,6 @@ struct ResShape {
 template <int ORDER, int D, int MODE = 0>
 __global__ void __launch_bounds__(ResShape<D>::NT, 4)
     k_res_pencil(LevelView L, double inv_h2, unsigned long long* out = nullptr) {
-  pdl_enter();
   using S = ResShape<D>;
   comp_view(L);
   constexpr int T = S::T, TP = S::TP, FP = S::FP, R = S::R, NT = S::NT;
@@ -885,7 +882,6 @@ struct RR2Shape {
 template <int ORDER>
 __global__ void __maxnreg__(80)
     k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
-  pdl_enter();
   using S = RR2Shape;
   comp_view(L);
   comp_view(C);
@@ -1065,9 +1061,9 @@ __global__ void __maxnreg__(80)
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {
   if (fine.B != PB || fine.npen <= 0 || fine.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (fine.h * fine.h);
-  if (order == 2) pdl_launch(k_rr2_pencil<2>, dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s, fine, coarse, inv_h2);
-  else if (order == 4) pdl_launch(k_rr2_pencil<4>, dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s, fine, coarse, inv_h2);
-  else pdl_launch(k_rr2_pencil<6>, dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s, fine, coarse, inv_h2);
+  if (order == 2) k_rr2_pencil<2><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else if (order == 4) k_rr2_pencil<4><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
+  else k_rr2_pencil<6><<<dim3(fine.npen, fine.nc), RR2Shape::NT, RR2Shape::SMEM, s>>>(fine, coarse, inv_h2);
   note_launch();
   return true;
 }
@@ -1146,9 +1142,9 @@ static bool res_pencil_launch(const LevelView& L, int order, unsigned long long*
   const double inv_h2 = 1.0 / (L.h * L.h);
   constexpr int NT = ResShape<RES_D>::NT;
   constexpr size_t SM = ResShape<RES_D>::SMEM;
-  if (order == 2) pdl_launch(k_res_pencil<2, RES_D, MODE>, dim3(L.npen, L.nc), NT, SM, s, L, inv_h2, out);
-  else if (order == 4) pdl_launch(k_res_pencil<4, RES_D, MODE>, dim3(L.npen, L.nc), NT, SM, s, L, inv_h2, out);
-  else pdl_launch(k_res_pencil<6, RES_D, MODE>, dim3(L.npen, L.nc), NT, SM, s, L, inv_h2, out);
+  if (order == 2) k_res_pencil<2, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
+  else if (order == 4) k_res_pencil<4, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
+  else k_res_pencil<6, RES_D, MODE><<<dim3(L.npen, L.nc), NT, SM, s>>>(L, inv_h2, out);
   note_launch();
   return true;
 }
@@ -1158,8 +1154,8 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
   if (order == 6) {
     const double inv_h2 = 1.0 / (L.h * L.h);
     const double inv_d = 1.0 / ((-128.0 / 30.0) * inv_h2);
-    if (L.sw_npen > 0) pdl_launch(k_rb6_pencil<RB6_NREG, true>, dim3(L.sw_npen, L.nc), 192, RB6Shape::SMEM, s, L, omega, inv_h2, inv_d);
-    else pdl_launch(k_rb6_pencil<RB6_NREG, false>, dim3(L.npen, L.nc), 192, RB6Shape::SMEM, s, L, omega, inv_h2, inv_d);
+    if (L.sw_npen > 0) k_rb6_pencil<RB6_NREG, true><<<dim3(L.sw_npen, L.nc), 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
+    else k_rb6_pencil<RB6_NREG, false><<<dim3(L.npen, L.nc), 192, RB6Shape::SMEM, s>>>(L, omega, inv_h2, inv_d);
     note_launch();
     return true;
   }
@@ -1171,13 +1167,17 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
   const TileMaps& m = tm ? *tm : none;
   if (tm) {
     if (L.sw_npen > 0)
-      pdl_launch((order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, true>), dim3(grid, L.nc), RBT::NT, RBT::SMEM, s, L, omega, inv_h2, inv_d, m);
+      (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, true>)
+          <<<dim3(grid, L.nc), RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
     else
-      pdl_launch((order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, true>), dim3(grid, L.nc), RBT::NT, RBT::SMEM, s, L, omega, inv_h2, inv_d, m);
+      (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, true> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, true>)
+          <<<dim3(grid, L.nc), RBT::NT, RBT::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   } else if (L.sw_npen > 0) {
-    pdl_launch((order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, false>), dim3(grid, L.nc), RBS::NT, RBS::SMEM, s, L, omega, inv_h2, inv_d, m);
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, true, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, true, false>)
+        <<<dim3(grid, L.nc), RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   } else {
-    pdl_launch((order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>), dim3(grid, L.nc), RBS::NT, RBS::SMEM, s, L, omega, inv_h2, inv_d, m);
+    (order == 2 ? k_rb_pencil<2, RB_D, RB_R, RB_NREG, false, false> : k_rb_pencil<4, RB_D, RB_R, RB_NREG, false, false>)
+        <<<dim3(grid, L.nc), RBS::NT, RBS::SMEM, s>>>(L, omega, inv_h2, inv_d, m);
   }
   note_launch();
   return true;
@@ -1186,7 +1186,7 @@ bool launch_rb_pencil(const LevelView& L, int order, double omega, const TileMap
 bool launch_rhs_pencil(const LevelView& L, int order, cudaStream_t s) {
   if (order != 4 || L.B != PB || L.npen <= 0 || L.pen_lmax > PMAXL) return false;
   const double inv_h2 = 1.0 / (L.h * L.h);
-  pdl_launch(k_res_pencil<4, RES_D, 3>, dim3(L.npen, L.nc), ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s, L, inv_h2, nullptr);
+  k_res_pencil<4, RES_D, 3><<<dim3(L.npen, L.nc), ResShape<RES_D>::NT, ResShape<RES_D>::SMEM, s>>>(L, inv_h2, nullptr);
   note_launch();
   return true;
 }
