@@ -813,7 +813,7 @@ void build_ghost_boxes(mg_handle* h) {
             emit(lo, hi);
           }
     }
-    if (sizeof(double) * (size_t)(l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
+    if (sizeof(double) * (size_t)(2 * l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
       throw MgError(MG_ERR_LAYOUT_GHOST, "ghost box exceeds the c2f kernel's shared memory");
   }
 }
