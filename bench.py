@@ -36,8 +36,12 @@ sys.path.insert(0, ROOT)
 METRIC = "V-cycle unknowns/s and smoother+residual HBM GB/s (% of B200 peak), fp64"
 UNIT = "unknowns/s"
 NORTH_STAR_PEAK_GBS = 8000.0
-# algorithmic bytes per unknown of the level a stage runs on
-BYTES_PER_UNKNOWN = {"smooth": 24, "smooth_res": 32, "residual": 24, "prolong": 18, "restrict": 18}
+# algorithmic bytes per unknown of the level the stage is booked on (DESIGN.md
+# §6): sweep (read u, f; write
+# u'), residual (read u, f; write r), prolongation (read u, coarse ε; write u), fused
+# residual + restriction (read u, f; write coarse u, coarse r: 16 + 2), FAS right-hand side
+# on the coarse level (read u, r; write û; f on covered nodes only, not counted)
+BYTES_PER_UNKNOWN = {"smooth": 24, "smooth_res": 32, "residual": 24, "prolong": 18, "restrict": 18, "fas": 24}
 
 
 def peak_hbm():

@@ -117,6 +117,12 @@ typedef struct mg_desc {
                                 fastest measured), 1 TMA tensor copies (cp.async.bulk.tensor, 9
                                 boxes per field and plane) into an mbarrier ring; measured 2.5x
                                 slower on B200; same values bit for bit */
+  int32_t ghost_kernel;      /* c2f ghost boxes: 0 auto (on levels with >= 2048 boxes <= 2 nodes
+                                thick along some axis, i.e. the layers of the distance-1 halo,
+                                and no exterior chain: those boxes one warp each with the thin
+                                axis interpolated first; every other box one CTA each, x, y, z
+                                passes), 1 every box on the CTA kernel, 2 every thin box on the
+                                warp kernel; else MG_ERR_ARG */
 } mg_desc;
 
 /* Validate the layout (nesting, 2:1, unbounded-face rule), build the level
@@ -192,7 +198,7 @@ int mg_time_op(mg_handle* h, int op, int level, int reps, double* ms_out);
  * and starts; mg_profile_read fills ms[stage*nlev + level] and counts[...] for the
  * stages MG_ST_* below (nlev = mg_num_levels).  Synchronises the stream. */
 enum { MG_ST_SMOOTH = 0, MG_ST_SMOOTH_RES = 1, MG_ST_RESIDUAL = 2, MG_ST_GHOST = 3, MG_ST_RESTRICT = 4,
-       MG_ST_PROLONG = 5, MG_ST_COARSE = 6, MG_ST_INJECT_UP = 7, MG_ST_NORM = 8, MG_ST_COUNT = 9 };
+       MG_ST_PROLONG = 5, MG_ST_COARSE = 6, MG_ST_INJECT_UP = 7, MG_ST_NORM = 8, MG_ST_FAS = 9, MG_ST_COUNT = 10 };
 int mg_profile(mg_handle* h, int enable);
 int mg_profile_read(mg_handle* h, double* ms, int64_t* counts);
 /* Number of kernels this library has launched so far in the process (all handles). */

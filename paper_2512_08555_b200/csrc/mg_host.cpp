@@ -96,7 +96,8 @@ struct Level {
   // (dst level | src level << 4, dst index, src index), every source on the finest level
   std::vector<int32_t> chain_lev, chain_dst, chain_src;
   int32_t *d_chain_lev = nullptr, *d_chain_dst = nullptr, *d_chain_src = nullptr;
-  int gbox_szA = 0, gbox_szB = 0;  // c2f box kernel shared memory (doubles), max over the level's boxes
+  int gbox_szA = 0, gbox_szB = 0;  // c2f box kernel shared memory (doubles), max over the level's thick boxes
+  int gbox_nthin = 0;              // boxes [0, gbox_nthin) go to the warp-per-box thin kernel
   std::vector<int32_t> sw_blk, sw_len, sw_z;  // sweep pencils (z-split blocks on small levels)
   int pen_lmax = 0;
   std::vector<uint32_t> nbr_real, nbr_ext;
@@ -194,7 +195,7 @@ struct mg_handle {
 namespace {
 
 enum Stage { ST_SMOOTH = 0, ST_SMOOTH_RES, ST_RESIDUAL, ST_GHOST, ST_RESTRICT, ST_PROLONG, ST_COARSE, ST_INJECT_UP,
-             ST_NORM, ST_COUNT };
+             ST_NORM, ST_FAS, ST_COUNT };
 
 cudaEvent_t get_ev(mg_handle* h) {
   if (!h->evpool.empty()) {
@@ -209,7 +210,7 @@ cudaEvent_t get_ev(mg_handle* h) {
 
 const char* const kStageName[ST_COUNT] = {"mg smooth", "mg smooth+residual", "mg residual", "mg ghost fill",
                                           "mg restrict", "mg prolong", "mg coarse solve", "mg inject-up",
-                                          "mg norm"};
+                                          "mg norm", "mg FAS rhs"};
 
 // RAII around one stage: an NVTX range (host timeline, for nsys / ncu --nvtx filters)
 // and, when profiling, a CUDA event pair on the handle's stream.
@@ -322,6 +323,7 @@ void validate_and_build(mg_handle* h) {
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
     if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
     if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 1)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..1");
+    if (a == 0 && (d.ghost_kernel < 0 || d.ghost_kernel > 2)) throw MgError(MG_ERR_ARG, "ghost_kernel must be 0..2");
     if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1 || d.staging < 0 || d.staging > 1))
       throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse and staging 0..1");
     // face pairs: periodic, unbounded, or semi-unbounded: EVEN/ODD symmetry at
@@ -726,6 +728,8 @@ void build_ghost_boxes(mg_handle* h) {
     const Level& C = h->L[m - 1];
     l.gbox.clear();
     l.gbox_szA = l.gbox_szB = 0;
+    std::vector<int32_t> thin, thick;  // records of boxes <= 2 / > 2 nodes thick along the thinnest axis
+    int thin_szA = 0, thin_szB = 0;
     const int B = l.B;
     for (int gi = 0; gi < l.nghost; ++gi) {
       std::vector<uint8_t> nd(l.B3);
@@ -763,10 +767,15 @@ void build_ghost_boxes(mg_handle* h) {
                             ? -1
                             : C.bmap[((size_t)b2 * C.bmap_n[1] + b1) * C.bmap_n[0] + b0];
         }
-        l.gbox.insert(l.gbox.end(), rec, rec + GBOX_REC);
-        // region A = max(coarse stage, pass-y output), region B = pass-x output
-        l.gbox_szA = std::max(l.gbox_szA, std::max(nc[0] * nc[1] * nc[2], nf[0] * nf[1] * nc[2]));
-        l.gbox_szB = std::max(l.gbox_szB, nf[0] * nc[1] * nc[2]);
+        // thin boxes (<= 2 nodes along some axis: the layers of the distance-1 halo) are
+        // candidates for the warp-per-box kernel (decided per level below)
+        const bool is_thin = std::min(nf[0], std::min(nf[1], nf[2])) <= 2;
+        (is_thin ? thin : thick).insert((is_thin ? thin : thick).end(), rec, rec + GBOX_REC);
+        // CTA kernel: region A = max(coarse stage, pass-y output), region B = pass-x output
+        int& szA = is_thin ? thin_szA : l.gbox_szA;
+        int& szB = is_thin ? thin_szB : l.gbox_szB;
+        szA = std::max(szA, std::max(nc[0] * nc[1] * nc[2], nf[0] * nf[1] * nc[2]));
+        szB = std::max(szB, nf[0] * nc[1] * nc[2]);
       };
       // cut points per axis
       std::vector<int> cut[3];
@@ -813,7 +822,21 @@ void build_ghost_boxes(mg_handle* h) {
             emit(lo, hi);
           }
     }
-    if (sizeof(double) * (size_t)(2 * l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
+    // The warp-per-box kernel (mg_ghost.cu) wins when the level has enough boxes to fill
+    // the GPU with warps (cfg5 levels 2-4: 2 000 - 13 000 boxes); with few boxes, or the
+    // large multi-layer boxes of exterior chains (U1, cfg3), one CTA per box has more
+    // parallelism per box (B200: cfg5 level 1, 800 boxes, 110 vs 90 us; cfg3 747 vs 491
+    // us of ghost fill per V-cycle).  mg_desc.ghost_kernel: 1 never, 2 always.
+    const int nthin = (int)(thin.size() / GBOX_REC);
+    const bool use_thin = h->d.ghost_kernel == 2 || (h->d.ghost_kernel == 0 && !l.ext_chain && nthin >= 2048);
+    l.gbox_nthin = use_thin ? nthin : 0;
+    if (!use_thin) {
+      l.gbox_szA = std::max(l.gbox_szA, thin_szA);
+      l.gbox_szB = std::max(l.gbox_szB, thin_szB);
+    }
+    l.gbox = std::move(thin);
+    l.gbox.insert(l.gbox.end(), thick.begin(), thick.end());
+    if (sizeof(double) * (size_t)(l.gbox_szA + l.gbox_szB) > c2f_box_smem_max(I))
       throw MgError(MG_ERR_LAYOUT_GHOST, "ghost box exceeds the c2f kernel's shared memory");
   }
 }
@@ -1146,6 +1169,17 @@ void setup_coarse(mg_handle* h) {
 // ----------------------------------------------------------------------------------
 void swap_u(Level& l) { l.cur = 1 - l.cur; }
 
+// c2f of every ghost box of level m: thin boxes one warp each, thick boxes one CTA each
+void c2f_boxes(mg_handle* h, int m, double* fine_field, const double* coarse_field, bool ext_zero) {
+  Level& F = h->L[m];
+  const int nbox = (int)F.gbox.size() / GBOX_REC;
+  if (nbox == 0) return;
+  const LevelView fv = view(h, m), cv = view(h, m - 1);
+  launch_c2f_thin(fv, cv, F.d_gbox, F.gbox_nthin, fine_field, coarse_field, h->I, ext_zero, h->s);
+  launch_c2f_box(fv, cv, F.d_gbox + (size_t)F.gbox_nthin * GBOX_REC, nbox - F.gbox_nthin, F.gbox_szA, F.gbox_szB,
+                 fine_field, coarse_field, h->I, ext_zero, h->s);
+}
+
 // boundary-ghost refresh of level m (reading Z9): f2c injection into level m-1,
 // then c2f; exterior chains (reading U1) refresh every coarser level first.
 void refresh(mg_handle* h, int m) {
@@ -1172,13 +1206,7 @@ void refresh(mg_handle* h, int m) {
                            h->s);
     }
   }
-  for (int j = lo; j <= m; ++j) {
-    Level& F = h->L[j];
-    if (F.gbox.empty()) continue;
-    LevelView fv = view(h, j), cv = view(h, j - 1);
-    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.u[F.cur], cv.u, h->I, false,
-                   h->s);
-  }
+  for (int j = lo; j <= m; ++j) c2f_boxes(h, j, h->L[j].u[h->L[j].cur], h->L[j - 1].u[h->L[j - 1].cur], false);
 }
 
 bool has_ghosts(mg_handle* h, int m) { return m > 0 && !h->L[m].c2f_dst.empty(); }
@@ -1189,8 +1217,10 @@ void residual_kernel(mg_handle* h, int m) {
   if (!launch_res_pencil(v, h->order, h->s)) launch_residual(v, h->order, h->s);
 }
 
-void sweep(mg_handle* h, int m, bool with_res) {
-  refresh(h, m);
+// fresh: the boundary ghosts of level m are current (refreshed since the last write of
+// u on levels m and m-1), so the refresh before the sweep is skipped
+void sweep(mg_handle* h, int m, bool with_res, bool fresh = false) {
+  if (!fresh) refresh(h, m);
   Level& l = h->L[m];
   const int mode = h->smoother == MG_SMOOTHER_RBGS ? SM_RB : SM_JACOBI;
   // Fuse the residual into the last sweep only on small-block levels: on B = 16
@@ -1242,7 +1272,7 @@ void restrict_level(mg_handle* h, int m) {
     launch_restrict(view(h, m), view(h, m - 1), h->s);
   }
   refresh(h, m - 1);
-  Prof pr(h, ST_RESTRICT, m);
+  Prof pr(h, ST_FAS, m - 1);  // FAS right-hand side + û of the coarse level (its unknowns)
   if (launch_fas_pencil(view(h, m - 1), h->order, h->s)) {
     // the pencil FAS kernel wrote û on the real blocks; the prolongation also takes ε on
     // the exterior band (reading Z13-W, U1 / level 0), stored in the ghost blocks
@@ -1324,8 +1354,15 @@ void inject_up_all(mg_handle* h) {
 void vcycle_body(mg_handle* h) {
   const int top = (int)h->L.size() - 1;
   for (int m = top; m >= 1; --m) {
-    for (int k = 1; k <= h->eta1; ++k) sweep(h, m, false);
-    refresh(h, m);
+    // below the top, restrict_level(m + 1) has just refreshed level m (the FAS kernel
+    // after it writes f and û only): the first pre-sweep's refresh would recompute the
+    // same ghost values
+    bool fresh = m < top;
+    for (int k = 1; k <= h->eta1; ++k) {
+      sweep(h, m, false, fresh);
+      fresh = false;
+    }
+    if (!fresh) refresh(h, m);
     restrict_level(h, m);
   }
   coarse_solve(h);
@@ -1487,13 +1524,7 @@ void set_rhs(mg_handle* h, const double* f_dev) {
     launch_inject_up(fv, cv, h->L[m - 1].f, h->s);
   }
   // f ghosts: c2f of f, f := 0 beyond unbounded faces (reading Z16)
-  for (int m = 1; m < nlev; ++m) {
-    Level& F = h->L[m];
-    if (F.gbox.empty()) continue;
-    LevelView fv = view(h, m), cv = view(h, m - 1);
-    launch_c2f_box(fv, cv, F.d_gbox, (int)F.gbox.size() / GBOX_REC, F.gbox_szA, F.gbox_szB, F.f, h->L[m - 1].f, h->I, true,
-                   h->s);
-  }
+  for (int m = 1; m < nlev; ++m) c2f_boxes(h, m, h->L[m].f, h->L[m - 1].f, true);
   const int64_t cs0 = (int64_t)h->L[0].ntot() * h->L[0].B3;
   if (!h->fwall.empty()) launch_fill_list((int)h->fwall.size(), h->d_fwall, h->L[0].f, 0.0, h->nc, cs0, h->s);
   if (!h->fm_dst.empty())

@@ -108,6 +108,8 @@ void prepare_pencil_kernels();
 // (slot sx + 3 sy + 9 sz; -1 = none), 1 unused
 constexpr int GBOX_REC = 40;
 size_t c2f_box_smem_max(int I);
+void launch_c2f_thin(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, double* fine_field,
+                     const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void launch_c2f_box(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, int szA,
                     int szB, double* fine_field, const double* coarse_field, int I, bool ext_zero, cudaStream_t s);
 void prepare_ghost_kernels();

@@ -314,14 +314,16 @@ __device__ __forceinline__ void rb_body(const LevelView& L, const RBCtx& cx, int
         const double2 cc = *reinterpret_cast<const double2*>(U);
         const double2 p = *reinterpret_cast<const double2*>(TMA ? Us + (ro >> 18) : U + TW);
         const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);  // u(x0-1), u(x0+2)
+        // rows y-1 + y+1 per column: the diagonal sums need one shuffle per column
+        // (u(x0-1, y-1) + u(x0-1, y+1) is the left lane's qy)
+        const double qx = m.x + p.x, qy = m.y + p.y;
         cq[0] = cc.x;
         cq[1] = cc.y;
-        s4q[0] = (l + cc.y) + (m.x + p.x);
-        s4q[1] = (cc.x + r) + (m.y + p.y);
+        s4q[0] = (l + cc.y) + qx;
+        s4q[1] = (cc.x + r) + qy;
         if (ORDER == 4) {
-          const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
-          d4q[0] = (ml + m.y) + (pl + p.y);
-          d4q[1] = (m.x + mr) + (p.x + pr);
+          d4q[0] = shfl_up1(qy) + qy;
+          d4q[1] = qx + shfl_dn1(qx);
         } else {
           d4q[0] = d4q[1] = 0.0;
         }
@@ -561,13 +563,13 @@ __device__ __forceinline__ void rb6_body(const LevelView& L, const RBCtx& cx, in
         const double2 cc = *reinterpret_cast<const double2*>(U);
         const double2 p = *reinterpret_cast<const double2*>(U + TW);
         const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
-        const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
+        const double qx = m.x + p.x, qy = m.y + p.y;  // rows y±1 per column (diagonals: one shuffle)
         cq[0] = cc.x;
         cq[1] = cc.y;
-        s4q[0] = (l + cc.y) + (m.x + p.x);
-        s4q[1] = (cc.x + r) + (m.y + p.y);
-        d4q[0] = (ml + m.y) + (pl + p.y);
-        d4q[1] = (m.x + mr) + (p.x + pr);
+        s4q[0] = (l + cc.y) + qx;
+        s4q[1] = (cc.x + r) + qy;
+        d4q[0] = shfl_up1(qy) + qy;
+        d4q[1] = qx + shfl_dn1(qx);
       }
       // γ of column O at its red plane s-2 (red values of plane s-2 written last step)
       double gam;
@@ -861,88 +863,61 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
 // fine positions outside the level's blocks, reading Z14) is computed as in the RB
 // sweep (pairs of columns, shuffles for the in-row neighbours, Mehrstellen partial
 // sums per column: r(z) = f(z) - h6 [α(z-1) + β(z) + α(z+1)]); each pair also forms
-// the x-weighted sum at its even column (one shuffle) into a 2-plane shared ring, and
-// 2 extra warps form the y- and z-weights and the coarse values (u injection at even
-// planes, E7; r_c = Σ w w w r, E6).  The fine residual is never written to HBM.
-// Step s: load plane s | r at plane s-1 | xy weights of r(s-2) | coarse r at s-3.
+// the x-weighted sum at its even column (one shuffle) into a 2-plane shared ring.
+// Warps hold rows of one parity (0-2 even, 3-5 odd, as in the sweep), so the coarse
+// work stays in the even-row warps: the pair at (x0, y) = (2 qx, 2 qy) writes the
+// coarse u(qx, qy) at even planes from its own centre value (injection, E7) and forms
+// the y- and z-weights of the coarse residual (E6) from its own x-weighted sum (kept
+// in a register) and rows y±1 of the ring.  No extra warps: 6 warps, 4 CTAs per SM.
+// The fine residual is never written to HBM.
+// Step s: load plane s | r at plane s-1 | y weights of r(s-2) | coarse r at s-3.
 struct RR2Shape {
   static constexpr int T = PB + 4, TW = 26, TP = T * TW;  // u tile as in the RB sweep
   static constexpr int D = 2, R = 4;
-  static constexpr int NR = 192;                           // 6 warps of 30 pair threads
-  static constexpr int NT = NR + 64;                       // + 2 warps for the coarse nodes
+  static constexpr int NT = 192;                           // 6 warps of 30 pair threads
   static constexpr int NPAIR = T * T / 2;                  // 200 u pairs per plane
-  static constexpr int NLD = (NPAIR + NT - 1) / NT;        // 1
+  static constexpr int NLD = (NPAIR + NT - 1) / NT;        // 2
   // x-weighted residual rows sx (one per pair, at its even column): rows [-1, 17),
   // pairs 0..9, odd pitch
   static constexpr int SXW = 11, SXP = 18 * SXW;
-  // [R][TP] u | [R][NR] f pairs | [2][SXP] sx
-  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + R * NR * 2 + 2 * SXP);
+  // [R][TP] u | [R][NT] f pairs | [2][SXP] sx
+  static constexpr size_t SMEM = sizeof(double) * (size_t)(R * TP + R * NT * 2 + 2 * SXP);
 };
 
-template <int ORDER>
-__global__ void __maxnreg__(80)
-    k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
+template <int ORDER, int RP>
+__device__ __forceinline__ void rr2_body(const LevelView& L, const LevelView& C, const int* snb, const uint32_t* sreal,
+                                         const int* spar, double* sm, const int (&ld_xy)[2], const int (&ld_sxy)[2],
+                                         const int (&ld_dst)[2], int wg, int lane, int len, double inv_h2) {
   using S = RR2Shape;
-  comp_view(L);
-  comp_view(C);
-  constexpr int T = S::T, TW = S::TW, TP = S::TP, D = S::D, R = S::R, NR = S::NR, NT = S::NT;
-  constexpr int SXW = S::SXW, SXP = S::SXP;
-  extern __shared__ __align__(16) double sm[];
+  constexpr int TW = S::TW, TP = S::TP, D = S::D, R = S::R, NT = S::NT, NLD = S::NLD, SXW = S::SXW, SXP = S::SXP;
   double* su = sm;
-  double2* sf = reinterpret_cast<double2*>(sm + R * TP);  // [R][NR]
-  double* sxr = sm + R * TP + R * NR * 2;                  // [2][SXP]
-  __shared__ int snb[PMAXL * 27];
-  __shared__ uint32_t sreal[PMAXL];
-  __shared__ int spar[PMAXL * 4];
+  double2* sf = reinterpret_cast<double2*>(sm + R * TP);  // [R][NT]
+  double* sxr = sm + R * TP + R * NT * 2;                  // [2][SXP]
   const int tid = threadIdx.x;
-  const int len = __ldg(L.pen_len + blockIdx.x);
   const int nz = PB * len;
-  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
-  for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
-  if (tid < len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
-  if (tid < 4 * len) spar[tid] = __ldg(L.parent + 4 * (size_t)__ldg(pb + tid / 4) + tid % 4);
-  // u load items (interior 128-byte lines first, then halo pieces), one per thread
-  int ld_xy, ld_sxy, ld_dst;
-  {
-    const int j = tid;
-    int py, px;
-    if (j < 8 * T) {
-      py = j / 8;
-      px = 2 + 2 * (j % 8);
-    } else {
-      const int hh = j - 8 * T;
-      py = hh / 2;
-      px = (hh & 1) ? PB + 2 : 0;
-    }
-    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
-    ld_xy = (y - PB * dy) * PB + (x - PB * dx);
-    ld_sxy = j < S::NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
-    ld_dst = py * TW + px;
-  }
-  // residual pair threads (warps 0-5): rows y = 3 w + lane / 10 - 1 in [-1, 17), x0 even
-  const int w = tid >> 5, lane = tid & 31;
-  const bool rthr = w < 6;
-  const bool valid = rthr && lane < 30;
-  const int ry = rthr ? 3 * w + (valid ? lane / 10 : 2) - 1 : 0;
+  const bool valid = lane < 30;  // lanes 30, 31 mirror lane 29 (broadcast reads), write nothing
+  const int ri = valid ? 3 * wg + lane / 10 : 3 * wg + 2;
   const int pi = valid ? lane % 10 : 9;
-  const int x0 = 2 * pi - 2;
+  const int ry = 2 * ri - RP, x0 = 2 * pi - 2;
   const int i0 = (ry + 2) * TW + (x0 + 2);
   const int dxc = reg16(x0), dyc = reg16(ry);
   const int sxy = (dxc + 1) + 3 * (dyc + 1);
   const int fxy = (ry - PB * dyc) * PB + (x0 - PB * dxc);
-  double2* sfme = sf + (rthr ? tid : 0);
-  // coarse threads (warps 6-7): (qx, qy) of the octant
-  const bool cthr = tid >= NR;
-  const int qx = (tid - NR) & 7, qy = ((tid - NR) >> 3) & 7;
-  __syncthreads();
+  double2* sfme = sf + tid;
+  double* sxme = sxr + (ry + 1) * SXW + pi;
+  // coarse pair: even row, even column inside the block (RP = 0 warps only)
+  const bool cthr = RP == 0 && valid && pi >= 1 && pi <= 8 && ry <= 14;
+  const int qx = pi - 1, qy = ry >> 1;
 
-  const double* ip = nullptr;
+  const double* ip[NLD];
   const double* fp = nullptr;
   auto seek_issue = [&](int z) {
     int k, dz, zl;
     plane_src(z, nz, len, k, dz, zl);
     const int o = zl * (PB * PB);
-    ip = ld_sxy < 0 ? nullptr : L.u + (size_t)snb[k * 27 + ld_sxy + 9 * (dz + 1)] * PB3 + o + ld_xy;
+#pragma unroll
+    for (int d = 0; d < NLD; ++d)
+      ip[d] = ld_sxy[d] < 0 ? nullptr : L.u + (size_t)snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)] * PB3 + o + ld_xy[d];
     fp = L.f + (size_t)snb[k * 27 + sxy + 9 * (dz + 1)] * PB3 + o + fxy;
   };
   // stage plane z (called for z = -2, -1, … in order) into ring slot (z+2) & (R-1)
@@ -950,9 +925,13 @@ __global__ void __maxnreg__(80)
     if (!decltype(checked)::value || z < nz + 2) {
       if ((z & 15) == 0) seek_issue(z);
       const int slot = (z + 2) & (R - 1);
-      if (ld_sxy >= 0) cpa16(su + slot * TP + ld_dst, ip);
-      ip += PB * PB;
-      if (valid && (!decltype(checked)::value || (z >= -1 && z <= nz))) cpa16(sfme + slot * NR, fp);
+#pragma unroll
+      for (int d = 0; d < NLD; ++d) {
+        if (ld_sxy[d] < 0) continue;
+        cpa16(su + slot * TP + ld_dst[d], ip[d]);
+        ip[d] += PB * PB;
+      }
+      if (valid && (!decltype(checked)::value || (z >= -1 && z <= nz))) cpa16(sfme + slot * NT, fp);
       fp += PB * PB;
     }
     cpa_commit();
@@ -969,7 +948,8 @@ __global__ void __maxnreg__(80)
   for (int q = 0; q < D; ++q) issue(-2 + q, std::true_type{});
 
   double aA[2] = {0, 0}, aP[2] = {0, 0};  // per column: α(s-1); α(s-2) + β(s-1)
-  double t0 = 0, t1 = 0, t2 = 0;          // coarse threads: T at planes s-2, s-3, s-4
+  double sxp = 0.0;                       // this pair's x-weighted residual at plane s-2
+  double t0 = 0, t1 = 0, t2 = 0;          // coarse pairs: y-weighted sums at planes s-2, s-3, s-4
   const double h6 = ORDER == 4 ? inv_h2 * (1.0 / 6.0) : ORDER == 6 ? inv_h2 * (1.0 / 30.0) : inv_h2;
   // per column: α = 2c + S4, β = 2S4 + D4 - 24c (M = 4, times 6h^2); α = 14c + 3S4 + D4,
   // β = 14S4 + 3D4 - 128c (M = 6, times 30h^2; the corners enter through D4 in α)
@@ -991,54 +971,55 @@ __global__ void __maxnreg__(80)
       cpa_wait<D - 1>();
       __syncthreads();
       issue(s + D, std::integral_constant<bool, LAST>{});
-      if (rthr) {
-        // plane s (shuffles: every lane of warps 0-5 takes part)
-        const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
-        const double2 m = *reinterpret_cast<const double2*>(U - TW);
-        const double2 cc = *reinterpret_cast<const double2*>(U);
-        const double2 p = *reinterpret_cast<const double2*>(U + TW);
-        const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
-        double cq[2] = {cc.x, cc.y};
-        double s4q[2] = {(l + cc.y) + (m.x + p.x), (cc.x + r) + (m.y + p.y)};
-        double d4q[2] = {0, 0};
-        if (ORDER >= 4) {
-          const double ml = shfl_up1(m.y), mr = shfl_dn1(m.x), pl = shfl_up1(p.y), pr = shfl_dn1(p.x);
-          d4q[0] = (ml + m.y) + (pl + p.y);
-          d4q[1] = (m.x + mr) + (p.x + pr);
+      // plane s (shuffles: every lane takes part)
+      const double* U = su + ((s + 2) & (R - 1)) * TP + i0;
+      const double2 m = *reinterpret_cast<const double2*>(U - TW);
+      const double2 cc = *reinterpret_cast<const double2*>(U);
+      const double2 p = *reinterpret_cast<const double2*>(U + TW);
+      const double l = shfl_up1(cc.y), r = shfl_dn1(cc.x);
+      const double qxs = m.x + p.x, qys = m.y + p.y;  // rows y±1 per column (diagonals: one shuffle)
+      double cq[2] = {cc.x, cc.y};
+      double s4q[2] = {(l + cc.y) + qxs, (cc.x + r) + qys};
+      double d4q[2] = {0, 0};
+      if (ORDER >= 4) {
+        d4q[0] = shfl_up1(qys) + qys;
+        d4q[1] = qxs + shfl_dn1(qxs);
+      }
+      double sxc = 0.0;
+      if (!EDGE || s >= 0) {  // residual at plane s-1 in [-1, nz]
+        if (((s - 1) & 15) == 0) seek_live(s - 1);
+        const double2 fq = sfme[((s + 1) & (R - 1)) * NT];
+        double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
+        if (live) {
+          rr.x = fq.x - (aP[0] + alpha_of(cq[0], s4q[0], d4q[0])) * h6;
+          rr.y = fq.y - (aP[1] + alpha_of(cq[1], s4q[1], d4q[1])) * h6;
         }
-        if (!EDGE || s >= 0) {  // residual at plane s-1 in [-1, nz]
-          if (((s - 1) & 15) == 0) seek_live(s - 1);
-          const double2 fq = sfme[((s + 1) & (R - 1)) * NR];
-          double2 rr = make_double2(0.0, 0.0);  // r := 0 outside the level's blocks (Z14)
-          if (live) {
-            rr.x = fq.x - (aP[0] + alpha_of(cq[0], s4q[0], d4q[0])) * h6;
-            rr.y = fq.y - (aP[1] + alpha_of(cq[1], s4q[1], d4q[1])) * h6;
-          }
-          // full weighting along x at this pair's even column x0: r(x0-1) is the left
-          // lane's second column (the definition's order: 0.25 r(-1) + 0.5 r(0) + 0.25 r(1))
-          const double rl = shfl_up1(rr.y);
-          const double sx = 0.25 * rl + 0.5 * rr.x + 0.25 * rr.y;
-          if (valid) sxr[((s - 1) & 1) * SXP + (ry + 1) * SXW + pi] = sx;
-        }
+        // full weighting along x at this pair's even column x0: r(x0-1) is the left
+        // lane's second column (the definition's order: 0.25 r(-1) + 0.5 r(0) + 0.25 r(1))
+        const double rl = shfl_up1(rr.y);
+        sxc = 0.25 * rl + 0.5 * rr.x + 0.25 * rr.y;
+        if (valid) sxme[((s - 1) & 1) * SXP] = sxc;
+      }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          aP[q] = aA[q] + beta_of(cq[q], s4q[q], d4q[q]);  // α(s-1) + β(s): the node at s, completed at step s+1
-          aA[q] = alpha_of(cq[q], s4q[q], d4q[q]);
-        }
-      } else if (cthr) {
-        // coarse u = fine u(2i) at even interior planes (E7)
+      for (int q = 0; q < 2; ++q) {
+        aP[q] = aA[q] + beta_of(cq[q], s4q[q], d4q[q]);  // α(s-1) + β(s): the node at s, completed at step s+1
+        aA[q] = alpha_of(cq[q], s4q[q], d4q[q]);
+      }
+      if (cthr) {
+        // coarse u = fine u(2i) at even interior planes (E7): this pair's centre value
         if ((j & 1) == 0 && (!EDGE || (s >= 0 && s < nz))) {
           const int k = s >> 4, qz = (s & 15) >> 1;
           const int* pr = spar + 4 * k;
-          C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] =
-              su[((s + 2) & (R - 1)) * TP + (2 * qy + 2) * TW + (2 * qx + 2)];
+          C.u[(size_t)pr[0] * C.B3 + ((pr[3] + qz) * C.B + (pr[2] + qy)) * C.B + (pr[1] + qx)] = cq[0];
         }
-        // full weighting of the residual plane s-2 (written last step): x, then y, then z
+        // full weighting of the residual plane s-2 along y (rows y±1 written last step,
+        // row y this pair's own), then along z
         if (!EDGE || s >= 1) {
-          const double* rp = sxr + ((s - 2) & 1) * SXP + (2 * qy + 1) * SXW + (qx + 1);  // pair qx+1: x0 = 2qx
+          const double* rp = sxme + ((s - 2) & 1) * SXP;
           double sy = 0.0;
-#pragma unroll
-          for (int dy = -1; dy <= 1; ++dy) sy += (dy == 0 ? 0.5 : 0.25) * rp[dy * SXW];
+          sy += 0.25 * rp[-SXW];
+          sy += 0.5 * sxp;
+          sy += 0.25 * rp[SXW];
           t2 = t1; t1 = t0; t0 = sy;
           const int zc = s - 3;  // even when j is odd
           if ((j & 1) == 1 && zc >= 0 && zc < nz) {
@@ -1049,6 +1030,7 @@ __global__ void __maxnreg__(80)
           }
         }
       }
+      sxp = sxc;
     }
   };
   const int nt = (nz + 4) >> 2;
@@ -1056,6 +1038,48 @@ __global__ void __maxnreg__(80)
   for (int t = 1; t < nt - 1; ++t) group(4 * t, std::integral_constant<int, 1>{});
   group(4 * (nt - 1), std::integral_constant<int, 2>{});
   cpa_wait<0>();
+}
+
+template <int ORDER>
+__global__ void __maxnreg__(80)
+    k_rr2_pencil(LevelView L, LevelView C, double inv_h2) {
+  using S = RR2Shape;
+  comp_view(L);
+  comp_view(C);
+  constexpr int T = S::T, TW = S::TW, NT = S::NT, NLD = S::NLD;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int snb[PMAXL * 27];
+  __shared__ uint32_t sreal[PMAXL];
+  __shared__ int spar[PMAXL * 4];
+  const int tid = threadIdx.x;
+  const int len = __ldg(L.pen_len + blockIdx.x);
+  const int32_t* pb = L.pen_blk + (size_t)blockIdx.x * L.pen_lmax;
+  for (int i = tid; i < len * 27; i += NT) snb[i] = __ldg(L.nbr + (size_t)__ldg(pb + i / 27) * 27 + i % 27);
+  if (tid < len) sreal[tid] = __ldg(L.nbr_real + __ldg(pb + tid));
+  if (tid < 4 * len) spar[tid] = __ldg(L.parent + 4 * (size_t)__ldg(pb + tid / 4) + tid % 4);
+  // u load items (interior 128-byte lines first, then halo pieces), as in the RB sweep
+  int ld_xy[2], ld_sxy[2], ld_dst[2];
+#pragma unroll
+  for (int d = 0; d < NLD; ++d) {
+    const int j = tid + d * NT;
+    int py, px;
+    if (j < 8 * T) {
+      py = j / 8;
+      px = 2 + 2 * (j % 8);
+    } else {
+      const int hh = j - 8 * T;
+      py = hh / 2;
+      px = (hh & 1) ? PB + 2 : 0;
+    }
+    const int x = px - 2, y = py - 2, dx = reg16(x), dy = reg16(y);
+    ld_xy[d] = (y - PB * dy) * PB + (x - PB * dx);
+    ld_sxy[d] = j < S::NPAIR ? (dx + 1) + 3 * (dy + 1) : -1;
+    ld_dst[d] = py * TW + px;
+  }
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  if (w < 3) rr2_body<ORDER, 0>(L, C, snb, sreal, spar, sm, ld_xy, ld_sxy, ld_dst, w, lane, len, inv_h2);
+  else rr2_body<ORDER, 1>(L, C, snb, sreal, spar, sm, ld_xy, ld_sxy, ld_dst, w - 3, lane, len, inv_h2);
 }
 
 bool launch_res_restrict_pencil(const LevelView& fine, const LevelView& coarse, int order, cudaStream_t s) {

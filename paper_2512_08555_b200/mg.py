@@ -27,7 +27,7 @@ EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_sol
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
            "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
            "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison", "mg_transfer"]
-STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm"]
+STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm", "fas"]
 
 
 class MgDesc(C.Structure):
@@ -37,7 +37,7 @@ class MgDesc(C.Structure):
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
                 ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
                 ("zsplit", C.c_int32), ("fuse", C.c_int32), ("ncomp", C.c_int32), ("coarse_pruning", C.c_int32),
-                ("staging", C.c_int32)]
+                ("staging", C.c_int32), ("ghost_kernel", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -175,6 +175,7 @@ class Solver:
         d.staging = int(cfg.get("staging", 0))
         d.ncomp = int(cfg.get("ncomp", 1))
         d.coarse_pruning = int(cfg.get("coarse_pruning", 0))
+        d.ghost_kernel = int(cfg.get("ghost_kernel", 0))
         self.nc = max(1, d.ncomp)
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))

@@ -208,7 +208,7 @@ def test_vcycle_parity(name, cycles):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,variant", [("puu1", {}), ("cfg3_64", {}), ("puu1_m6", {}),
                                           ("puu2", {"pencil_blocks": 2}), ("cfg3_64", {"pencil_blocks": 4}),
-                                          ("cfg5_small", {"pencil_blocks": 2})])
+                                          ("cfg5_small", {"pencil_blocks": 2}), ("cfg5_small", {"ghost_kernel": 2})])
 def test_vcycle_parity_graph_and_determinism(name, variant):
     """CUDA-graph launched V-cycles (the bench configuration) vs the oracle, and bitwise
     determinism of two fresh runs; cfg3_64 exercises the composed exterior-chain

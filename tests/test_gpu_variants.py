@@ -15,7 +15,8 @@ from tests.test_gpu_parity import CYCLE_TOL, OP_TOL, _cfg, _prepared
 
 LAYOUTS = ["puu2", "cfg3_64", "ou_uu", "per_adapt", "cfg2_64"]
 VARIANTS = [dict(pencil_blocks=1, zsplit=1), dict(pencil_blocks=1, zsplit=2), dict(pencil_blocks=2),
-            dict(pencil_blocks=4), dict(pencil_blocks=2, fuse=1), dict(pencil_blocks=2, staging=1)]
+            dict(pencil_blocks=4), dict(pencil_blocks=2, fuse=1), dict(pencil_blocks=2, staging=1),
+            dict(ghost_kernel=1), dict(ghost_kernel=2)]
 
 
 def _vid(v):

@@ -19,8 +19,13 @@ def main():
     ap.add_argument("--cfg", default="cfg2")
     ap.add_argument("--cycles", type=int, default=5)
     ap.add_argument("--extra", default="{}", help="extra cfg keys (json), e.g. fuse, pencil_blocks")
+    ap.add_argument("--lib", default="", help="libmg.so to load instead of the in-tree one (A/B builds)")
     a = ap.parse_args()
     import torch
+
+    if a.lib:
+        from paper_2512_08555_b200.mg import load_library
+        load_library(a.lib)
 
     from paper_2512_08555_b200 import Solver
     from workloads import configs as C
@@ -48,8 +53,9 @@ def main():
     print(json.dumps({"cfg": a.cfg, "extra": a.extra, "blocks": [i["nreal"] for i in info], "ghosts": [i["nghost"] for i in info],
                       "us_per_cycle[stage][level]=(us, launches)": rows}), flush=True)
     S.use_graph(True)
-    ms = S.time_op("vcycle", 0, 10)
-    print(json.dumps({"cfg": a.cfg, "graph_ms_per_vcycle": ms}), flush=True)
+    runs = sorted(S.time_op("vcycle", 0, 20) for _ in range(5))
+    print(json.dumps({"cfg": a.cfg, "lib": a.lib, "extra": a.extra, "graph_ms_per_vcycle": runs[2], "runs": runs}),
+          flush=True)
 
 
 if __name__ == "__main__":
