@@ -203,6 +203,11 @@ int mg_profile(mg_handle* h, int enable);
 int mg_profile_read(mg_handle* h, double* ms, int64_t* counts);
 /* Number of kernels this library has launched so far in the process (all handles). */
 int64_t mg_kernel_launches(void);
+/* Host wall time (ms) of the phases of mg_create: [0] layout validation and level
+ * hierarchy, [1] ghost blocks / need masks / transfer lists, [2] ghost boxes, [3] pencils,
+ * [4] device allocation and table upload, [5] coarse-solve setup (LGF tables, cuFFT
+ * plans).  ms: 6 doubles, caller-owned. */
+int mg_setup_times(const mg_handle* h, double* ms);
 
 /* ---- Grid adaptation (§2.1; readings A1, A2).
  * No handle: adaptation produces a new leaf list, from which the caller creates a new

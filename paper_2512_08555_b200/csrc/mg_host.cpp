@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -129,6 +130,7 @@ struct Level {
 
 struct mg_handle {
   mg_desc d{};
+  double setup_ms[6] = {0, 0, 0, 0, 0, 0};  // mg_create phases (mg_setup_times)
   int per[3] = {1, 1, 1};
   int sym[3] = {0, 0, 0};  // symmetric low face: mirror sign (+1 even, -1 odd), 0 none
   int hi_odd[3] = {0, 0, 0};  // odd high face (mirror about the unstored node N; reading S2)
@@ -1617,12 +1619,26 @@ int mg_create(const mg_desc* d, void* stream, mg_handle** out) {
     if (cudaGetDevice(&dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && nsm > 0)
       h->nsm = nsm;
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](int i) {
+      const auto t1 = std::chrono::steady_clock::now();
+      h->setup_ms[i] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      t0 = t1;
+    };
     validate_and_build(h);
+    lap(0);
     build_ghosts(h);
+    lap(1);
     build_ghost_boxes(h);
+    lap(2);
     build_pencils(h);
+    lap(3);
     alloc_device(h);
+    CUDA_OK(cudaStreamSynchronize(h->s));
+    lap(4);
     setup_coarse(h);
+    CUDA_OK(cudaStreamSynchronize(h->s));
+    lap(5);
   });
   if (rc != MG_OK) {
     destroy(h);
@@ -1755,6 +1771,12 @@ int mg_profile_read(mg_handle* h, double* ms, int64_t* counts) {
 }
 
 int64_t mg_kernel_launches(void) { return (int64_t)launches_issued(); }
+
+int mg_setup_times(const mg_handle* h, double* ms) {
+  if (!h || !ms) return MG_ERR_ARG;
+  for (int i = 0; i < 6; ++i) ms[i] = h->setup_ms[i];
+  return MG_OK;
+}
 
 int mg_num_levels(mg_handle* h) { return h ? (int)h->L.size() : MG_ERR_ARG; }
 

@@ -755,6 +755,11 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
     }
   }
   __syncthreads();
+  if (MODE == 2) {  // a pencil of fully covered blocks holds no leaf node: nothing to reduce
+    bool all = true;
+    for (int k = 0; k < len; ++k) all = all && scov[k] == 0xff;
+    if (all) return;
+  }
 
   auto issue = [&](int z) {
     if (z < nz + 1) {

@@ -26,7 +26,8 @@ MG_ALL_BLOCKS = 0x10000
 EXPORTS = ["mg_create", "mg_destroy", "mg_last_error", "mg_set_rhs", "mg_set_solution", "mg_get_solution",
            "mg_vcycle", "mg_residual_norm", "mg_solve", "mg_run_host", "mg_use_graph", "mg_level_info",
            "mg_level_blocks", "mg_num_levels", "mg_debug_field", "mg_debug_apply", "mg_time_op", "mg_profile",
-           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison", "mg_transfer"]
+           "mg_profile_read", "mg_kernel_launches", "mg_detail", "mg_adapt", "mg_debug_poison", "mg_transfer",
+           "mg_setup_times"]
 STAGES = ["smooth", "smooth_res", "residual", "ghost", "restrict", "prolong", "coarse", "inject_up", "norm", "fas"]
 
 
@@ -80,6 +81,7 @@ def load_library(path: str = _LIB_PATH):
     lib.mg_time_op.argtypes = [P, I, I, I, C.POINTER(D)]
     lib.mg_profile.argtypes = [P, I]
     lib.mg_profile_read.argtypes = [P, C.POINTER(D), C.POINTER(C.c_int64)]
+    lib.mg_setup_times.argtypes = [P, C.POINTER(D)]
     lib.mg_kernel_launches.argtypes = []
     lib.mg_kernel_launches.restype = C.c_int64
     I32P = C.POINTER(C.c_int32)
@@ -334,6 +336,12 @@ class Solver:
 
     def kernel_launches(self):
         return int(self.lib.mg_kernel_launches())
+
+    def setup_times(self):
+        """Host wall time (ms) of mg_create's phases (include/mg.h mg_setup_times)."""
+        ms = (C.c_double * 6)()
+        self._check(self.lib.mg_setup_times(self.h, ms))
+        return dict(zip(["hierarchy", "ghosts", "ghost_boxes", "pencils", "device_alloc", "coarse_setup"], list(ms)))
 
     def time_op(self, op, m, reps):
         ms = C.c_double()

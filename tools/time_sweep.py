@@ -25,8 +25,13 @@ def main():
     ap.add_argument("--stagings", default="0,1")
     ap.add_argument("--cycles", type=int, default=6)
     ap.add_argument("--extra", default="{}", help="extra cfg keys (json), e.g. pencil_blocks")
+    ap.add_argument("--lib", default="", help="libmg.so to load instead of the in-tree one (A/B builds)")
     args = ap.parse_args()
     import torch
+
+    if args.lib:
+        from paper_2512_08555_b200.mg import load_library
+        load_library(args.lib)
 
     from paper_2512_08555_b200 import Solver
     from workloads import configs as C
@@ -69,7 +74,7 @@ def main():
             S.vcycle(10)
             e1.record()
             torch.cuda.synchronize()
-            print(json.dumps({"config": name, "staging": st, "bitwise_same_as_first": same, "sweep": rows,
+            print(json.dumps({"config": name, "lib": args.lib, "staging": st, "bitwise_same_as_first": same, "sweep": rows,
                               "vcycle_ms": e0.elapsed_time(e1) / 10}), flush=True)
             del S
             torch.cuda.empty_cache()
