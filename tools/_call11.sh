@@ -1,0 +1,3 @@
+for lib in _ab/head/libmg.so _ab/m3/libmg.so; do
+timeout 300 python tools/time_sweep.py --configs cfg2,cfg5 --stagings 0 --cycles 6 --lib $lib >> gpurun_out/sweep11.jsonl 2>> gpurun_out/sweep11.err
+done
