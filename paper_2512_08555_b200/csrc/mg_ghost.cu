@@ -286,6 +286,9 @@ __global__ void __launch_bounds__(GT_W * 32, 3) k_c2f_thin(const int32_t* __rest
   const int* ofc = soff[w][ac];
   const int* sla = sslot[w][a];
   const int* ofa = soff[w][a];
+  // e / n for the flattened loops below as a multiply-high: exact for e * n < 2^32 (n >= 2;
+  // ncb >= I always, nfb = 1 for edge and corner boxes)
+  const unsigned mb = 0xFFFFFFFFu / (unsigned)ncb + 1u, mfb = nfb > 1 ? 0xFFFFFFFFu / (unsigned)nfb + 1u : 0u;
   double* P = sP[w];
   double* T = sT[w];
   double* dst = ff + (size_t)rec[0] * F.B3 + doff;
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(GT_W * 32, 3) k_c2f_thin(const int32_t* __rest
       for (int k = 0; k < K; ++k) {
         const int e = e0 + 32 * k;
         if (e >= npl) continue;
-        const int qc = e / ncb, qb = e - qc * ncb;
+        const int qc = (int)__umulhi((unsigned)e, mb), qb = e - qc * ncb;
         const int s0 = 12 + slb[qb] + slc[qc];
         const double* src = cf + ofb[qb] + ofc[qc];
 #pragma unroll
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(GT_W * 32, 3) k_c2f_thin(const int32_t* __rest
     __syncwarp();
     // T[fc][qb]: the rule along c
     for (int e = lane; e < nfc * ncb; e += 32) {
-      const int fc = e / ncb, qb = e - fc * ncb;
+      const int fc = (int)__umulhi((unsigned)e, mb), qb = e - fc * ncb;
       int first;
       const bool odd = taps<I>(g0c + fc, c0c, first);
       T[e] = apply_taps<I>(P + first * ncb + qb, ncb, odd);
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(GT_W * 32, 3) k_c2f_thin(const int32_t* __rest
     const int Ja = g0a + la;
     const bool exta = !pera && (Ja < 0 || Ja >= Na);
     for (int e = lane; e < nfc * nfb; e += 32) {
-      const int fc = e / nfb, fb = e - fc * nfb;
+      const int fc = nfb > 1 ? (int)__umulhi((unsigned)e, mfb) : e, fb = e - fc * nfb;
       const int Jb = g0b + fb, Jc = g0c + fc;
       const bool ext = exta || (!perb && (Jb < 0 || Jb >= Nb)) || (!perc && (Jc < 0 || Jc >= Nc));
       double v;
