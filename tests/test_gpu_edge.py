@@ -99,7 +99,7 @@ def test_block_size_8_parity(B):
     f = S.sample_on_leaves(dom, lv, lambda x, y, z: S.gaussian_charge(x, y, z, sigma=0.1, c=(0.4, 0.5, 0.5)))
     p = Pair(d, lv, f)
     for _ in range(2):
-        p.o.vcycle(1)
+        p.ocycle()
         p.g.vcycle(1)
     assert rel_err(p.solution(), p.o.get_solution()) < 1e-9
 
@@ -154,7 +154,7 @@ def test_poisoned_unneeded_ghosts_are_never_read(name, variant):
     p = Pair(cfg, lv, f)
     p.g.debug_poison()
     for _ in range(2):
-        p.o.vcycle(1)
+        p.ocycle()
         p.g.vcycle(1)
     u = p.solution()
     assert np.isfinite(u).all()

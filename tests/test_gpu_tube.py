@@ -16,7 +16,7 @@ def test_tube_small_parity(order):
     for comp in (0, 1):
         p = Pair(cfg, lv, f3[comp])
         for _ in range(3):
-            p.o.vcycle(1)
+            p.ocycle()
             p.g.vcycle(1)
         assert rel_err(p.solution(), p.o.get_solution()) < 1e-9
 

@@ -44,7 +44,7 @@ def test_vcycle_parity_variants(name, variant, order):
     cfg, lv, f = _with(name, variant, order)
     p = Pair(cfg, lv, f)
     for c in range(2):
-        p.o.vcycle(1)
+        p.ocycle()
         p.g.vcycle(1)
         e = rel_err(p.solution(), p.o.get_solution())
         assert e < CYCLE_TOL, (name, variant, c, e)
@@ -121,7 +121,7 @@ def test_large_level_parity(name, variant):
     p = Pair(cfg, lv, f)
     assert p.g.level_info(len(p.o.levels) - 1)["nreal"] >= 148
     for c in range(2):
-        p.o.vcycle(1)
+        p.ocycle()
         p.g.vcycle(1)
         e = rel_err(p.solution(), p.o.get_solution())
         assert e < CYCLE_TOL, (name, c, e)
@@ -135,7 +135,7 @@ def test_cfg5_shaped_variants(variant):
     cfg, lv, f = _with("cfg5_small", variant)
     p = Pair(cfg, lv, f)
     for c in range(3):
-        p.o.vcycle(1)
+        p.ocycle()
         p.g.vcycle(1)
         e = rel_err(p.solution(), p.o.get_solution())
         assert e < CYCLE_TOL, (variant, c, e)
