@@ -13,7 +13,10 @@ import pytest
 from tests.gpu_helpers import Pair, rel_err
 from tests.test_gpu_parity import CYCLE_TOL, OP_TOL, _cfg, _prepared
 
-LAYOUTS = ["puu2", "cfg3_64", "ou_uu", "per_adapt", "cfg2_64"]
+# jumps and exterior (U1) ghost blocks: puu2, cfg3_64, per_adapt; ghost-free: cfg2_64.  (The
+# semi-unbounded ou_uu, whose oracle costs ~25 s per test, stays in test_gpu_parity: its
+# symmetric face changes only the coarse solve, not the pencil kernels varied here.)
+LAYOUTS = ["puu2", "cfg3_64", "per_adapt", "cfg2_64"]
 VARIANTS = [dict(pencil_blocks=1, zsplit=1), dict(pencil_blocks=1, zsplit=2), dict(pencil_blocks=2),
             dict(pencil_blocks=4), dict(pencil_blocks=2, fuse=1), dict(pencil_blocks=2, staging=1),
             dict(ghost_kernel=1), dict(ghost_kernel=2)]
@@ -62,7 +65,7 @@ def _prep(name, variant, order):
         T._cfg = orig
 
 
-OP_CASES = [(n, v, 4) for n in ("puu2", "cfg3_64", "ou_uu") for v in VARIANTS] + \
+OP_CASES = [(n, v, 4) for n in ("puu2", "cfg3_64", "per_adapt") for v in VARIANTS] + \
            [("cfg3_64", v, 6) for v in VARIANTS[1:4]]
 
 

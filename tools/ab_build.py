@@ -48,7 +48,7 @@ def main():
         if p.wait() != 0:
             raise SystemExit("compile failed")
     subprocess.run([B.NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", os.path.join(out, "libmg.so")]
-                   + objs + ["-lcufft"], check=True)
+                   + objs + ["-lcufft", "-lcublas"], check=True)
     for o in objs:
         os.remove(o)
     print(os.path.join(out, "libmg.so"))
