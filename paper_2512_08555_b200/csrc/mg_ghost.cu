@@ -6,11 +6,15 @@
 // midpoint weights on coarse (J_d-1)/2 - I/2 + 1 … (J_d-1)/2 + I/2, I = M + 2.
 //
 // The per-node form costs I^3 = 216 scattered coarse reads for an odd-odd-odd node.
-// Here one CTA handles one ghost box (a box of needed nodes of one ghost block; the
-// host splits every block's needed nodes into disjoint thin boxes): it stages the coarse support of the box in shared memory once and
-// applies the rule separably, x then y then z — the same nesting and summation
-// order as the per-node definition (Σ_z w_z Σ_y w_y Σ_x w_x W), so results are
-// identical to it, with ~3I multiply-adds per node.
+// The host splits every ghost block's needed nodes into disjoint boxes, and two kernels
+// apply the rule separably:
+//   k_c2f_box:  one CTA per box; stages the box's coarse support in shared memory once
+//               and applies the rule x, then y, then z — the per-node definition's
+//               nesting and summation order (Σ_z w_z Σ_y w_y Σ_x w_x W), ~3I
+//               multiply-adds per node;
+//   k_c2f_thin: one warp per box <= 2 nodes thick along some axis (the 1-thick face,
+//               edge and corner layers of the distance-1 halo), thin axis first, no
+//               staging and no CTA barriers (used on levels with many such boxes).
 #include <cuda_runtime.h>
 
 #include <cstdint>
