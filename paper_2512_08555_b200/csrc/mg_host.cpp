@@ -104,6 +104,7 @@ struct Level {
   std::vector<uint32_t> nbr_real, nbr_ext;
   bool has_ext_ghosts = false;  // some real block has a ghost neighbour beyond an unbounded face
   std::vector<uint8_t> covmask, c2f_ext;
+  int64_t n_c2f = 0;  // needed boundary-ghost nodes (the per-node lists c2f_* are kept for level 0 only)
   int bmap_lo[3] = {0, 0, 0}, bmap_n[3] = {1, 1, 1};
   // device
   double* u[2] = {nullptr, nullptr};
@@ -508,6 +509,31 @@ void need_node(mg_handle* h, Level& l, int Jx, int Jy, int Jz) {
   l.need[g][loc >> 6] |= 1ull << (loc & 63);
 }
 
+// is_real_node with a one-entry block cache (setup loops walk neighbouring nodes, which
+// mostly fall in the block of the previous lookup)
+struct RealNodeCache {
+  const mg_handle* h;
+  const Level* l;
+  int bx = INT32_MIN, by = 0, bz = 0, idx = -1;
+  bool operator()(int Jx, int Jy, int Jz, int* flat) {
+    int J[3] = {Jx, Jy, Jz};
+    for (int a = 0; a < 3; ++a) {
+      if (h->per[a]) J[a] = ((J[a] % l->N[a]) + l->N[a]) % l->N[a];
+      else if (J[a] < 0 || J[a] >= l->N[a]) return false;
+    }
+    const int cx = J[0] / l->B, cy = J[1] / l->B, cz = J[2] / l->B;
+    if (cx != bx || cy != by || cz != bz) {
+      bx = cx;
+      by = cy;
+      bz = cz;
+      idx = l->find(cx, cy, cz);
+    }
+    if (idx < 0 || idx >= l->nreal) return false;
+    if (flat) *flat = idx * l->B3 + ((J[2] - cz * l->B) * l->B + (J[1] - cy * l->B)) * l->B + (J[0] - cx * l->B);
+    return true;
+  }
+};
+
 bool is_real_node(const mg_handle* h, const Level& l, int Jx, int Jy, int Jz, int* flat) {
   int J[3] = {Jx, Jy, Jz};
   for (int a = 0; a < 3; ++a) {
@@ -551,10 +577,16 @@ void build_ghosts(mg_handle* h) {
         if (idx >= 0 && idx < l.nreal) continue;
         const int lo[3] = {dx < 0 ? l.B - g : 0, dy < 0 ? l.B - g : 0, dz < 0 ? l.B - g : 0};
         const int hi[3] = {dx > 0 ? g : l.B, dy > 0 ? g : l.B, dz > 0 ? g : l.B};
+        // the slab lies in one (ghost) block: mark it there (need_node per node, batched)
+        need_node(h, l, (c[0] + dx) * l.B + lo[0], (c[1] + dy) * l.B + lo[1], (c[2] + dz) * l.B + lo[2]);
+        const int gidx = l.find(nc[0], nc[1], nc[2]) - l.nreal;
+        auto& bits = l.need[gidx];
         for (int z = lo[2]; z < hi[2]; ++z)
           for (int y = lo[1]; y < hi[1]; ++y)
-            for (int x = lo[0]; x < hi[0]; ++x)
-              need_node(h, l, (c[0] + dx) * l.B + x, (c[1] + dy) * l.B + y, (c[2] + dz) * l.B + z);
+            for (int x = lo[0]; x < hi[0]; ++x) {
+              const int loc = (z * l.B + y) * l.B + x;
+              bits[loc >> 6] |= 1ull << (loc & 63);
+            }
       }
     }
     if (m == 0) {
@@ -564,7 +596,9 @@ void build_ghosts(mg_handle* h) {
     }
     // list the needed ghost nodes; for m >= 1 derive the c2f taps on level m-1
     Level* C = m > 0 ? &h->L[m - 1] : nullptr;
-    std::unordered_set<int64_t> injset;
+    std::vector<uint8_t> injected(m > 0 ? (size_t)C->nreal * C->B3 : 0, 0);  // f2c entries listed
+    RealNodeCache ctap{h, C}, cinj{h, C}, finj{h, &l};
+    l.n_c2f = 0;
     for (int gi = 0; gi < l.nghost; ++gi) {
       const auto c = l.coords[l.nreal + gi];
       int bb_lo[3] = {1 << 30, 1 << 30, 1 << 30}, bb_hi[3] = {-(1 << 30), -(1 << 30), -(1 << 30)};
@@ -582,9 +616,12 @@ void build_ghosts(mg_handle* h) {
             if (!h->per[a] && (J[a] < -h->GE || J[a] >= l.N[a] + h->GE))
               throw MgError(MG_ERR_LAYOUT_GHOST, "exterior ghost beyond the coarse-solve band");
         }
-        l.c2f_dst.push_back((l.nreal + gi) * l.B3 + loc);
-        for (int a = 0; a < 3; ++a) l.c2f_J.push_back(J[a]);
-        l.c2f_ext.push_back(ext ? 1 : 0);
+        ++l.n_c2f;
+        if (m == 0) {  // the coarse solve scatters its exterior band to these nodes
+          l.c2f_dst.push_back((l.nreal + gi) * l.B3 + loc);
+          for (int a = 0; a < 3; ++a) l.c2f_J.push_back(J[a]);
+          l.c2f_ext.push_back(ext ? 1 : 0);
+        }
         for (int a = 0; a < 3; ++a) {
           bb_lo[a] = std::min(bb_lo[a], J[a]);
           bb_hi[a] = std::max(bb_hi[a], J[a]);
@@ -604,7 +641,7 @@ void build_ghosts(mg_handle* h) {
           } else {
             for (int k = 0; k < 8; ++k) {
               const int x = (k & 1) ? t1[0] : t0[0], y = (k & 2) ? t1[1] : t0[1], z = (k & 4) ? t1[2] : t0[2];
-              if (!is_real_node(h, *C, x, y, z, nullptr))
+              if (!ctap(x, y, z, nullptr))
                 throw MgError(MG_ERR_LAYOUT_GHOST, "ghost interpolation stencil leaves the coarse level (2:1?)");
             }
           }
@@ -616,12 +653,12 @@ void build_ghosts(mg_handle* h) {
           for (int y = fdiv(bb_lo[1], 2) - h->I / 2; y <= fdiv(bb_hi[1], 2) + h->I / 2; ++y)
             for (int x = fdiv(bb_lo[0], 2) - h->I / 2; x <= fdiv(bb_hi[0], 2) + h->I / 2; ++x) {
               int cflat, fflat;
-              if (!is_real_node(h, *C, x, y, z, &cflat)) continue;
-              if (!is_real_node(h, l, 2 * x, 2 * y, 2 * z, &fflat)) continue;
-              if (injset.insert(cflat).second) {
-                l.inj_dst.push_back(cflat);
-                l.inj_src.push_back(fflat);
-              }
+              if (!cinj(x, y, z, &cflat)) continue;
+              if (injected[cflat]) continue;
+              if (!finj(2 * x, 2 * y, 2 * z, &fflat)) continue;
+              injected[cflat] = 1;
+              l.inj_dst.push_back(cflat);
+              l.inj_src.push_back(fflat);
             }
       }
     }
@@ -779,20 +816,26 @@ void build_ghost_boxes(mg_handle* h) {
         szA = std::max(szA, std::max(nc[0] * nc[1] * nc[2], nf[0] * nf[1] * nc[2]));
         szB = std::max(szB, nf[0] * nc[1] * nc[2]);
       };
-      // cut points per axis
+      // cut points per axis: planes k where the need mask differs from plane k-1 anywhere
+      std::vector<uint8_t> dif(3 * B, 0);
+      for (int z = 0; z < B; ++z)
+        for (int y = 0; y < B; ++y) {
+          const uint8_t* row = &nd[(z * B + y) * B];
+          for (int x = 1; x < B; ++x) dif[x] |= row[x] != row[x - 1];
+          if (y > 0) {
+            const uint8_t* prev = row - B;
+            for (int x = 0; x < B; ++x) dif[B + y] |= row[x] != prev[x];
+          }
+          if (z > 0) {
+            const uint8_t* prev = row - B * B;
+            for (int x = 0; x < B; ++x) dif[2 * B + z] |= row[x] != prev[x];
+          }
+        }
       std::vector<int> cut[3];
       for (int a = 0; a < 3; ++a) {
         cut[a].push_back(0);
-        for (int k = 1; k < B; ++k) {
-          bool diff = false;
-          for (int i = 0; i < B && !diff; ++i)
-            for (int j = 0; j < B && !diff; ++j) {
-              const int p[3][3] = {{k, i, j}, {i, k, j}, {i, j, k}};
-              const int q[3][3] = {{k - 1, i, j}, {i, k - 1, j}, {i, j, k - 1}};
-              diff = at(p[a][0], p[a][1], p[a][2]) != at(q[a][0], q[a][1], q[a][2]);
-            }
-          if (diff) cut[a].push_back(k);
-        }
+        for (int k = 1; k < B; ++k)
+          if (dif[a * B + k]) cut[a].push_back(k);
         cut[a].push_back(B);
       }
       const int n0 = (int)cut[0].size() - 1, n1 = (int)cut[1].size() - 1, n2 = (int)cut[2].size() - 1;
@@ -1211,7 +1254,7 @@ void refresh(mg_handle* h, int m) {
   for (int j = lo; j <= m; ++j) c2f_boxes(h, j, h->L[j].u[h->L[j].cur], h->L[j - 1].u[h->L[j - 1].cur], false);
 }
 
-bool has_ghosts(mg_handle* h, int m) { return m > 0 && !h->L[m].c2f_dst.empty(); }
+bool has_ghosts(mg_handle* h, int m) { return m > 0 && h->L[m].n_c2f > 0; }
 
 // r = f - Δu on all level-m nodes (ghosts already refreshed)
 void residual_kernel(mg_handle* h, int m) {
@@ -1786,7 +1829,7 @@ int mg_level_info(mg_handle* h, int level, int64_t* info) {
   int64_t nleaf_blocks = 0;
   for (int i = 0; i < l.nreal; ++i) nleaf_blocks += l.covmask[i] == 0;
   const int64_t v[10] = {l.B, l.nreal, l.nghost, l.N[0], l.N[1], l.N[2], l.amr,
-                         (int64_t)l.c2f_dst.size(), (int64_t)l.inj_dst.size(), nleaf_blocks};
+                         l.n_c2f, (int64_t)l.inj_dst.size(), nleaf_blocks};
   std::memcpy(info, v, sizeof(v));
   return MG_OK;
 }
