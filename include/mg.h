@@ -110,9 +110,12 @@ typedef struct mg_desc {
                                 returns leaf arrays [ncomp][n_leaf][B][B][B], one V-cycle and every
                                 kernel launch cover all components (gridDim.y = ncomp), the norms
                                 are the max over components, the coarse solve is one batched FFT */
-  int32_t coarse_pruning;    /* x-periodic, y/z-unbounded coarse solve: 0 auto (1-D transforms that
+  int32_t coarse_pruning;    /* x-periodic, y/z-unbounded coarse solve: 0 auto (1-D cuFFT passes that
                                 skip the zero half of the padded source and unread outputs),
-                                1 the plain 3-D transform of the padded lattice */
+                                1 the plain 3-D transform of the padded lattice (cuFFT),
+                                2 the pruned solve with the y and z transforms, the multiplier and
+                                the window as three fused kernels of mixed-radix FFTs in shared
+                                memory (mg_fft.cu; measured slower than 0); else MG_ERR_ARG */
   int32_t staging;           /* plane tiles of the RB sweep: 0 cp.async ring (default, the
                                 fastest measured), 1 TMA tensor copies (cp.async.bulk.tensor, 9
                                 boxes per field and plane) into an mbarrier ring; measured 2.5x

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmg.so")
-SOURCES = ["mg_kernels.cu", "mg_pencil.cu", "mg_ghost.cu", "mg_adapt.cu", "mg_host.cpp", "mg_lgf.cpp", "mg_adapt.cpp"]
+SOURCES = ["mg_kernels.cu", "mg_pencil.cu", "mg_ghost.cu", "mg_fft.cu", "mg_adapt.cu", "mg_host.cpp", "mg_lgf.cpp",
+           "mg_adapt.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-I" + os.path.join(ROOT, "include")] + os.environ.get("MG_NVCC_EXTRA", "").split()

@@ -170,6 +170,10 @@ struct mg_handle {
   bool pruned = false;
   cufftHandle pr_xf = 0, pr_y = 0, pr_z = 0, pr_y1 = 0, pr_y2 = 0, pr_xb = 0;
   double *pr_X = nullptr, *pr_R = nullptr, *pr_mult = nullptr;
+  // fused y / z transforms of the pruned solve (mg_fft.cu): plans and device twiddles
+  FFTPlan fp_y, fp_z;
+  double *d_twy = nullptr, *d_twz = nullptr;
+  bool fused_fft = false;
   void *pr_C1 = nullptr, *pr_C2 = nullptr, *pr_C3 = nullptr;
   int pr_W[3] = {0, 0, 0};  // window (x periodic: N; y, z: N + 2 GE)
   std::vector<cufftHandle*> plans() {
@@ -325,7 +329,7 @@ void validate_and_build(mg_handle* h) {
     if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
     if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
-    if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 1)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..1");
+    if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 2)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..2");
     if (a == 0 && (d.ghost_kernel < 0 || d.ghost_kernel > 2)) throw MgError(MG_ERR_ARG, "ghost_kernel must be 0..2");
     if (a == 0 && (d.zsplit < 0 || d.zsplit > 2 || d.fuse < 0 || d.fuse > 1 || d.staging < 0 || d.staging > 1))
       throw MgError(MG_ERR_ARG, "zsplit must be 0..2, fuse and staging 0..1");
@@ -1162,6 +1166,15 @@ void setup_coarse(mg_handle* h) {
     CUFFT_OK(cufftPlanMany(&h->pr_z, 1, &nz, &emb, Hx * Py, 1, &emb, Hx * Py, 1, CUFFT_Z2Z, Hx * Py));
     for (cufftHandle* p : {&h->pr_xf, &h->pr_xb, &h->pr_y, &h->pr_y1, &h->pr_y2, &h->pr_z})
       CUFFT_OK(cufftSetStream(*p, h->s));
+    // fused y / z transforms (mg_desc.coarse_pruning 2; measured slower than the cuFFT
+    // passes of the default)
+    std::vector<double> twy, twz;
+    h->fused_fft = h->d.coarse_pruning == 2 && fft_plan(Py, h->fp_y, twy) && fft_plan(Pz, h->fp_z, twz) &&
+                   Py <= 880 && Pz <= 880;  // mg_fft.cu FT_MAXN
+    if (h->fused_fft) {
+      h->d_twy = dev_upload(twy);
+      h->d_twz = dev_upload(twz);
+    }
   }
   // level-0 exterior f ghosts beyond symmetric low faces: signed mirror copies of real
   // level-0 nodes (f := 0 beyond unbounded faces, Z16; reading S1)
@@ -1355,21 +1368,29 @@ void coarse_solve_pruned(mg_handle* h) {
   const int N[3] = {Nx, Ny, Nz}, zero[3] = {0, 0, 0};
   launch_coarse_gather(c, h->pr_X, N, zero, zero, zero, zero, h->s);
   CUFFT_OK(cufftExecD2Z(h->pr_xf, h->pr_X, (cufftDoubleComplex*)h->pr_C1));
-  launch_spec_pad_y(h->pr_C1, h->pr_C2, Nz, Ny, Hx, Py, Pz, h->nc, h->s);
-  const size_t plane = (size_t)Hx * Py, comp = (size_t)Pz * plane;
-  auto C2 = [&](int cc, int z) { return (cufftDoubleComplex*)h->pr_C2 + cc * comp + (size_t)z * plane; };
-  for (int cc = 0; cc < h->nc; ++cc) {
-    CUDA_OK(cudaMemsetAsync(C2(cc, Nz), 0, (size_t)(Pz - Nz) * plane * sizeof(cufftDoubleComplex), h->s));
-    CUFFT_OK(cufftExecZ2Z(h->pr_y, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
-    CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
+  if (h->fused_fft) {
+    // y FFT (zero padding implicit), z FFT x multiplier x inverse z FFT (window rows),
+    // inverse y FFT + window, each one kernel (mg_fft.cu)
+    launch_fft_y_fwd(h->pr_C1, h->pr_C2, Ny, Nz, Hx, Pz, h->fp_y, h->d_twy, h->nc, h->s);
+    launch_fft_z_conv(h->pr_C2, h->pr_mult, Hx * Py, Nz, GE, h->fp_z, h->d_twz, h->nc, h->s);
+    launch_fft_y_inv(h->pr_C2, h->pr_C3, Hx, Pz, h->pr_W[1], h->pr_W[2], GE, h->fp_y, h->d_twy, h->nc, h->s);
+  } else {
+    launch_spec_pad_y(h->pr_C1, h->pr_C2, Nz, Ny, Hx, Py, Pz, h->nc, h->s);
+    const size_t plane = (size_t)Hx * Py, comp = (size_t)Pz * plane;
+    auto C2 = [&](int cc, int z) { return (cufftDoubleComplex*)h->pr_C2 + cc * comp + (size_t)z * plane; };
+    for (int cc = 0; cc < h->nc; ++cc) {
+      CUDA_OK(cudaMemsetAsync(C2(cc, Nz), 0, (size_t)(Pz - Nz) * plane * sizeof(cufftDoubleComplex), h->s));
+      CUFFT_OK(cufftExecZ2Z(h->pr_y, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
+      CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_FORWARD));
+    }
+    launch_coarse_mul_table(h->pr_C2, h->pr_mult, (int64_t)comp, h->nc, h->s);
+    for (int cc = 0; cc < h->nc; ++cc) {
+      CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
+      CUFFT_OK(cufftExecZ2Z(h->pr_y1, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
+      CUFFT_OK(cufftExecZ2Z(h->pr_y2, C2(cc, Pz - GE), C2(cc, Pz - GE), CUFFT_INVERSE));
+    }
+    launch_spec_window(h->pr_C2, h->pr_C3, h->pr_W[2], h->pr_W[1], Hx, Py, Pz, GE, h->nc, h->s);
   }
-  launch_coarse_mul_table(h->pr_C2, h->pr_mult, (int64_t)comp, h->nc, h->s);
-  for (int cc = 0; cc < h->nc; ++cc) {
-    CUFFT_OK(cufftExecZ2Z(h->pr_z, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
-    CUFFT_OK(cufftExecZ2Z(h->pr_y1, C2(cc, 0), C2(cc, 0), CUFFT_INVERSE));
-    CUFFT_OK(cufftExecZ2Z(h->pr_y2, C2(cc, Pz - GE), C2(cc, Pz - GE), CUFFT_INVERSE));
-  }
-  launch_spec_window(h->pr_C2, h->pr_C3, h->pr_W[2], h->pr_W[1], Hx, Py, Pz, GE, h->nc, h->s);
   CUFFT_OK(cufftExecZ2D(h->pr_xb, (cufftDoubleComplex*)h->pr_C3, h->pr_R));
   const int off[3] = {0, GE, GE};
   launch_coarse_scatter(c, h->pr_R, h->pr_W, off, c2f_list(h->L[0]), h->s);
@@ -1614,7 +1635,8 @@ void destroy(mg_handle* h) {
     if (p) cudaFree(p);
   for (cufftHandle* p : h->plans())
     if (*p) cufftDestroy(*p);
-  for (void* p : {(void*)h->pr_X, (void*)h->pr_R, (void*)h->pr_mult, h->pr_C1, h->pr_C2, h->pr_C3})
+  for (void* p : {(void*)h->pr_X, (void*)h->pr_R, (void*)h->pr_mult, h->pr_C1, h->pr_C2, h->pr_C3, (void*)h->d_twy,
+                  (void*)h->d_twz})
     if (p) cudaFree(p);
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   delete h;

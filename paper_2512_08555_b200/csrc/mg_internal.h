@@ -2,6 +2,7 @@
 // (mg_host.cpp) and the sm_100a kernels (mg_kernels.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -107,6 +108,21 @@ void prepare_pencil_kernels();
 // coarse block index of each of the 3 x 3 x 3 block slots the box's taps meet
 // (slot sx + 3 sy + 9 sz; -1 = none), 1 unused
 constexpr int GBOX_REC = 40;
+// mixed-radix FFT plan of the fused pruned coarse solve (mg_fft.cu): radices r[f], the
+// product p[f] of the earlier ones, twiddle offset toff[f] (complex entries)
+struct FFTPlan {
+  static constexpr int MAXF = 12;
+  int n = 0, nf = 0;
+  int r[MAXF] = {}, p[MAXF] = {}, toff[MAXF] = {};
+};
+bool fft_plan(int n, FFTPlan& P, std::vector<double>& tw);
+void prepare_fft_kernels();
+void launch_fft_y_fwd(const void* c1, void* c2, int Ny, int Nz, int Hx, int Pz, const FFTPlan& py, const double* twy,
+                      int nc, cudaStream_t s);
+void launch_fft_z_conv(void* c2, const double* mult, int Q, int Nz, int GE, const FFTPlan& pz, const double* twz,
+                       int nc, cudaStream_t s);
+void launch_fft_y_inv(const void* c2, void* c3, int Hx, int Pz, int Wy, int Wz, int GE, const FFTPlan& py,
+                      const double* twy, int nc, cudaStream_t s);
 size_t c2f_box_smem_max(int I);
 void launch_c2f_thin(const LevelView& fine, const LevelView& coarse, const int32_t* boxes, int nbox, double* fine_field,
                      const double* coarse_field, int I, bool ext_zero, cudaStream_t s);

@@ -472,6 +472,7 @@ static void smooth_dispatch(const LevelView& L, int mode, double omega, bool res
 void prepare_kernels() {
   prepare_pencil_kernels();
   prepare_ghost_kernels();
+  prepare_fft_kernels();
   prepare_b<16, 2>(); prepare_b<16, 4>(); prepare_b<16, 6>();
   prepare_b<8, 2>(); prepare_b<8, 4>(); prepare_b<8, 6>();
   prepare_b<4, 2>(); prepare_b<4, 4>(); prepare_b<4, 6>();

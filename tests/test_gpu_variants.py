@@ -167,10 +167,11 @@ def test_tma_and_cpasync_staging_bitwise(name):
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["puu1", "puu2", "cfg4_small", "cfg5_small"])
 def test_pruned_coarse_solve_matches_3d_and_oracle(name):
-    """The x-periodic, y/z-unbounded coarse solve through 1-D transforms (default) equals
-    the oracle at the per-operator tolerance on the level-0 nodes, and its exterior band
-    (read by the level-0 leaf residual) gives the oracle's composite residual; the plain
-    padded 3-D transform (mg_desc.coarse_pruning = 1) gives the same band."""
+    """The x-periodic, y/z-unbounded coarse solve through 1-D cuFFT transforms (default)
+    equals the oracle at the per-operator tolerance on the level-0 nodes, and its exterior
+    band (read by the level-0 leaf residual) gives the oracle's composite residual; the
+    plain padded 3-D transform (mg_desc.coarse_pruning = 1) and the fused shared-memory FFT
+    kernels of mg_fft.cu (2) give the same level-0 values and band."""
     import torch
 
     from paper_2512_08555_b200 import Solver
@@ -185,12 +186,14 @@ def test_pruned_coarse_solve_matches_3d_and_oracle(name):
     ro, rg = p.o.residual_norm()[0], p.g.residual_norm()[0]
     assert abs(rg - ro) <= 1e-10 * max(1.0, np.abs(c.f).max())
     cfg, lv, f = _cfg(name)
-    cfg = dict(cfg)
-    cfg["coarse_pruning"] = 1
-    q = Solver(cfg, lv)
-    q.set_rhs(torch.from_numpy(f).cuda())
-    for m in range(len(p.o.levels)):          # the same state as p's GPU side
-        for fld in (0, 1, 3):
-            q.debug_field(fld, m, p.g.debug_field(fld, m))
-    q.debug_apply("coarse_solve", 0)
-    assert abs(q.residual_norm()[0] - rg) <= 1e-12 * max(1.0, rg)
+    for mode in (1, 2):   # the padded 3-D transform; the fused FFT kernels
+        c2 = dict(cfg)
+        c2["coarse_pruning"] = mode
+        q = Solver(c2, lv)
+        q.set_rhs(torch.from_numpy(f).cuda())
+        for m in range(len(p.o.levels)):          # the same state as p's GPU side
+            for fld in (0, 1, 3):
+                q.debug_field(fld, m, p.g.debug_field(fld, m))
+        q.debug_apply("coarse_solve", 0)
+        assert abs(q.residual_norm()[0] - rg) <= 1e-12 * max(1.0, rg), mode
+        assert rel_err(q.debug_field(0, 0).cpu().numpy(), p.g.debug_field(0, 0).cpu().numpy()) < 1e-13, mode
