@@ -53,27 +53,74 @@ def peak_hbm():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region:
+    an NVML thread polling every 2 ms between __enter__ and __exit__ (the main thread
+    waits in cudaEventSynchronize, which releases the GIL); nvidia-smi -lms 50 when NVML
+    is unavailable."""
 
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
-        self.p = None
         self.index = index
+        self.p = None
+        self.thread = None
+        self.sm, self.mx, self.reasons, self.source = [], None, set(), None
+        self.out = ""
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            return pynvml.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(self.index).uuid))
+        except Exception:
+            return pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            h = self._nvml_handle()
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self.stop = threading.Event()
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.sm.append(float(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)))
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.reasons.update(n for n, bit in bits.items() if r & bit)
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.source = "nvml, 2 ms polling during the timed region"
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
                                        "--format=csv,noheader,nounits", "-lms", "50"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.source = "nvidia-smi -lms 50"
         except Exception:
             self.p = None
         time.sleep(0.15)
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=1)
+            return
         if self.p is not None:
             time.sleep(0.1)
             self.p.terminate()
@@ -81,24 +128,23 @@ class ClockSampler:
                 self.out, _ = self.p.communicate(timeout=5)
             except Exception:
                 self.p.kill()
-
-    def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in (self.out or "").strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                self.sm.append(float(parts[0]))
+                self.mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:]):
+            for n, v in zip(self.NAMES, parts[2:]):
                 if v.lower() in ("active", "1"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                    self.reasons.add(n)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "sm_mhz_min": min(self.sm) if self.sm else None, "source": self.source}
 
 
 def max_over_ranks(x, dist, device):
@@ -325,23 +371,38 @@ def measure(S, cfg, args, dist, dev, ws, local, with_clocks=True):
         S.vcycle(1)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clk = ClockSampler(local) if with_clocks else None
+
+    def timed_region():
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(local) if with_clocks else None
+        if clk:
+            clk.__enter__()
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.vcycle(1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__()
+        if dist:
+            dist.barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, dev), clk
+
+    ms, clk = timed_region()
+    # timing rule: a region that saw a hardware / thermal slowdown, or SM clocks well
+    # below max with no reason, is rejected and measured once more
+    remeasured, flag = None, 0.0
     if clk:
-        clk.__enter__()
-    e0.record(stream)
-    for _ in range(args.steps):
-        S.vcycle(1)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    if clk:
-        clk.__exit__()
-    if dist:
-        dist.barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, dev)
+        c = clk.summary()
+        bad = [r for r in c["reasons"] if r != "sw_power_cap"]
+        low = c["sm_mhz"] is not None and c["sm_max_mhz"] and not c["reasons"] and c["sm_mhz"] < 0.85 * c["sm_max_mhz"]
+        flag = 1.0 if (bad or low) else 0.0
+    if max_over_ranks(flag, dist, dev) > 0:  # every rank re-runs the region (barriers inside)
+        remeasured = {"first_ms_per_step": ms, "first_clocks": clk.summary() if clk else None}
+        ms, clk = timed_region()
 
     # per-stage live timing (CUDA events on the library's stream around every stage)
     S.use_graph(False)
@@ -374,7 +435,7 @@ def measure(S, cfg, args, dist, dev, ws, local, with_clocks=True):
     eta = cfg["eta1"] + cfg["eta2"]
     rl_stage_ms = smoothed * (24 * eta + 52) / (peak * 1e9) * 1e3
     rl_fused_ms = smoothed * (24 * eta + 4) / (peak * 1e9) * 1e3
-    return dict(ms=ms, clocks=clk.summary() if clk else None, levels=levels, kernels=kernels, dom=(st, lv, K),
+    return dict(ms=ms, clocks=dict(clk.summary(), remeasured=remeasured) if clk else None, levels=levels, kernels=kernels, dom=(st, lv, K),
                 stage_ms=stage_ms, coarse_ms=coarse_ms, launches_per_cycle=launches_per_cycle,
                 rl_stage_ms=rl_stage_ms, rl_fused_ms=rl_fused_ms, peak=peak, peak_src=peak_src)
 
