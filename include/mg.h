@@ -100,7 +100,7 @@ typedef struct mg_desc {
    * suite runs every code path the automatic choice takes at full size.  Results are
    * identical up to rounding order for every setting. */
   int32_t pencil_blocks;     /* blocks per pencil of the z-marching kernels on B = 16 levels:
-                                0 auto (by level size), 1, 2 or 4; else MG_ERR_ARG */
+                                0 auto (by level size), 1, 2, 3 or 4; else MG_ERR_ARG */
   int32_t zsplit;            /* RB sweep of 1-block pencils split into two 8-plane z-parts:
                                 0 auto (levels with fewer blocks than SMs), 1 never, 2 always */
   int32_t fuse;              /* 0 auto: fused pencil kernels where eligible (last pre-sweep +

@@ -328,8 +328,8 @@ void validate_and_build(mg_handle* h) {
   if (d.eta1 < 0 || d.eta2 < 0 || !(d.h0 > 0)) throw MgError(MG_ERR_ARG, "bad eta/h0");
   for (int a = 0; a < 3; ++a) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
-    if (a == 0 && !(d.pencil_blocks == 0 || d.pencil_blocks == 1 || d.pencil_blocks == 2 || d.pencil_blocks == 4))
-      throw MgError(MG_ERR_ARG, "pencil_blocks must be 0, 1, 2 or 4");
+    if (a == 0 && !(d.pencil_blocks >= 0 && d.pencil_blocks <= 4))
+      throw MgError(MG_ERR_ARG, "pencil_blocks must be 0..4");
     if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
     if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 2)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..2");
     if (a == 0 && (d.ghost_kernel < 0 || d.ghost_kernel > 2)) throw MgError(MG_ERR_ARG, "ghost_kernel must be 0..2");
@@ -897,13 +897,12 @@ void build_ghost_boxes(mg_handle* h) {
 // `lmax` blocks, longest first.  The z-marching kernels (mg_pencil.cu) walk one
 // pencil per CTA; halos above/below a pencil come through the neighbour tables.
 void build_pencils(mg_handle* h) {
-  // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs.
-  // A level with fewer blocks than ~2 resident waves (#SM x 4 CTAs) uses 1-block
-  // pencils, larger levels 2; ghost-free levels of >= 4 waves whose z-runs average >= 8
-  // blocks 4 — cfg2 256^3 on B200 after the sweep rewrite: sweep 96.9 -> 90.7 us,
-  // V-cycle 0.715 -> 0.694 ms; levels with ghost blocks (cfg3 and cfg5 finest: 1.30 ->
-  // 1.35 ms and 6.53 -> 6.69 ms with 4) stay at 2.  mg_desc.pencil_blocks forces one
-  // length (tests), mg_desc.zsplit the z-split of small levels.
+  // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs
+  // (rule below).  Ghost-free levels of >= 4 waves whose z-runs average >= 8 blocks use 4
+  // — cfg2 256^3 on B200 after the sweep rewrite: sweep 96.9 -> 90.7 us, V-cycle 0.715 ->
+  // 0.694 ms; on levels with ghost blocks 4 was slower (cfg3 and cfg5 finest: 1.30 ->
+  // 1.35 ms and 6.53 -> 6.69 ms).  mg_desc.pencil_blocks forces one length (tests),
+  // mg_desc.zsplit the z-split of small levels.
   const int lmax_force = h->d.pencil_blocks;
   const int nsm = h->nsm;
   for (auto& l : h->L) {
@@ -915,8 +914,15 @@ void build_pencils(mg_handle* h) {
       if (a == 0 || cols[a][0] != cols[a - 1][0] || cols[a][1] != cols[a - 1][1] || cols[a][2] != cols[a - 1][2] + 1)
         ++nruns;
     const bool long_runs = nruns > 0 && l.nreal >= 8 * nruns && l.nghost == 0;
+    // automatic length by waves of 1-block pencils (W = nreal / (4 #SM)), measured on cfg5's
+    // levels (graph V-cycle 5.84 -> 5.78 ms): W < 1.75: 1; 1.75 <= W < 8: 2 (level 1,
+    // 1152 blocks: sweep 38.7 -> 34.2 us); 8 <= W < 24: 3 (level 3, 6640 blocks: sweep
+    // 163.7 -> 154.3 us, residual + restriction 154.8 -> 147.9 us); W >= 24: 2 (level 4,
+    // 23144 blocks: 3-block pencils 515 vs 506 us); ghost-free levels of >= 4 waves with
+    // long z-runs: 4
+    const double W = (double)l.nreal / (4.0 * nsm);
     const int lmax = lmax_force ? lmax_force
-                                : (l.nreal >= 4 * nsm * 4 && long_runs ? 4 : (l.nreal >= 2 * nsm * 4 ? 2 : 1));
+                                : (W >= 4 && long_runs ? 4 : (W >= 8 && W < 24 ? 3 : (W >= 1.75 ? 2 : 1)));
     l.pen_blk.clear();
     l.pen_len.clear();
     l.pen_lmax = lmax;

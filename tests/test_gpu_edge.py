@@ -108,7 +108,7 @@ def test_block_size_8_parity(B):
 def test_variant_controls_rejected():
     d = _base()
     lv = Lay.uniform_leaves(C.domain(d))
-    assert _err_code(_base(pencil_blocks=3), lv) == MG_ERR_ARG
+    assert _err_code(_base(pencil_blocks=5), lv) == MG_ERR_ARG
     assert _err_code(_base(zsplit=3), lv) == MG_ERR_ARG
     assert _err_code(_base(fuse=2), lv) == MG_ERR_ARG
 
