@@ -100,7 +100,8 @@ typedef struct mg_desc {
    * suite runs every code path the automatic choice takes at full size.  Results are
    * identical up to rounding order for every setting. */
   int32_t pencil_blocks;     /* blocks per pencil of the z-marching kernels on B = 16 levels:
-                                0 auto (by level size), 1, 2, 3 or 4; else MG_ERR_ARG */
+                                0 auto (by level size), 1, 2, 3 or 4 (with the wave-tail split
+                                off); else MG_ERR_ARG */
   int32_t zsplit;            /* RB sweep of 1-block pencils split into two 8-plane z-parts:
                                 0 auto (levels with fewer blocks than SMs), 1 never, 2 always */
   int32_t fuse;              /* 0 auto: fused pencil kernels where eligible (last pre-sweep +
@@ -126,6 +127,11 @@ typedef struct mg_desc {
                                 axis interpolated first; every other box one CTA each, x, y, z
                                 passes), 1 every box on the CTA kernel, 2 every thin box on the
                                 warp kernel; else MG_ERR_ARG */
+  int32_t pencil_order;      /* how z-runs of blocks are cut into pencils and launched: 0 auto (2 on
+                                levels of >= 24 waves of 1-block pencils, else 1), 1 balanced chunks,
+                                longest first, 2 chunks cut where the block's z index is a multiple
+                                of the pencil length, launched in z-major order whatever their
+                                length; else MG_ERR_ARG */
 } mg_desc;
 
 /* Validate the layout (nesting, 2:1, unbounded-face rule), build the level

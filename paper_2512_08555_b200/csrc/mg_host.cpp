@@ -330,6 +330,7 @@ void validate_and_build(mg_handle* h) {
     if (d.base_blocks[a] <= 0) throw MgError(MG_ERR_ARG, "bad base_blocks");
     if (a == 0 && !(d.pencil_blocks >= 0 && d.pencil_blocks <= 4))
       throw MgError(MG_ERR_ARG, "pencil_blocks must be 0..4");
+    if (a == 0 && (d.pencil_order < 0 || d.pencil_order > 2)) throw MgError(MG_ERR_ARG, "pencil_order must be 0..2");
     if (a == 0 && (d.ncomp < 0 || d.ncomp > 8)) throw MgError(MG_ERR_ARG, "ncomp must be 0..8 (0 = 1)");
     if (a == 0 && (d.coarse_pruning < 0 || d.coarse_pruning > 2)) throw MgError(MG_ERR_ARG, "coarse_pruning must be 0..2");
     if (a == 0 && (d.ghost_kernel < 0 || d.ghost_kernel > 2)) throw MgError(MG_ERR_ARG, "ghost_kernel must be 0..2");
@@ -900,39 +901,66 @@ void build_pencils(mg_handle* h) {
   // Pencil length: long pencils amortise the 2+2 halo planes, short ones give more CTAs
   // (rule below).  Ghost-free levels of >= 4 waves whose z-runs average >= 8 blocks use 4
   // — cfg2 256^3 on B200 after the sweep rewrite: sweep 96.9 -> 90.7 us, V-cycle 0.715 ->
-  // 0.694 ms; on levels with ghost blocks 4 was slower (cfg3 and cfg5 finest: 1.30 ->
-  // 1.35 ms and 6.53 -> 6.69 ms).  mg_desc.pencil_blocks forces one length (tests),
-  // mg_desc.zsplit the z-split of small levels.
+  // 0.694 ms.  mg_desc.pencil_blocks forces one length and mg_desc.pencil_order the
+  // chunking and launch order (tests), mg_desc.zsplit the z-split of small levels.
   const int lmax_force = h->d.pencil_blocks;
   const int nsm = h->nsm;
+  const int S = 4 * nsm;  // CTA slots: the sweep and the fused residual + restriction run 4 CTAs per SM
+  // makespan of the list schedule of a launch on S slots (cost of a pencil: 16 len + 4 plane steps)
+  auto makespan = [&](const std::vector<int>& lens) {
+    std::priority_queue<long, std::vector<long>, std::greater<long>> q;
+    for (int i = 0; i < S; ++i) q.push(0);
+    long m = 0;
+    for (int L : lens) {
+      const long t = q.top() + 16 * L + 4;
+      q.pop();
+      q.push(t);
+      m = std::max(m, t);
+    }
+    return m;
+  };
   for (auto& l : h->L) {
     std::vector<std::array<int, 4>> cols;  // (bx, by, bz, idx)
     for (int i = 0; i < l.nreal; ++i) cols.push_back({l.coords[i][0], l.coords[i][1], l.coords[i][2], i});
     std::sort(cols.begin(), cols.end());
+    auto run_start = [&](size_t a) {
+      return a == 0 || cols[a][0] != cols[a - 1][0] || cols[a][1] != cols[a - 1][1] || cols[a][2] != cols[a - 1][2] + 1;
+    };
     int nruns = 0;
-    for (size_t a = 0; a < cols.size(); ++a)
-      if (a == 0 || cols[a][0] != cols[a - 1][0] || cols[a][1] != cols[a - 1][1] || cols[a][2] != cols[a - 1][2] + 1)
-        ++nruns;
+    for (size_t a = 0; a < cols.size(); ++a) nruns += run_start(a);
     const bool long_runs = nruns > 0 && l.nreal >= 8 * nruns && l.nghost == 0;
     // automatic length by waves of 1-block pencils (W = nreal / (4 #SM)), measured on cfg5's
     // levels (graph V-cycle 5.84 -> 5.78 ms): W < 1.75: 1; 1.75 <= W < 8: 2 (level 1,
     // 1152 blocks: sweep 38.7 -> 34.2 us); 8 <= W < 24: 3 (level 3, 6640 blocks: sweep
-    // 163.7 -> 154.3 us, residual + restriction 154.8 -> 147.9 us); W >= 24: 2 (level 4,
-    // 23144 blocks: 3-block pencils 515 vs 506 us); ghost-free levels of >= 4 waves with
-    // long z-runs: 4
+    // 163.7 -> 154.3 us, residual + restriction 154.8 -> 147.9 us); ghost-free levels of
+    // >= 4 waves with long z-runs, and every level of W >= 24: 4.
+    // Chunking and order.  "Balanced" (W < 24): a z-run of n blocks is cut into
+    // ceil(n / lmax) nearly equal pencils, launched longest first, then by the z of the
+    // first block and Morton order of (bx, by).  "Aligned" (W >= 24: cfg5 level 4, 23144
+    // blocks): pencils are cut where bz is a multiple of lmax and launched by (bz / lmax,
+    // Morton(bx, by)) whatever their length, so that the CTAs resident together cover the
+    // same z-slab of neighbouring columns and re-read each other's halos from L2 — with
+    // balanced chunks the neighbours of a 4-block pencil start at other z and in other
+    // length classes, and 4-block pencils were slower than 2-block ones (554 vs 506 us);
+    // aligned, they are faster: cfg5 level-4 sweep 510 -> 492 us, fused residual +
+    // restriction 495 -> 472 us (profiles/r02_pencil_aligned_ab.jsonl; lengths 3, 5, 6, 8:
+    // 503, 491, 497, 508 us).
     const double W = (double)l.nreal / (4.0 * nsm);
     const int lmax = lmax_force ? lmax_force
-                                : (W >= 4 && long_runs ? 4 : (W >= 8 && W < 24 ? 3 : (W >= 1.75 ? 2 : 1)));
+                                : ((W >= 4 && long_runs) || W >= 24 ? 4 : (W >= 8 ? 3 : (W >= 1.75 ? 2 : 1)));
+    const bool aligned = h->d.pencil_order ? h->d.pencil_order == 2 : W >= 24;
     l.pen_blk.clear();
     l.pen_len.clear();
     l.pen_lmax = lmax;
     if (l.B != 16) continue;
     std::vector<std::vector<int>> pens;
-    for (size_t a = 0; a < cols.size();) {
+    for (size_t a = 0; aligned && a < cols.size(); ++a) {
+      if (run_start(a) || cols[a][2] % lmax == 0) pens.emplace_back();
+      pens.back().push_back(cols[a][3]);
+    }
+    for (size_t a = 0; !aligned && a < cols.size();) {
       size_t b = a + 1;
-      while (b < cols.size() && cols[b][0] == cols[a][0] && cols[b][1] == cols[a][1] &&
-             cols[b][2] == cols[b - 1][2] + 1)
-        ++b;
+      while (b < cols.size() && !run_start(b)) ++b;
       const int n = (int)(b - a), nchunk = (n + lmax - 1) / lmax;
       for (int c = 0, pos = 0; c < nchunk; ++c) {
         const int len = n / nchunk + (c < n % nchunk ? 1 : 0);
@@ -943,41 +971,26 @@ void build_pencils(mg_handle* h) {
       }
       a = b;
     }
-    // launch order: longest first; then by the z of the first block and Morton order of
-    // (bx, by), so that CTAs resident at the same time are spatial neighbours and re-read
-    // each other's halos from L2
+    // launch order (see above): CTAs resident at the same time are spatial neighbours and
+    // re-read each other's halos from L2
     auto key = [&](const std::vector<int>& p) {
       const auto& c = l.coords[p[0]];
-      return ((uint64_t)c[2] << 42) | morton(c[0], c[1], 0);
+      return ((uint64_t)(aligned ? c[2] / lmax : c[2]) << 42) | morton(c[0], c[1], 0);
     };
     auto order = [&](std::vector<std::vector<int>>& ps) {
       std::stable_sort(ps.begin(), ps.end(), [&](const std::vector<int>& x, const std::vector<int>& y) {
-        if (x.size() != y.size()) return x.size() > y.size();
+        if (!aligned && x.size() != y.size()) return x.size() > y.size();
         return key(x) < key(y);
       });
     };
     order(pens);
-    if (!lmax_force && lmax >= 2) {
-      // wave tail: CTAs start in launch order on S = 4 x #SM slots (the sweep and the
-      // fused residual + restriction run 4 CTAs per SM); the last wave of long pencils
-      // can leave most slots idle.  Split the last k long pencils into 1-block pencils
-      // (launched after all long ones) for the k that minimises the makespan of this
-      // list schedule (cost of a pencil: 16 len + 4 plane steps).  cfg5 level 2 (2768
-      // blocks, 2.3 waves of 2-block pencils): k = 200, sweep 85.4 -> 76.0 us, fused
-      // residual + restriction 77 -> 72 us; graph V-cycle -35 us (0.6 %)
-      const int S = 4 * nsm;
-      auto makespan = [&](const std::vector<int>& lens) {
-        std::priority_queue<long, std::vector<long>, std::greater<long>> q;
-        for (int i = 0; i < S; ++i) q.push(0);
-        long m = 0;
-        for (int L : lens) {
-          const long t = q.top() + 16 * L + 4;
-          q.pop();
-          q.push(t);
-          m = std::max(m, t);
-        }
-        return m;
-      };
+    // wave tail: CTAs start in launch order on the S slots; the last wave of long pencils
+    // can leave most slots idle.  Split the last k pencils into 1-block pencils, launched
+    // last, for the k that minimises the makespan of the list schedule.  cfg5 level 2
+    // (2768 blocks, 2.3 waves of 2-block pencils): k = 200, sweep 85.4 -> 76.0 us, fused
+    // residual + restriction 77 -> 72 us; level 4 (aligned): k = 96 of 6732, sweep 497 ->
+    // 492 us
+    if (!lmax_force && lmax >= 2 && !aligned) {
       int nlong = 0;
       while (nlong < (int)pens.size() && (int)pens[nlong].size() == lmax) ++nlong;
       std::vector<int> base;
@@ -999,6 +1012,39 @@ void build_pencils(mg_handle* h) {
         pens.swap(out);
         order(pens);
       }
+    } else if (!lmax_force && lmax >= 2) {
+      const int n = (int)pens.size();
+      std::vector<int> base;
+      for (auto& p : pens) base.push_back((int)p.size());
+      long best = makespan(base);
+      int bestk = 0;
+      for (int k = 8; k <= std::min(n, 2 * S); k += 8) {
+        std::vector<int> lens(base.begin(), base.begin() + (n - k));
+        for (int i = n - k; i < n; ++i)
+          for (int t = 0; t < base[i]; ++t) lens.push_back(1);
+        const long m = makespan(lens);
+        if (m < best) best = m, bestk = k;
+      }
+      if (bestk > 0) {
+        std::vector<std::vector<int>> out(pens.begin(), pens.begin() + (n - bestk));
+        for (int i = n - bestk; i < n; ++i)
+          for (int b : pens[i]) out.push_back({b});
+        pens.swap(out);
+      }
+    }
+    // every real block in exactly one pencil, each pencil a z-run of one column
+    {
+      std::vector<char> seen(l.nreal, 0);
+      size_t nb = 0;
+      for (auto& p : pens) {
+        if (p.empty() || (int)p.size() > lmax) throw MgError(MG_ERR_STATE, "pencil list: bad length");
+        for (size_t t = 0; t < p.size(); ++t, ++nb) {
+          const auto &c = l.coords[p[t]], &c0 = l.coords[p[0]];
+          if (seen[p[t]]++ || c[0] != c0[0] || c[1] != c0[1] || c[2] != c0[2] + (int)t)
+            throw MgError(MG_ERR_STATE, "pencil list: not a partition into z-runs");
+        }
+      }
+      if (nb != (size_t)l.nreal) throw MgError(MG_ERR_STATE, "pencil list: blocks missing");
     }
     for (auto& p : pens) {
       l.pen_len.push_back((int32_t)p.size());

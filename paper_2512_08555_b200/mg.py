@@ -38,7 +38,7 @@ class MgDesc(C.Structure):
                 ("eta1", C.c_int32), ("eta2", C.c_int32), ("allow_unbounded_refined", C.c_int32),
                 ("n_leaf", C.c_int64), ("leaves", C.POINTER(C.c_int32)), ("pencil_blocks", C.c_int32),
                 ("zsplit", C.c_int32), ("fuse", C.c_int32), ("ncomp", C.c_int32), ("coarse_pruning", C.c_int32),
-                ("staging", C.c_int32), ("ghost_kernel", C.c_int32)]
+                ("staging", C.c_int32), ("ghost_kernel", C.c_int32), ("pencil_order", C.c_int32)]
 
 
 class MgError(RuntimeError):
@@ -178,6 +178,7 @@ class Solver:
         d.ncomp = int(cfg.get("ncomp", 1))
         d.coarse_pruning = int(cfg.get("coarse_pruning", 0))
         d.ghost_kernel = int(cfg.get("ghost_kernel", 0))
+        d.pencil_order = int(cfg.get("pencil_order", 0))
         self.nc = max(1, d.ncomp)
         d.n_leaf = len(lv)
         d.leaves = lv.ctypes.data_as(C.POINTER(C.c_int32))

@@ -9,7 +9,7 @@ from collections import OrderedDict
 import numpy as np
 
 # mg_desc kernel-variant controls: they select GPU kernels only, never the oracle
-VARIANT_KNOBS = ("pencil_blocks", "zsplit", "fuse", "staging", "ghost_kernel", "coarse_pruning")
+VARIANT_KNOBS = ("pencil_blocks", "zsplit", "fuse", "staging", "ghost_kernel", "coarse_pruning", "pencil_order")
 _OCACHE = OrderedDict()
 _OCACHE_MAX = 24
 

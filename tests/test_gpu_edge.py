@@ -110,6 +110,7 @@ def test_variant_controls_rejected():
     lv = Lay.uniform_leaves(C.domain(d))
     assert _err_code(_base(pencil_blocks=5), lv) == MG_ERR_ARG
     assert _err_code(_base(zsplit=3), lv) == MG_ERR_ARG
+    assert _err_code(_base(pencil_order=3), lv) == MG_ERR_ARG
     assert _err_code(_base(fuse=2), lv) == MG_ERR_ARG
 
 
@@ -139,7 +140,8 @@ def test_cauchy_criterion_on_device_matches_oracle():
                                           ("cfg3_64", {"pencil_blocks": 4}), ("ou_uu", {}), ("oo_pp", {}),
                                           ("per_adapt", {}), ("cfg5_small", {}), ("puu1_m6", {}),
                                           ("cfg3_64_m6", {"pencil_blocks": 2}), ("cfg5_small", {"ghost_kernel": 2}),
-                                          ("cfg3_64", {"ghost_kernel": 2}), ("puu1_m6", {"ghost_kernel": 2})])
+                                          ("cfg3_64", {"ghost_kernel": 2}), ("puu1_m6", {"ghost_kernel": 2}),
+                                          ("cfg5_small", {"pencil_blocks": 4, "pencil_order": 2})])
 def test_poisoned_unneeded_ghosts_are_never_read(name, variant):
     """initcheck substitute (compute-sanitizer is closed on this pool): every ghost-block
     node outside the needed halo holds NaN (mg_debug_poison); V-cycles, the composite

@@ -19,11 +19,13 @@ from tests.test_gpu_parity import CYCLE_TOL, OP_TOL, _cfg, _prepared
 LAYOUTS = ["puu2", "cfg3_64", "per_adapt", "cfg2_64"]
 VARIANTS = [dict(pencil_blocks=1, zsplit=1), dict(pencil_blocks=1, zsplit=2), dict(pencil_blocks=2),
             dict(pencil_blocks=3), dict(pencil_blocks=4), dict(pencil_blocks=2, fuse=1), dict(pencil_blocks=2, staging=1),
-            dict(ghost_kernel=1), dict(ghost_kernel=2)]
+            dict(ghost_kernel=1), dict(ghost_kernel=2),
+            # z-aligned chunks in z-major launch order (the automatic choice on levels of >= 24 waves)
+            dict(pencil_blocks=4, pencil_order=2), dict(pencil_blocks=3, pencil_order=2)]
 
 
 def _vid(v):
-    return "-".join(f"{k[0]}{v[k]}" for k in sorted(v))
+    return "-".join(f"{'o' if k == 'pencil_order' else k[0]}{v[k]}" for k in sorted(v))
 
 
 def _with(name, variant, order=None):
@@ -38,7 +40,7 @@ def _with(name, variant, order=None):
 # M = 4 on every layout x variant; M = 6 (k_rb6_pencil, the radius-2 RHS) on the
 # multi-block-pencil variants of two layouts with ghost blocks
 CASES = [(n, v, 4) for n in LAYOUTS for v in VARIANTS] + \
-        [(n, v, 6) for n in ("puu2", "cfg3_64") for v in VARIANTS[1:5]]
+        [(n, v, 6) for n in ("puu2", "cfg3_64") for v in VARIANTS[1:5] + VARIANTS[9:10]]
 
 
 @pytest.mark.gpu
@@ -132,7 +134,8 @@ def test_large_level_parity(name, variant):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("variant", [dict(pencil_blocks=2), dict(pencil_blocks=3), dict(pencil_blocks=4),
-                                     dict(pencil_blocks=1, zsplit=1)],
+                                     dict(pencil_blocks=1, zsplit=1), dict(pencil_blocks=4, pencil_order=2),
+                                     dict(pencil_blocks=2, pencil_order=2)],
                          ids=_vid)
 def test_cfg5_shaped_variants(variant):
     """The 5-level PUU torus layout (cfg5 recipe, reduced) with forced pencil lengths."""

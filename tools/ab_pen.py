@@ -1,0 +1,62 @@
+#!/usr/bin/env python
+"""A/B of pencil-list experiments (env MG_EXP_PEN read by mg_create) on one config.
+
+  python tools/ab_pen.py --cfg cfg5 --settings "" "4,24" "8,24" "4,8" --reps 20
+
+Per setting: per-level stage times of non-graph V-cycles (CUDA events per stage) and the
+graph-launched V-cycle time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="cfg5")
+    ap.add_argument("--settings", nargs="*", default=[""])
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--env", default="MG_EXP_PEN")
+    a = ap.parse_args()
+    import torch
+
+    from paper_2512_08555_b200 import Solver
+    from workloads import configs as C
+    cfg = getattr(C, a.cfg)()
+    dom, leaves, f = C.build(cfg)
+    fd = torch.from_numpy(f).cuda()
+    for rnd in range(2):
+        for st in a.settings:
+            if st:
+                os.environ[a.env] = st
+            else:
+                os.environ.pop(a.env, None)
+            S = Solver(cfg, leaves)
+            S.set_rhs(fd)
+            S.vcycle(2)
+            S.profile(True)
+            S.vcycle(a.reps)
+            torch.cuda.synchronize()
+            pr = S.profile_read()
+            S.profile(False)
+            out = {"setting": st, "round": rnd}
+            for stage in ("smooth", "restrict", "fas", "ghost", "prolong"):
+                ms, n = pr[stage]
+                out[stage + "_us"] = [round(1e3 * m / max(c, 1), 1) for m, c in zip(ms, n)]
+            S.use_graph(True)
+            S.vcycle(3)
+            out["vcycle_graph_ms"] = round(S.time_op(100, 0, a.reps), 4)
+            out["residual"] = S.residual_norm()[1]
+            print(json.dumps(out), flush=True)
+            del S
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
