@@ -37,7 +37,7 @@ def main():
         open(os.path.join(inc, "mg.h"), "wb").write(data)
     else:
         shutil.copy(os.path.join(ROOT, "include", "mg.h"), os.path.join(inc, "mg.h"))
-    flags = [f for f in B.FLAGS if not f.startswith("-I")] + ["-I" + inc]
+    flags = [f for f in B.FLAGS if not f.startswith("-I")] + ["-I" + inc] + os.environ.get("MG_AB_DEFS", "").split()
     objs = []
     procs = []
     for s in B.SOURCES:

@@ -23,8 +23,13 @@ def main():
     ap.add_argument("--settings", nargs="*", default=[""])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--env", default="MG_EXP_PEN")
+    ap.add_argument("--lib", default="", help="libmg.so to load instead of the in-tree one (A/B builds)")
     a = ap.parse_args()
     import torch
+
+    if a.lib:
+        from paper_2512_08555_b200.mg import load_library
+        load_library(a.lib)
 
     from paper_2512_08555_b200 import Solver
     from workloads import configs as C
@@ -45,7 +50,7 @@ def main():
             torch.cuda.synchronize()
             pr = S.profile_read()
             S.profile(False)
-            out = {"setting": st, "round": rnd}
+            out = {"setting": st, "lib": a.lib, "round": rnd}
             for stage in ("smooth", "restrict", "fas", "ghost", "prolong"):
                 ms, n = pr[stage]
                 out[stage + "_us"] = [round(1e3 * m / max(c, 1), 1) for m, c in zip(ms, n)]
