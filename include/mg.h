@@ -121,7 +121,7 @@ typedef struct mg_desc {
                                 fastest measured), 1 TMA tensor copies (cp.async.bulk.tensor, 9
                                 boxes per field and plane) into an mbarrier ring; measured 2.5x
                                 slower on B200; same values bit for bit */
-  int32_t ghost_kernel;      /* c2f ghost boxes: 0 auto (on levels with >= 2048 boxes <= 2 nodes
+  int32_t ghost_kernel;      /* c2f ghost boxes: 0 auto (on levels with >= 1024 boxes <= 2 nodes
                                 thick along some axis, i.e. the layers of the distance-1 halo,
                                 and no exterior chain: those boxes one warp each with the thin
                                 axis interpolated first; every other box one CTA each, x, y, z

@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(GB_NT) k_c2f_box(const int32_t* __restrict__ b
 // the box's coarse taps and the record's 27 coarse block indices (zero outside the
 // coarse level, only reached by unused plane entries).
 // ---------------------------------------------------------------------------------
-constexpr int GT_W = 8;  // warps (boxes) per CTA
+// warps (boxes) per CTA and CTAs per SM at 80 registers: one-warp CTAs fill the SMs most
+// evenly (cfg5 refresh of level 3 / 4, us: 8 x 3: 45.4 / 86.7, 4 x 6: 42.5 / 82.3, 2 x 12:
+// 39.4 / 80.2, 1 x 24: 35.6 / 76.5; 64 registers (8 x 4) spill: 48 / 100)
+constexpr int GT_W = 1, GT_MINB = 24;
 
 template <int I>
 struct GT {
@@ -222,7 +225,7 @@ struct GT {
 };
 
 template <int I>
-__global__ void __launch_bounds__(GT_W * 32, 3) k_c2f_thin(const int32_t* __restrict__ boxes, int nbox, LevelView F,
+__global__ void __launch_bounds__(GT_W * 32, GT_MINB) k_c2f_thin(const int32_t* __restrict__ boxes, int nbox, LevelView F,
                                                         LevelView C, double* __restrict__ ff,
                                                         const double* __restrict__ cf, bool ext_zero) {
   using S = GT<I>;

@@ -875,12 +875,13 @@ void build_ghost_boxes(mg_handle* h) {
           }
     }
     // The warp-per-box kernel (mg_ghost.cu) wins when the level has enough boxes to fill
-    // the GPU with warps (cfg5 levels 2-4: 2 000 - 13 000 boxes); with few boxes, or the
-    // large multi-layer boxes of exterior chains (U1, cfg3), one CTA per box has more
-    // parallelism per box (B200: cfg5 level 1, 800 boxes, 110 vs 90 us; cfg3 747 vs 491
-    // us of ghost fill per V-cycle).  mg_desc.ghost_kernel: 1 never, 2 always.
+    // the GPU with warps (cfg5 levels 2-4: 2 000 - 13 000 boxes; with one-warp CTAs also
+    // cfg5 level 2, 30.6 -> 23.5 us per refresh, and cfg4 level 2, 22.3 -> 20.0 us); with
+    // few boxes (cfg5 level 1, ~800: equal), or the large multi-layer boxes of exterior
+    // chains (U1, cfg3: 102 -> 125 us of ghost fill per refresh chain), one CTA per box has
+    // more parallelism per box.  mg_desc.ghost_kernel: 1 never, 2 always.
     const int nthin = (int)(thin.size() / GBOX_REC);
-    const bool use_thin = h->d.ghost_kernel == 2 || (h->d.ghost_kernel == 0 && !l.ext_chain && nthin >= 2048);
+    const bool use_thin = h->d.ghost_kernel == 2 || (h->d.ghost_kernel == 0 && !l.ext_chain && nthin >= 1024);
     l.gbox_nthin = use_thin ? nthin : 0;
     if (!use_thin) {
       l.gbox_szA = std::max(l.gbox_szA, thin_szA);

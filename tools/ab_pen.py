@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--settings", nargs="*", default=[""])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--env", default="MG_EXP_PEN")
+    ap.add_argument("--cfgset", nargs="*", default=[], help="cfg overrides key=int (mg_desc variant controls)")
     ap.add_argument("--lib", default="", help="libmg.so to load instead of the in-tree one (A/B builds)")
     a = ap.parse_args()
     import torch
@@ -35,6 +36,9 @@ def main():
     from workloads import configs as C
     cfg = getattr(C, a.cfg)()
     dom, leaves, f = C.build(cfg)
+    for kv in a.cfgset:
+        k, v = kv.split("=")
+        cfg[k] = int(v)
     fd = torch.from_numpy(f).cuda()
     for rnd in range(2):
         for st in a.settings:
@@ -50,7 +54,7 @@ def main():
             torch.cuda.synchronize()
             pr = S.profile_read()
             S.profile(False)
-            out = {"setting": st, "lib": a.lib, "round": rnd}
+            out = {"setting": st, "lib": a.lib, "cfgset": a.cfgset, "round": rnd}
             for stage in ("smooth", "restrict", "fas", "ghost", "prolong"):
                 ms, n = pr[stage]
                 out[stage + "_us"] = [round(1e3 * m / max(c, 1), 1) for m, c in zip(ms, n)]
