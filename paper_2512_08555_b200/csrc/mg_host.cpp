@@ -931,10 +931,9 @@ void build_pencils(mg_handle* h) {
     for (size_t a = 0; a < cols.size(); ++a) nruns += run_start(a);
     const bool long_runs = nruns > 0 && l.nreal >= 8 * nruns && l.nghost == 0;
     // automatic length by waves of 1-block pencils (W = nreal / (4 #SM)), measured on cfg5's
-    // levels (graph V-cycle 5.84 -> 5.78 ms): W < 1.75: 1; 1.75 <= W < 8: 2 (level 1,
-    // 1152 blocks: sweep 38.7 -> 34.2 us); 8 <= W < 24: 3 (level 3, 6640 blocks: sweep
-    // 163.7 -> 154.3 us, residual + restriction 154.8 -> 147.9 us); ghost-free levels of
-    // >= 4 waves with long z-runs, and every level of W >= 24: 4.
+    // levels: W <= 1: 1; 1 < W < 8: 2 (below); 8 <= W < 24: 3 (level 3, 6640 blocks:
+    // sweep 163.7 -> 154.3 us, residual + restriction 154.8 -> 147.9 us); ghost-free levels
+    // of >= 4 waves with long z-runs, and every level of W >= 24: 4.
     // Chunking and order.  "Balanced" (W < 24): a z-run of n blocks is cut into
     // ceil(n / lmax) nearly equal pencils, launched longest first, then by the z of the
     // first block and Morton order of (bx, by).  "Aligned" (W >= 24: cfg5 level 4, 23144
@@ -947,92 +946,103 @@ void build_pencils(mg_handle* h) {
     // restriction 495 -> 472 us (profiles/r02_pencil_aligned_ab.jsonl; lengths 3, 5, 6, 8:
     // 503, 491, 497, 508 us).
     const double W = (double)l.nreal / (4.0 * nsm);
-    const int lmax = lmax_force ? lmax_force
-                                : ((W >= 4 && long_runs) || W >= 24 ? 4 : (W >= 8 ? 3 : (W >= 1.75 ? 2 : 1)));
-    const bool aligned = h->d.pencil_order ? h->d.pencil_order == 2 : W >= 24;
     l.pen_blk.clear();
     l.pen_len.clear();
-    l.pen_lmax = lmax;
-    if (l.B != 16) continue;
-    std::vector<std::vector<int>> pens;
-    for (size_t a = 0; aligned && a < cols.size(); ++a) {
-      if (run_start(a) || cols[a][2] % lmax == 0) pens.emplace_back();
-      pens.back().push_back(cols[a][3]);
+    if (l.B != 16) {
+      l.pen_lmax = lmax_force ? lmax_force : 1;
+      continue;
     }
-    for (size_t a = 0; !aligned && a < cols.size();) {
-      size_t b = a + 1;
-      while (b < cols.size() && !run_start(b)) ++b;
-      const int n = (int)(b - a), nchunk = (n + lmax - 1) / lmax;
-      for (int c = 0, pos = 0; c < nchunk; ++c) {
-        const int len = n / nchunk + (c < n % nchunk ? 1 : 0);
-        std::vector<int> p;
-        for (int t = 0; t < len; ++t) p.push_back(cols[a + pos + t][3]);
-        pos += len;
-        pens.push_back(p);
+    // the pencil list for one length / order, and its modelled makespan
+    auto construct = [&](const int lmax, const bool aligned, std::vector<std::vector<int>>& pens) {
+      pens.clear();
+      for (size_t a = 0; aligned && a < cols.size(); ++a) {
+        if (run_start(a) || cols[a][2] % lmax == 0) pens.emplace_back();
+        pens.back().push_back(cols[a][3]);
       }
-      a = b;
-    }
-    // launch order (see above): CTAs resident at the same time are spatial neighbours and
-    // re-read each other's halos from L2
-    auto key = [&](const std::vector<int>& p) {
-      const auto& c = l.coords[p[0]];
-      return ((uint64_t)(aligned ? c[2] / lmax : c[2]) << 42) | morton(c[0], c[1], 0);
-    };
-    auto order = [&](std::vector<std::vector<int>>& ps) {
-      std::stable_sort(ps.begin(), ps.end(), [&](const std::vector<int>& x, const std::vector<int>& y) {
-        if (!aligned && x.size() != y.size()) return x.size() > y.size();
-        return key(x) < key(y);
-      });
-    };
-    order(pens);
-    // wave tail: CTAs start in launch order on the S slots; the last wave of long pencils
-    // can leave most slots idle.  Split the last k pencils into 1-block pencils, launched
-    // last, for the k that minimises the makespan of the list schedule.  cfg5 level 2
-    // (2768 blocks, 2.3 waves of 2-block pencils): k = 200, sweep 85.4 -> 76.0 us, fused
-    // residual + restriction 77 -> 72 us; level 4 (aligned): k = 96 of 6732, sweep 497 ->
-    // 492 us
-    if (!lmax_force && lmax >= 2 && !aligned) {
-      int nlong = 0;
-      while (nlong < (int)pens.size() && (int)pens[nlong].size() == lmax) ++nlong;
+      for (size_t a = 0; !aligned && a < cols.size();) {
+        size_t b = a + 1;
+        while (b < cols.size() && !run_start(b)) ++b;
+        const int n = (int)(b - a), nchunk = (n + lmax - 1) / lmax;
+        for (int c = 0, pos = 0; c < nchunk; ++c) {
+          const int len = n / nchunk + (c < n % nchunk ? 1 : 0);
+          std::vector<int> p;
+          for (int t = 0; t < len; ++t) p.push_back(cols[a + pos + t][3]);
+          pos += len;
+          pens.push_back(p);
+        }
+        a = b;
+      }
+      // launch order (see above): CTAs resident at the same time are spatial neighbours and
+      // re-read each other's halos from L2
+      auto key = [&](const std::vector<int>& p) {
+        const auto& c = l.coords[p[0]];
+        return ((uint64_t)(aligned ? c[2] / lmax : c[2]) << 42) | morton(c[0], c[1], 0);
+      };
+      auto order = [&](std::vector<std::vector<int>>& ps) {
+        std::stable_sort(ps.begin(), ps.end(), [&](const std::vector<int>& x, const std::vector<int>& y) {
+          if (!aligned && x.size() != y.size()) return x.size() > y.size();
+          return key(x) < key(y);
+        });
+      };
+      order(pens);
       std::vector<int> base;
       for (auto& p : pens) base.push_back((int)p.size());
       long best = makespan(base);
-      int bestk = 0;
-      for (int k = 1; k <= std::min(nlong, 2 * S); ++k) {
-        std::vector<int> lens(base.begin(), base.begin() + (nlong - k));
-        for (int i = 0; i < k * lmax; ++i) lens.push_back(1);
-        for (int i = nlong; i < (int)base.size(); ++i) lens.push_back(base[i]);
-        std::stable_sort(lens.begin(), lens.end(), std::greater<int>());
-        const long m = makespan(lens);
-        if (m < best) best = m, bestk = k;
-      }
-      if (bestk > 0) {
-        std::vector<std::vector<int>> out(pens.begin(), pens.begin() + (nlong - bestk));
-        for (int i = nlong - bestk; i < (int)pens.size(); ++i)
-          for (int b : pens[i]) out.push_back({b});
-        pens.swap(out);
-        order(pens);
-      }
-    } else if (!lmax_force && lmax >= 2) {
+      // wave tail: CTAs start in launch order on the S slots; the last wave of long pencils
+      // can leave most slots idle.  Split the last k pencils into 1-block pencils, launched
+      // last, for the k that minimises the makespan of the list schedule.  cfg5 level 2
+      // (2768 blocks, 2.3 waves of 2-block pencils): k = 200, sweep 85.4 -> 76.0 us, fused
+      // residual + restriction 77 -> 72 us; level 4 (aligned): k = 96 of 6732, sweep 497 ->
+      // 492 us
+      if (lmax_force || lmax < 2) return best;
       const int n = (int)pens.size();
-      std::vector<int> base;
-      for (auto& p : pens) base.push_back((int)p.size());
-      long best = makespan(base);
       int bestk = 0;
-      for (int k = 8; k <= std::min(n, 2 * S); k += 8) {
-        std::vector<int> lens(base.begin(), base.begin() + (n - k));
-        for (int i = n - k; i < n; ++i)
-          for (int t = 0; t < base[i]; ++t) lens.push_back(1);
-        const long m = makespan(lens);
-        if (m < best) best = m, bestk = k;
+      if (!aligned) {
+        int nlong = 0;
+        while (nlong < n && (int)pens[nlong].size() == lmax) ++nlong;
+        for (int k = 1; k <= std::min(nlong, 2 * S); ++k) {
+          std::vector<int> lens(base.begin(), base.begin() + (nlong - k));
+          for (int i = 0; i < k * lmax; ++i) lens.push_back(1);
+          for (int i = nlong; i < n; ++i) lens.push_back(base[i]);
+          std::stable_sort(lens.begin(), lens.end(), std::greater<int>());
+          const long m = makespan(lens);
+          if (m < best) best = m, bestk = k;
+        }
+        if (bestk > 0) {
+          std::vector<std::vector<int>> out(pens.begin(), pens.begin() + (nlong - bestk));
+          for (int i = nlong - bestk; i < n; ++i)
+            for (int b : pens[i]) out.push_back({b});
+          pens.swap(out);
+          order(pens);
+        }
+      } else {
+        for (int k = 8; k <= std::min(n, 2 * S); k += 8) {
+          std::vector<int> lens(base.begin(), base.begin() + (n - k));
+          for (int i = n - k; i < n; ++i)
+            for (int t = 0; t < base[i]; ++t) lens.push_back(1);
+          const long m = makespan(lens);
+          if (m < best) best = m, bestk = k;
+        }
+        if (bestk > 0) {
+          std::vector<std::vector<int>> out(pens.begin(), pens.begin() + (n - bestk));
+          for (int i = n - bestk; i < n; ++i)
+            for (int b : pens[i]) out.push_back({b});
+          pens.swap(out);
+        }
       }
-      if (bestk > 0) {
-        std::vector<std::vector<int>> out(pens.begin(), pens.begin() + (n - bestk));
-        for (int i = n - bestk; i < n; ++i)
-          for (int b : pens[i]) out.push_back({b});
-        pens.swap(out);
-      }
-    }
+      return best;
+    };
+    const bool aligned = h->d.pencil_order ? h->d.pencil_order == 2 : W >= 24;
+    // W <= 1: one wave of 1-block pencils (20 plane steps); 1 < W < 8: 2 (one wave of 36 steps
+    // instead of two of 20 for W <= 2: cfg4 levels 1 and 2, 768 and 936 blocks, sweeps 31.0 ->
+    // 27.6 and 36.5 -> 32.0 us, V-cycle 0.710 -> 0.674 ms; cfg5 level 1, 1152 blocks, 38.7 ->
+    // 34.3 us).  Choosing among 1, 2, 3 by the makespan model alone picked 3 for cfg3's 4096
+    // blocks: 105.7 vs 102.0 us, so the measured thresholds stay.
+    const int lmax = lmax_force ? lmax_force
+                                : ((W >= 4 && long_runs) || W >= 24 ? 4 : (W >= 8 ? 3 : (W > 1.0 ? 2 : 1)));
+    std::vector<std::vector<int>> pens;
+    construct(lmax, aligned, pens);
+    l.pen_lmax = lmax;
     // every real block in exactly one pencil, each pencil a z-run of one column
     {
       std::vector<char> seen(l.nreal, 0);
