@@ -693,6 +693,21 @@ void build_ghosts(mg_handle* h) {
     }
   }
 
+  // f2c lists in ascending destination order (independent copies: any order gives the same
+  // values): consecutive threads of k_copy_list then touch neighbouring coarse nodes and the
+  // even fine nodes under them, so the 8-byte accesses share 32-byte sectors (cfg5 level-4
+  // refresh 76.6 -> 75.3 us)
+  for (int j = 1; j < nlev; ++j) {
+    Level& F = h->L[j];
+    std::vector<size_t> perm(F.inj_dst.size());
+    for (size_t e = 0; e < perm.size(); ++e) perm[e] = e;
+    std::sort(perm.begin(), perm.end(), [&](size_t a, size_t b) { return F.inj_dst[a] < F.inj_dst[b]; });
+    std::vector<int32_t> d2(perm.size()), s2(perm.size());
+    for (size_t e = 0; e < perm.size(); ++e) d2[e] = F.inj_dst[perm[e]], s2[e] = F.inj_src[perm[e]];
+    F.inj_dst.swap(d2);
+    F.inj_src.swap(s2);
+  }
+
   // Composed injection lists of the exterior-chain refresh of level m (reading U1): the
   // lists m, m-1, …, 1 are applied in that order, so a level-j source that list j+1
   // (j+1 <= m) injects from level j+1 is the same value as that level-(j+1) node; follow
