@@ -233,3 +233,31 @@ def test_adaptive_fullsize_converges_sampled_residual(name):
     u = s.get_solution().cpu().numpy()
     r, fmax, used = _sampled_residual(cfg, leaves, f, u, rng, nsamp=600)
     assert used > 200 and r <= cfg["tol"] * fmax, (r, fmax)
+
+
+@pytest.mark.gpu
+def test_cfg5_fullsize_production_equals_parity_tested_variants():
+    """BASELINE's full size, in the launch configuration bench.py times (automatic kernel
+    variants, CUDA-graph V-cycles): every leaf value after 3 V-cycles equals, up to rounding
+    order, that of the forced variants the small-layout parity suite compares with the oracle
+    element by element (balanced 2-block pencils, CTA-per-box ghost kernel, unfused residual
+    and restriction, plain 3-D coarse transform).  On cfg5 the automatic choice is z-aligned
+    4-block pencils with the wave-tail split on level 4, 3- and 2-block pencils with the tail
+    split below, the warp-per-box ghost kernel on levels 2-4 and the pruned coarse solve."""
+    cfg = C.cfg5()
+    dom, leaves, f = C.build(cfg)
+    s = _solver(cfg, leaves, f)
+    s.use_graph(True)
+    s.vcycle(3)
+    u_auto = s.get_solution().cpu().numpy()
+    r_auto = s.residual_norm()[1]
+    del s
+    forced = dict(cfg, pencil_blocks=2, pencil_order=1, ghost_kernel=1, fuse=1, coarse_pruning=1)
+    s = _solver(forced, leaves, f)
+    s.vcycle(3)
+    u_forced = s.get_solution().cpu().numpy()
+    r_forced = s.residual_norm()[1]
+    scale = np.abs(u_forced).max()
+    assert np.isfinite(u_auto).all() and scale > 0
+    assert np.abs(u_auto - u_forced).max() <= 1e-11 * scale, np.abs(u_auto - u_forced).max() / scale
+    assert abs(r_auto - r_forced) <= 1e-6 * r_forced
