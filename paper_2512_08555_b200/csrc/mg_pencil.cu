@@ -768,7 +768,8 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
       const int slot = (z + 1) % R;
 #pragma unroll
       for (int d = 0; d < 2; ++d) {
-        if (!ld_on[d] || (ld_f[d] && (dz != 0 || MODE == 3))) continue;
+        // MODE 1: r is read only on blocks with a covered octant
+        if (!ld_on[d] || (ld_f[d] && (dz != 0 || MODE == 3 || (MODE == 1 && scov[k] == 0)))) continue;
         const int blk = snb[k * 27 + ld_sxy[d] + 9 * (dz + 1)];
         const double* src = (ld_f[d] ? fin : tsrc) + (size_t)blk * PB3 + zl * (PB * PB) + ld_xy[d];
         cpa16(sm + ld_dst[d] + slot * (ld_f[d] ? FP : TP), src);
@@ -791,13 +792,28 @@ __global__ void __launch_bounds__(ResShape<D>::NT, 4)
     c2 = c1; c1 = c0;
     a2 = a1; a1 = a0;
     d2 = d1; d1 = d0;
+    // MODE 1 (FAS): the operator is evaluated only on blocks with a covered octant, so the
+    // in-plane sums of plane s are needed only if the block of plane s-1, s or s+1 has one;
+    // elsewhere the pass just copies u into û (CTA-uniform branches)
+    bool sums = true, lap = true;
+    if (MODE == 1) {
+      const int kl = min(max((s - 1) >> 4, 0), len - 1), km = min(max(s >> 4, 0), len - 1),
+                kh = min(max((s + 1) >> 4, 0), len - 1);
+      sums = (scov[kl] | scov[km] | scov[kh]) != 0;
+      lap = s >= 1 && scov[(s - 1) >> 4] != 0;
+    }
     {
       const double* U = su + ((s + 1) % R) * TP + ci;
       c0 = U[0];
-      a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
-      if (ORDER == 6) d0 = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
+      if (sums) {
+        a0 = (U[-1] + U[1]) + (U[-T] + U[T]);
+        if (ORDER == 6) d0 = (U[-T - 1] + U[-T + 1]) + (U[T - 1] + U[T + 1]);
+      }
     }
-    if (MODE == 3 && s >= 1) {
+    if (MODE == 1 && s >= 1 && !lap) {
+      const int r = s - 1;
+      L.uhat[(size_t)snb[(r >> 4) * 27 + 13] * PB3 + (r & 15) * (PB * PB) + tid] = c1;
+    } else if (MODE == 3 && s >= 1) {
       // f* at plane r = s-1: δ² along x, y from the tile, along z from the carried centres,
       // summed as ((δ²x + δ²y) + δ²z) / 12 (the generic kernel's order)
       const int r = s - 1;
