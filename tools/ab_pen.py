@@ -1,10 +1,14 @@
 #!/usr/bin/env python
-"""A/B of pencil-list experiments (env MG_EXP_PEN read by mg_create) on one config.
+"""A/B timing of host-side scheduling choices and kernel builds on one config (tuning aid).
 
-  python tools/ab_pen.py --cfg cfg5 --settings "" "4,24" "8,24" "4,8" --reps 20
+  python tools/ab_pen.py --cfg cfg5 --cfgset pencil_order=2 pencil_blocks=4   # mg_desc variant controls
+  python tools/ab_pen.py --lib _ab/x/libmg.so                                 # a tools/ab_build.py build
+  python tools/ab_pen.py --env MG_EXP_X --settings "" "1"                     # a temporary getenv switch
+                                                                              # compiled into an experiment
 
-Per setting: per-level stage times of non-graph V-cycles (CUDA events per stage) and the
-graph-launched V-cycle time.
+Per setting (twice, interleaved): per-level stage times of non-graph V-cycles (CUDA events per
+stage, us per launch, index = level) and the graph-launched V-cycle time.  The library itself
+reads no environment variables; --env only serves experiments that add one temporarily.
 """
 from __future__ import annotations
 
